@@ -1,0 +1,498 @@
+#!/usr/bin/env python
+"""Benchmark: HE conv layers/s (+ batched NTT / key-switch GB/s) on B200.
+
+Default workload (N=1): the server-side HE conv stack of BASELINE config 4
+(ResNet-18 shape, 64x64x3: 20 conv layers incl. 1x1 projections, 47.57 G
+60-bit x 8-bit MACs, 5824 output ciphertexts) at the reference's default
+RLWE parameters (n=2048, 60-bit q). One step = every conv layer of the
+stack once, each on its own seeded ciphertexts resident in HBM.
+`value` = conv layers/s (device-timed, CUDA events). `e2e` = the same stack
+through the public API (conv.conv_proposed) from host numpy ciphertexts,
+host<->device copies inside the timed region. Sub-metrics from config 2
+(N=16384, 4 RNS limbs, 64 ciphertexts): batched NTT and hoisted rotation
+sweep GB/s.
+
+`--impl reference` times the reference's CPU algorithm (the C restatement
+in oracle/, all host threads) on a bounded sample of the same workload.
+
+Run: python bench.py [--gpus N --steps K --warmup W]; for N>1 under
+torch.distributed.run (one process per GPU, weak scaling, no collective on
+the data path).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "HE conv layers/s + NTT/key-switch GB/s as % of B200 roofline vs CPU oracle"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ workload
+
+
+def build_stack(workload: str, seed: int = 4):
+    """Seeded per-layer ciphertexts + K1 plans of every conv layer."""
+    import torch
+
+    from paper_2401_16732_b200 import conv, params, stacks
+
+    P = params.default_params()
+    rng = np.random.default_rng(seed)
+    layers = []
+    for l in stacks.conv_layers(stacks.CONFIGS[workload]()):
+        lay = conv.layout_direct(P, l.H, l.W, l.f_w)
+        n_in = lay.ct_count(l.c_i)
+        w = rng.integers(-127, 128, (l.c_o, l.c_i, l.f_w, l.f_w), dtype=np.int64)
+        spec = conv.ConvLayerSpec(l.H, l.W, l.f_w, l.c_i, l.c_o, w)
+        host = rng.integers(0, P.q, (n_in, 2, P.n), dtype=np.int64)
+        plan = conv.conv_plan(spec, lay, P)
+        layers.append({
+            "layer": l, "layout": lay, "spec": spec, "plan": plan, "host": host,
+            "dev": torch.from_numpy(host).cuda(),
+            "out": torch.empty((plan.n_out, 2, P.n), dtype=torch.int64, device="cuda"),
+            "macs": plan.n_out * plan.K * 2 * P.n,
+            "bytes": 8 * 2 * P.n * (n_in + plan.n_out) + 2 * plan.c_o * plan.K,
+        })
+    return P, layers
+
+
+def flush_l2(buf):
+    buf.add_(1)  # 256 MiB write, > 126 MB L2 (outside the timed events)
+
+
+def run_peaks():
+    """Measured integer-pipe peaks (register-resident micro-benchmarks)."""
+    import torch
+
+    from paper_2401_16732_b200 import _native, device
+
+    sink = torch.zeros(4, dtype=torch.int64, device="cuda")
+    st = device.stream()
+    blocks, threads = 148 * 8, 256
+    res = {}
+    for name, call, per in (
+        ("imad_wide", lambda it: _native.call("fhe_peak_imad_wide", blocks, threads, it, sink.data_ptr(), st), 16),
+        ("butterfly", lambda it: _native.call("fhe_peak_butterfly", blocks, threads, it, 1152921486375014401,
+                                              sink.data_ptr(), st), 8),
+    ):
+        call(64)
+        torch.cuda.synchronize()
+        best = 0.0
+        for it in (4096, 8192):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            call(it)
+            e1.record()
+            torch.cuda.synchronize()
+            ops = blocks * threads * it * per
+            best = max(best, ops / (e0.elapsed_time(e1) * 1e-3))
+        res[name] = best
+    return res
+
+
+def time_steps(fn, steps, warmup, flush_buf=None):
+    """Per-step CUDA-event timing on torch's current stream (the kernels' stream)."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(steps):
+        if flush_buf is not None:
+            flush_l2(flush_buf)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def cpu_baseline(P, layers, threads: int, budget_s: float = 12.0):
+    """C oracle (oracle/conv_oracle.c) on a bounded sample: per layer the
+    first `threads` output units, extrapolated to the full layer."""
+    lib = ctypes.CDLL(str(ROOT / "oracle" / "liboracle.so"))
+    lib.oracle_conv.restype = ctypes.c_int
+    total = 0.0
+    sampled_units = 0
+    t_start = time.perf_counter()
+    for L in layers:
+        plan = L["plan"]
+        w = plan.w.cpu().numpy().astype(np.int16)
+        src = plan.src.cpu().numpy().astype(np.int32)
+        step = plan.step.cpu().numpy().astype(np.int32)
+        host = np.ascontiguousarray(L["host"]).view(np.uint64)
+        units = min(plan.n_out, threads)
+        out = np.zeros((units, 2, P.n), dtype=np.uint64)
+        t0 = time.perf_counter()
+        rc = lib.oracle_conv(ctypes.c_uint64(P.q), P.n, host.ctypes.data, host.shape[0], w.ctypes.data, plan.c_o,
+                             plan.K, src.ctypes.data, step.ctypes.data, plan.frags, plan.fstride, out.ctypes.data,
+                             threads, units)
+        dt = time.perf_counter() - t0
+        assert rc == 0
+        total += dt * plan.n_out / units
+        sampled_units += units
+    return total, sampled_units
+
+
+# ------------------------------------------------------- config-2 sweep
+
+
+def sub_benchmarks(steps, warmup, hbm):
+    """Config 2 at N=16384, L=4 limbs, B=64 ciphertexts: NTT fwd/inv and the
+    hoisted rotation sweep (steps 1,2,4..N/4) — GB/s of algorithmic bytes."""
+    import torch
+
+    from paper_2401_16732_b200 import _native, device, params, ring
+
+    N, L, B = 16384, 4, 64
+    p = params.find_plaintext_modulus(N)
+    limbs = params.limb_primes(N, p, L)
+    rng = np.random.default_rng(2)
+    x = np.stack([rng.integers(0, q, (B, 2, N), dtype=np.int64) for q in limbs], axis=1)  # [B][L][2][N]
+    t = torch.from_numpy(x).cuda()
+    out = torch.empty_like(t)
+    flush = torch.empty(2**25, dtype=torch.int64, device="cuda")
+    plans = device.plan_array(N, limbs)
+    rows = B * L * 2
+    st = device.stream()
+    res = {}
+    for name, fn in (("ntt_forward", "fhe_ntt_forward"), ("ntt_inverse", "fhe_ntt_inverse")):
+        ms = time_steps(lambda: _native.call(fn, plans, L, B, 2, t.data_ptr(), out.data_ptr(), st), steps, warmup, flush)
+        avg = sum(ms) / len(ms) * 1e-3
+        gbs = rows * N * 16 / avg / 1e9
+        res[name] = {"gbs": round(gbs, 1), "ms": round(avg * 1e3, 4), "frac_hbm": round(gbs / hbm, 3),
+                     "rows": rows, "N": N}
+    # rotation sweep: iNTT(c1) + l digit NTTs once (hoisted), then K4 per step
+    T, l = 16, 4
+    rsteps = [1 << i for i in range(N.bit_length() - 2)]  # 1 .. N/4
+    keys = {s: torch.from_numpy(np.stack([rng.integers(0, q, (l, 2, N), dtype=np.int64) for q in limbs])).cuda()
+            for s in rsteps}
+    c1 = t[:, :, 1].contiguous()
+    coeff = torch.empty_like(c1)
+    dig = torch.empty((B, L, l, N), dtype=torch.int64, device="cuda")
+    rot = torch.empty((B, L, 2, N), dtype=torch.int64, device="cuda")
+    mods = _native.u64_array(limbs)
+
+    def sweep():
+        _native.call("fhe_ntt_inverse", plans, L, B, 1, c1.data_ptr(), coeff.data_ptr(), st)
+        _native.call("fhe_ntt_forward_digits", plans, L, B, coeff.data_ptr(), dig.data_ptr(), T, l, st)
+        for s in rsteps:
+            _native.call("fhe_keyswitch_apply", mods, L, B, N, t.data_ptr(), dig.data_ptr(), keys[s].data_ptr(), l,
+                         pow(3, s, 2 * N), rot.data_ptr(), st)
+
+    ms = time_steps(sweep, max(2, steps // 2), warmup, flush)
+    avg = sum(ms) / len(ms) * 1e-3
+    ct_limbs = B * L
+    # per rotation: read c0 + l digit rows (gather) + write 2 rows; keys once per batch
+    alg = len(rsteps) * (ct_limbs * 8 * N * (1 + l + 2) + L * 2 * l * 8 * N) + ct_limbs * 8 * N * (2 + 2 * l)
+    gbs = alg / avg / 1e9
+    res["rotation_sweep"] = {"gbs": round(gbs, 1), "ms": round(avg * 1e3, 3), "frac_hbm": round(gbs / hbm, 3),
+                             "rotations": len(rsteps) * B, "rot_per_s": round(len(rsteps) * B / avg, 1),
+                             "N": N, "L": L, "B": B, "T": T}
+    return res
+
+
+# ---------------------------------------------------------------- main
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config4", choices=["config1", "config3", "config4", "config5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    hbm, hbm_kind = _peaks()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        return reference_arm(args, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    from paper_2401_16732_b200 import _native, conv
+
+    P, layers = build_stack(args.workload, seed=4 + rank)
+    flush = torch.empty(2**25, dtype=torch.int64, device="cuda")  # 256 MiB
+
+    def step():
+        for L in layers:
+            L["plan"].run(L["dev"], L["out"])
+
+    peaks = run_peaks() if rank == 0 else {}
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = _native.launch_count()
+    torch.cuda.synchronize()
+    # per-layer events inside the timed region (dominant-kernel roofline)
+    layer_ms = np.zeros(len(layers))
+    step_ms = []
+    for _ in range(args.steps):
+        flush_l2(flush)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
+        evs[0].record()
+        for i, L in enumerate(layers):
+            L["plan"].run(L["dev"], L["out"])
+            evs[i + 1].record()
+        step_ms.append(evs)
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    per_step = []
+    for evs in step_ms:
+        d = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(layers))]
+        layer_ms += d
+        per_step.append(sum(d))
+    total_ms = sum(per_step)
+    t_max = total_ms
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    n_layers = len(layers)
+    value = world * n_layers * args.steps / (t_max * 1e-3)
+    ms_per_step = t_max / args.steps
+
+    result = None
+    if rank == 0:
+        macs = sum(L["macs"] for L in layers)
+        alg_bytes = sum(L["bytes"] for L in layers)
+        k1_s = layer_ms.sum() / args.steps * 1e-3
+        achieved_tmac = macs / k1_s / 1e12
+        peak_tmac = peaks["imad_wide"] / 2 / 1e12  # 2 IMAD.WIDE per 60-bit x 8-bit MAC
+        result = {
+            "metric": METRIC, "value": round(value, 3), "unit": "conv layers/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 mod q (60-bit) x s8",
+            "data": "synthetic: seeded uniform ciphertexts mod q, seeded int weights in [-127,127]",
+            "config": {"workload": f"{args.workload}: ResNet-18 64x64x3 server-side HE conv stack"
+                       if args.workload == "config4" else args.workload,
+                       "conv_layers": n_layers, "macs_60x8": macs, "n": P.n, "q_bits": P.q.bit_length(),
+                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "int", "kernel": "conv_flash_kernel (K1, IMAD.WIDE)",
+                         "achieved": round(achieved_tmac, 4), "peak": round(peak_tmac, 4), "unit": "TMAC60/s",
+                         "frac": round(achieved_tmac / peak_tmac, 4),
+                         "peak_source": "measured here: fhe_peak_imad_wide (register-resident mad.wide.s32)/2",
+                         "hbm_achieved_gbs": round(alg_bytes / k1_s / 1e9, 1), "hbm_peak_gbs": hbm,
+                         "hbm_peak_source": hbm_kind, "traffic": None},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "peaks_measured": {k: v for k, v in peaks.items()},
+            "per_layer_ms": {L["layer"].name: round(float(m) / args.steps, 4) for L, m in zip(layers, layer_ms)},
+        }
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and not args.no_e2e:
+        result["e2e"] = e2e_arm(P, layers, max(2, args.steps // 4), n_layers)
+    if rank == 0 and not args.no_sub:
+        result["sub"] = sub_benchmarks(max(4, args.steps // 2), args.warmup, hbm)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        est_s, units = cpu_baseline(P, layers, threads)
+        result["cpu_baseline"] = {
+            "value": round(n_layers / est_s, 5), "unit": "conv layers/s", "cores": threads, "kind": "port",
+            "sample": f"oracle/conv_oracle.c, first {threads} output ciphertexts of each layer "
+                      f"({units} units total), extrapolated per layer to the full stack",
+        }
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_arm(P, layers, steps, n_layers):
+    """conv.conv_proposed through the public API from host numpy ciphertexts:
+    H2D of every layer input and D2H of every output inside the timed region."""
+    import torch
+
+    from paper_2401_16732_b200 import bfv, conv
+    from paper_2401_16732_b200.ring import Domain, ModPoly
+
+    def host_tensor(L):
+        cts = [bfv.Ciphertext(ModPoly(c[0], P.q), ModPoly(c[1], P.q), bfv.Encoding.DIRECT, Domain.COEFF)
+               for c in L["host"]]
+        return conv.PackedTensor(cts, L["layout"], L["spec"].c_i)
+
+    inputs = [host_tensor(L) for L in layers]
+    h2d = sum(L["host"].nbytes for L in layers)
+    d2h = sum(L["plan"].n_out * 2 * P.n * 8 for L in layers)
+
+    def run():
+        for L, x in zip(layers, inputs):
+            y = conv.conv_proposed(x, L["spec"], P)
+            y.cts[0].c0.coeffs  # one bulk D2H of the layer's output stack
+
+    run()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        for x in inputs:  # fresh host-resident ciphertexts each step (no cached device copies)
+            for ct in x.cts:
+                ct.c0.coeffs = ct.c0.coeffs
+                ct.c1.coeffs = ct.c1.coeffs
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    avg = sum(times) / len(times)
+    return {"value": round(n_layers / avg, 3), "unit": "conv layers/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(avg * 1e3, 3),
+            "api": "paper_2401_16732_b200.conv.conv_proposed (host numpy in, host numpy out)"}
+
+
+def reference_arm(args, world):
+    """The reference's CPU path (oracle/conv_oracle.c restatement, all host
+    threads) on a bounded sample of the same stack, same metric."""
+    import torch  # noqa: F401  (only for the ConvPlan host arrays, built on CPU below)
+
+    from paper_2401_16732_b200 import conv, params, stacks
+
+    P = params.default_params()
+    rng = np.random.default_rng(4)
+    lib = ctypes.CDLL(str(ROOT / "oracle" / "liboracle.so"))
+    threads = os.cpu_count() or 1
+    layers = []
+    for l in stacks.conv_layers(stacks.CONFIGS[args.workload]()):
+        lay = conv.layout_direct(P, l.H, l.W, l.f_w)
+        w = rng.integers(-127, 128, (l.c_o, l.c_i, l.f_w, l.f_w), dtype=np.int64)
+        host = rng.integers(0, P.q, (lay.ct_count(l.c_i), 2, P.n), dtype=np.int64).view(np.uint64)
+        taps = l.f_w * l.f_w
+        j = np.repeat(np.arange(l.c_i), taps)
+        t = np.tile(np.arange(taps), l.c_i)
+        steps = conv._tap_steps(lay, l.f_w)
+        if lay.fragmented:
+            src, fs, st = j * lay.frags, 1, steps[t]
+        else:
+            src, fs, st = j // lay.c_n, 0, steps[t] + lay.tile * (j % lay.c_n)
+        layers.append((l, lay, w.reshape(l.c_o, -1).astype(np.int16), src.astype(np.int32), st.astype(np.int32),
+                       fs, host))
+
+    def one_step():
+        est = 0.0
+        for l, lay, w, src, st, fs, host in layers:
+            n_out = l.c_o * lay.frags
+            units = min(n_out, threads)
+            out = np.zeros((units, 2, P.n), dtype=np.uint64)
+            t0 = time.perf_counter()
+            lib.oracle_conv(ctypes.c_uint64(P.q), P.n, host.ctypes.data, host.shape[0], w.ctypes.data, l.c_o,
+                            w.shape[1], src.ctypes.data, st.ctypes.data, lay.frags, fs, out.ctypes.data, threads,
+                            units)
+            est += (time.perf_counter() - t0) * n_out / units
+        return est
+
+    for _ in range(min(args.warmup, 1)):
+        one_step()
+    ests = [one_step() for _ in range(max(1, min(args.steps, 3)))]
+    est = sum(ests) / len(ests)
+    value = len(layers) / est
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "conv layers/s", "n_gpus": world,
+        "steps": len(ests), "warmup": min(args.warmup, 1), "ms_per_step": round(est * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 mod q (60-bit) x s8",
+        "data": "synthetic: seeded uniform ciphertexts mod q, seeded int weights",
+        "config": {"workload": args.workload, "conv_layers": len(layers)},
+        "cpu_baseline": {"value": round(value, 5), "unit": "conv layers/s", "cores": threads, "kind": "port",
+                         "sample": f"first {threads} output ciphertexts per layer, extrapolated to full layers"},
+        "e2e": {"value": round(value, 5), "unit": "conv layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

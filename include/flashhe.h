@@ -1,0 +1,209 @@
+/*
+ * flashhe.h — C ABI of libflashhe.so, the B200 (sm_100a) hot path of the
+ * Flash HE-convolution protocol (arxiv 2401.16732).
+ *
+ * The reference (`/root/reference/pkg/src/privinfer`, pure Python + numpy) has
+ * no FFI layer: its boundary is the Python module API. Each entry point below
+ * replaces one numpy hot loop of that API and is what a maintainer would bind
+ * from `privinfer` (ctypes / cffi) — see INTEGRATION.md. The Python package
+ * `paper_2401_16732_b200` is exactly such a binding.
+ *
+ * Conventions
+ *   - All data pointers are DEVICE pointers (cudaMalloc / torch CUDA memory)
+ *     unless a parameter says "host". Coefficients are uint64 holding the
+ *     reference's int64 values in [0, modulus) bit-for-bit.
+ *   - A "row" is one polynomial of n coefficients, contiguous. Batched calls
+ *     take rows laid out [B][L][P][n]: B ciphertexts, L RNS limbs (independent
+ *     moduli — the reference is single-modulus), P polys per
+ *     ciphertext (2: c0, c1). Row r uses limb (r / P) % L.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream). Every call is
+ *     asynchronous on that stream; errors of the launch itself are reported.
+ *   - Return value: FHE_OK or an FHE_ERR_* code; fhe_last_error() gives the
+ *     message (thread-local). The codes map 1:1 onto the exception types the
+ *     reference raises (errors.py:1-25).
+ *   - No entry point falls back to the CPU.
+ */
+#ifndef FLASHHE_H
+#define FLASHHE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library builds with -fvisibility=hidden */
+#endif
+
+#define FHE_OK 0
+#define FHE_ERR_PARAMETER 1 /* privinfer.errors.ParameterError          (errors.py:4)  */
+#define FHE_ERR_ENCODING 2  /* privinfer.errors.EncodingError           (errors.py:8)  */
+#define FHE_ERR_BUDGET 3    /* privinfer.errors.AccumulatorBudgetError  (errors.py:12) */
+#define FHE_ERR_PROTOCOL 4  /* privinfer.errors.ProtocolError           (errors.py:16) */
+#define FHE_ERR_VALUE 5     /* ValueError: malformed sizes / pointers               */
+#define FHE_ERR_CUDA 6      /* RuntimeError: CUDA launch / runtime failure          */
+
+#define FHE_MAX_LIMBS 8
+#define FHE_MAX_LOGN 17
+
+typedef struct fhe_plan fhe_plan; /* opaque: negacyclic NTT tables of one (n, q) */
+
+/* ---------------------------------------------------------------- misc */
+const char* fhe_last_error(void);
+int fhe_abi_version(void);
+/* number of kernel launches issued by this library since load (instrumentation) */
+uint64_t fhe_launch_count(void);
+
+/* Roofline micro-benchmarks (register-resident, no memory traffic):
+ * blocks*threads*iters*16 IMAD.WIDE (mad.wide.s32), and
+ * blocks*threads*iters*8 Harvey/Shoup forward butterflies mod q. */
+int fhe_peak_imad_wide(int blocks, int threads, int iters, int64_t* sink, void* stream);
+int fhe_peak_butterfly(int blocks, int threads, int iters, uint64_t q, uint64_t* sink,
+                       void* stream);
+
+/* ------------------------------------------------- plans (ring.NttPlan) */
+/* Host-only (no GPU needed). ring.NttPlan._find_root (ring.py:121-127):
+ * first g in [2, 10000) with psi = g^((q-1)/2n), psi^n == q-1. */
+int fhe_find_root(int n, uint64_t q, uint64_t* psi_out);
+/* Host-only: psi_brv / ipsi_brv / n_inv exactly as ring.NttPlan.__init__
+ * (ring.py:96-113). Outputs are host arrays of n entries (n_inv: 1 entry). */
+int fhe_plan_tables_host(int n, uint64_t q, uint64_t* psi_brv, uint64_t* ipsi_brv,
+                         uint64_t* n_inv);
+/* Device plan: tables (value + Shoup companion) uploaded to HBM.
+ * Replaces ring.get_plan / NttPlan.__init__ (ring.py:96-119, 205-212).
+ * Requires q ≡ 1 mod 2n (else FHE_ERR_PARAMETER, ring.py:97-98), q < 2^62. */
+int fhe_plan_create(int n, uint64_t q, fhe_plan** out);
+int fhe_plan_destroy(fhe_plan* plan);
+int fhe_plan_query(const fhe_plan* plan, int* n, uint64_t* q, uint64_t* psi);
+
+/* --------------------------------------------- K2: batched NTT / iNTT */
+/* ring.NttPlan.fwd (ring.py:129-144): natural order in, bit-reversed order
+ * out (out[i] = f(psi^(2*bitrev(i)+1))), canonical [0,q). src may equal dst.
+ * plans: host array of L plan pointers (same n). Rows [B][L][P][n]. */
+int fhe_ntt_forward(const fhe_plan* const* plans, int L, int B, int P,
+                    const uint64_t* src, uint64_t* dst, void* stream);
+/* ring.NttPlan.inv (ring.py:146-162), n^-1 folded into the last stage. */
+int fhe_ntt_inverse(const fhe_plan* const* plans, int L, int B, int P,
+                    const uint64_t* src, uint64_t* dst, void* stream);
+/* Key-switch digit planes, hoisted (bfv.hrot, bfv.py:485-491):
+ * src rows [B][L][n] canonical coefficients; dst rows [B][L][ndig][n] with
+ * dst[b][l][i] = NTT((src[b][l] >> (T*i)) & (2^T - 1)). */
+int fhe_ntt_forward_digits(const fhe_plan* const* plans, int L, int B,
+                           const uint64_t* src, uint64_t* dst, int T, int ndig,
+                           void* stream);
+
+/* -------------------------------------------- K3: elementwise ring ops */
+/* moduli: host array of L moduli (q_l < 2^62). Operand b is broadcast when
+ * Bb == 1 (over ciphertexts) or Pb == 1 (over polys); else Bb == B, Pb == P. */
+#define FHE_OP_ADD 0 /* ring.poly_add    (ring.py:219-223) */
+#define FHE_OP_SUB 1 /* ring.poly_sub    (ring.py:226-230) */
+#define FHE_OP_MUL 2 /* NttPlan.pointwise (ring.py:193-197) */
+int fhe_poly_binary(int op, const uint64_t* moduli, int L, int B, int P, int n,
+                    const uint64_t* a, const uint64_t* b, int Bb, int Pb,
+                    uint64_t* out, void* stream);
+/* ring.poly_neg (ring.py:233-235) */
+int fhe_poly_neg(const uint64_t* moduli, int L, int B, int P, int n,
+                 const uint64_t* a, uint64_t* out, void* stream);
+/* ring.scalar_mul (ring.py:238-243): k_per_limb host array, k < q_l */
+int fhe_poly_scalar_mul(const uint64_t* moduli, int L, int B, int P, int n,
+                        const uint64_t* a, const uint64_t* k_per_limb, uint64_t* out,
+                        void* stream);
+/* ring.monomial_mul (ring.py:279-299): out = a * x^(-shift) (any shift) */
+int fhe_poly_monomial(const uint64_t* moduli, int L, int B, int P, int n,
+                      const uint64_t* a, int64_t shift, uint64_t* out, void* stream);
+/* ring.apply_galois (ring.py:316-334): out = a(x^gpow), gpow odd */
+int fhe_poly_automorphism(const uint64_t* moduli, int L, int B, int P, int n,
+                          const uint64_t* a, uint64_t gpow, uint64_t* out, void* stream);
+/* bfv._delta_times (bfv.py:166-168) then + base:
+ * out = (base + delta * (m mod p)) mod q ; base may be NULL (treated as 0).
+ * m rows are int64 values (any sign). Used by plain_add / encrypt_online. */
+int fhe_poly_add_delta(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
+                       const uint64_t* base, const int64_t* m, uint64_t* out,
+                       void* stream);
+/* bfv.encrypt_private combine step (bfv.py:181):
+ * out = (delta * (m mod p) - as - e) mod q, m and e int64 (e small, signed),
+ * as canonical [0,q) (= iNTT(NTT(a) * s_eval)). */
+int fhe_encrypt_combine(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
+                        const int64_t* m, const uint64_t* as, const int64_t* e,
+                        uint64_t* out, void* stream);
+/* mod-switch a row set into another modulus: out = centered(v mod p) mod q
+ * (bfv.prepare_plaintext lift, bfv.py:351-356) */
+int fhe_poly_lift_centered(uint64_t p, uint64_t q, int R, int n, const int64_t* v,
+                           uint64_t* out, void* stream);
+
+/* ---------------------- ring.WidePoly lazy accumulator (ring.py:347-406) */
+/* lo/hi: int64 [n] limb accumulators (30-bit limbs, reference layout).
+ * accumulate:        lo += (f & (2^30-1)) * scalar ; hi += (f >> 30) * scalar
+ * accumulate_split:  lo += flo * scalar ; hi += fhi * scalar
+ * add_rotated:       (lo,hi) += (olo,ohi) * x^(-shift) (signed, lazy)
+ * finalize:          out = ((hi << 30) + lo) mod q, canonical            */
+int fhe_wide_accumulate(int n, const uint64_t* f, int64_t scalar, int64_t* lo, int64_t* hi,
+                        void* stream);
+int fhe_wide_accumulate_split(int n, const int64_t* flo, const int64_t* fhi, int64_t scalar,
+                              int64_t* lo, int64_t* hi, void* stream);
+int fhe_wide_add_rotated(int n, const int64_t* olo, const int64_t* ohi, int64_t shift,
+                         int64_t* lo, int64_t* hi, void* stream);
+int fhe_wide_finalize(int n, uint64_t q, const int64_t* lo, const int64_t* hi, uint64_t* out,
+                      void* stream);
+
+/* ------------------------------------ K6: decryption rounding + budget */
+/* bfv.decrypt_with_budget (bfv.py:278-293) given the raw phase
+ * u = [c1 s + c0]_q (canonical): m = ((u + delta/2) // delta) mod p and
+ * maxw[r] = max |u - delta * round(u/delta)| over row r (host reads it). */
+int fhe_decrypt_round(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
+                      const uint64_t* u, uint64_t* m_out, uint64_t* maxw_out,
+                      void* stream);
+
+/* ------------------------------------------ K1: Flash convolution core */
+/* Lazy DRot x CMult accumulation with one reduction per coefficient
+ * (conv._proposed_channel conv.py:326-352, _CtAccum conv.py:269-291,
+ * WidePoly ring.py:347-406). For output o in [0,c_o), fragment f in [0,frags),
+ * poly p in {0,1}, coefficient s in [0,n):
+ *   out[o*frags+f][p][s] = ( Σ_k w[o][k] * (in[src_k + f*frag_stride][p] * x^(-step_k))[s]
+ *                           + (p == 0 && bias ? bias_delta[o] * mask[f][s] : 0) ) mod q
+ * step_k in (-n, n). weights int16 [c_o][K] (|w| < 2^15; the reference bounds |w| < 2^8); term_src/term_step int32 [K];
+ * bias_delta [c_o] (Δ·(b mod p) mod q) and bias_mask uint8 [frags][n] may be
+ * NULL. Caller enforces the lazy budget (fhe_conv_check_budget). */
+int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
+                   const int16_t* weights, int c_o, int K, const int32_t* term_src,
+                   const int32_t* term_step, int frags, int frag_stride,
+                   const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
+                   void* stream);
+/* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
+ * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
+int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);
+
+/* -------------------------------------------- K4: hoisted key switching */
+/* Keys to Montgomery form (one-time, at switching-key upload):
+ * rows [B][L][P][n] -> x * 2^64 mod q_l. */
+int fhe_to_montgomery(const uint64_t* moduli, int L, int B, int P, int n,
+                      const uint64_t* a, uint64_t* out, void* stream);
+/* bfv.hrot (bfv.py:467-500) after hoisting: ct rows [B][L][2][n] (EVAL),
+ * digits rows [B][L][ndig][n] (fhe_ntt_forward_digits of iNTT(c1)),
+ * keys_mont rows [L][ndig][2][n] (swk0_i, swk1_i in Montgomery form).
+ * perm(x) = index_of_exp[(exp_at_index[x] * gpow) mod 2n] (ring.py:199-202):
+ *   out[b][l][0][x] = ct[b][l][0][perm x] + Σ_i D_i[perm x] * swk0_i[x]   mod q_l
+ *   out[b][l][1][x] =                       Σ_i D_i[perm x] * swk1_i[x]   mod q_l */
+int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct,
+                        const uint64_t* digits, const uint64_t* keys_mont, int ndig,
+                        uint64_t gpow, uint64_t* out, void* stream);
+
+/* ------------------------------------ K5: x^2+x share arithmetic (act2pc) */
+/* Client share pass, one vectorised pass
+ * over decrypted slots w in [0,p): y = (w^2 + w * 2^f) mod p. */
+int fhe_act_client_square(uint64_t p, int f, int64_t count, const uint64_t* w,
+                          uint64_t* y, void* stream);
+/* Server finalize constant: c = (r^2 - r*2^f + v) mod p,
+ * from r, r_sq, v in [0,p). */
+int fhe_act_server_const(uint64_t p, int f, int64_t count, const uint64_t* r,
+                         const uint64_t* r_sq, const uint64_t* v, uint64_t* c,
+                         void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASHHE_H */

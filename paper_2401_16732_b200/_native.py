@@ -1,0 +1,116 @@
+"""ctypes binding of libflashhe.so (include/flashhe.h) — the only path to compute.
+
+There is deliberately no CPU fallback: if the library or a CUDA device is
+missing, every compute entry point raises. Status codes are mapped to the
+reference's exception types (privinfer/errors.py:1-25).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import AccumulatorBudgetError, EncodingError, ParameterError, ProtocolError
+
+LIB_PATH = Path(__file__).resolve().parent / "libflashhe.so"
+
+FHE_OK = 0
+_ERRORS = {
+    1: ParameterError,
+    2: EncodingError,
+    3: AccumulatorBudgetError,
+    4: ProtocolError,
+    5: ValueError,
+    6: RuntimeError,
+}
+
+OP_ADD, OP_SUB, OP_MUL = 0, 1, 2
+MAX_LIMBS = 8
+
+_u64 = ctypes.c_uint64
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_vp = ctypes.c_void_p
+_PP = ctypes.POINTER(_vp)
+
+# name -> (restype, argtypes); mirrors include/flashhe.h exactly
+SIGNATURES = {
+    "fhe_last_error": (ctypes.c_char_p, []),
+    "fhe_abi_version": (_int, []),
+    "fhe_launch_count": (_u64, []),
+    "fhe_peak_imad_wide": (_int, [_int, _int, _int, _vp, _vp]),
+    "fhe_peak_butterfly": (_int, [_int, _int, _int, _u64, _vp, _vp]),
+    "fhe_find_root": (_int, [_int, _u64, _vp]),
+    "fhe_plan_tables_host": (_int, [_int, _u64, _vp, _vp, _vp]),
+    "fhe_plan_create": (_int, [_int, _u64, _PP]),
+    "fhe_plan_destroy": (_int, [_vp]),
+    "fhe_plan_query": (_int, [_vp, _vp, _vp, _vp]),
+    "fhe_ntt_forward": (_int, [_PP, _int, _int, _int, _vp, _vp, _vp]),
+    "fhe_ntt_inverse": (_int, [_PP, _int, _int, _int, _vp, _vp, _vp]),
+    "fhe_ntt_forward_digits": (_int, [_PP, _int, _int, _vp, _vp, _int, _int, _vp]),
+    "fhe_poly_binary": (_int, [_int, _vp, _int, _int, _int, _int, _vp, _vp, _int, _int, _vp, _vp]),
+    "fhe_poly_neg": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
+    "fhe_poly_scalar_mul": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "fhe_poly_monomial": (_int, [_vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp]),
+    "fhe_poly_automorphism": (_int, [_vp, _int, _int, _int, _int, _vp, _u64, _vp, _vp]),
+    "fhe_poly_add_delta": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp]),
+    "fhe_encrypt_combine": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fhe_poly_lift_centered": (_int, [_u64, _u64, _int, _int, _vp, _vp, _vp]),
+    "fhe_wide_accumulate": (_int, [_int, _vp, _i64, _vp, _vp, _vp]),
+    "fhe_wide_accumulate_split": (_int, [_int, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "fhe_wide_add_rotated": (_int, [_int, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "fhe_wide_finalize": (_int, [_int, _u64, _vp, _vp, _vp, _vp]),
+    "fhe_decrypt_round":(_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp]),
+    "fhe_conv_flash": (
+        _int,
+        [_u64, _int, _vp, _int, _vp, _int, _int, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp],
+    ),
+    "fhe_conv_check_budget": (_int, [_vp, _int, _int]),
+    "fhe_to_montgomery": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
+    "fhe_keyswitch_apply": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _int, _u64, _vp, _vp]),
+    "fhe_act_client_square": (_int, [_u64, _int, _i64, _vp, _vp, _vp]),
+    "fhe_act_server_const": (_int, [_u64, _int, _i64, _vp, _vp, _vp, _vp, _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libflashhe.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(
+                    f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            h = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(h, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = h
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != FHE_OK:
+        msg = lib().fhe_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def u64_array(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (_u64 * len(vals))(*vals)
+
+
+def launch_count() -> int:
+    return int(lib().fhe_launch_count())

@@ -1,0 +1,599 @@
+"""Homomorphic convolution engines on the B200 — drop-in for privinfer/conv.py.
+
+The proposed (Flash) engine, avg_pool and fully_connected all reduce to one
+device primitive, K1 (`fhe_conv_flash`): an exact integer contraction of
+weights against negacyclically shifted input rows, reduced once per output
+coefficient. `ConvPlan` holds the per-layer device operands (int16 weights,
+per-term source ciphertext and DRot step) so repeated calls are one launch.
+
+Tile bookkeeping (TileLayout, packing, channel positions) is host-side and
+follows conv.py:63-238; the conventional HRot+PMult baseline (conv.py:427-597)
+runs on the hoisted key-switch kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _native, bfv, device, ring
+from .bfv import Ciphertext, Encoding
+from .errors import AccumulatorBudgetError, EncodingError, ParameterError
+from .params import RingParams
+from .ring import Domain
+
+MAX_WEIGHT_BITS = 8  # |weight| < 2^8 (conv.py:28)
+CONV_DECOMP_LOG = 4  # baseline switching-key digit width (conv.py:35)
+
+
+@dataclass
+class ConvLayerSpec:
+    height: int
+    width: int
+    f_w: int
+    c_i: int
+    c_o: int
+    weights: np.ndarray  # (c_o, c_i, f_w, f_w) signed ints
+    weight_scale: int = 0
+    bias: np.ndarray | None = None
+
+    def __post_init__(self):
+        taps = self.f_w * self.f_w
+        self.weights = np.asarray(self.weights, dtype=np.int64).reshape(self.c_o, self.c_i, taps)
+        if self.f_w % 2 == 0:
+            raise ParameterError("kernel width must be odd")
+        if self.weights.size and int(np.abs(self.weights).max()) >= 1 << MAX_WEIGHT_BITS:
+            raise ParameterError(f"weights must stay below {MAX_WEIGHT_BITS} bits for lazy reduction")
+        if self.bias is not None:
+            self.bias = np.asarray(self.bias, dtype=np.int64)
+
+
+@dataclass(frozen=True)
+class TileLayout:
+    """How zero-bordered channel tiles occupy ciphertext slots (conv.py:63-110).
+
+    ring: rotation-orbit size (n direct, n/2 batch); units: orbits per
+    ciphertext; c_n: tiles per orbit; frags/frag_len/halo: the split of a
+    tile larger than one orbit into self-contained fragments."""
+
+    n: int
+    height: int
+    width: int
+    pad: int
+    ring: int
+    units: int
+    c_n: int
+    frags: int
+    frag_len: int
+    halo: int
+    stride: int = 1
+
+    @property
+    def w_p(self) -> int:
+        return self.width + 2 * self.pad
+
+    @property
+    def h_p(self) -> int:
+        return self.height + 2 * self.pad
+
+    @property
+    def tile(self) -> int:
+        return self.h_p * self.w_p
+
+    @property
+    def fragmented(self) -> bool:
+        return self.frags > 1
+
+    def units_for(self, channels: int) -> int:
+        return channels * self.frags if self.fragmented else -(-channels // self.c_n)
+
+    def ct_count(self, channels: int) -> int:
+        return -(-self.units_for(channels) // self.units)
+
+    def out_dims(self) -> tuple[int, int]:
+        return self.height // self.stride, self.width // self.stride
+
+
+def _make_layout(n: int, height: int, width: int, f_w: int, ring_slots: int, units: int) -> TileLayout:
+    pad = f_w // 2
+    tile = (height + 2 * pad) * (width + 2 * pad)
+    common = dict(n=n, height=height, width=width, pad=pad, ring=ring_slots, units=units)
+    if tile <= ring_slots:
+        return TileLayout(**common, c_n=ring_slots // tile, frags=1, frag_len=tile, halo=0)
+    halo = pad * (width + 2 * pad + 1)
+    frag_len = ring_slots - 2 * halo
+    if frag_len <= 0:
+        raise ParameterError("ring too small for even one padded row window")
+    return TileLayout(**common, c_n=1, frags=-(-tile // frag_len), frag_len=frag_len, halo=halo)
+
+
+def layout_direct(params: RingParams, height: int, width: int, f_w: int) -> TileLayout:
+    return _make_layout(params.n, height, width, f_w, params.n, 1)
+
+
+def layout_batch(params: RingParams, height: int, width: int, f_w: int) -> TileLayout:
+    return _make_layout(params.n, height, width, f_w, params.n // 2, 2)
+
+
+@dataclass
+class PackedTensor:
+    cts: list[Ciphertext]
+    layout: TileLayout
+    channels: int
+    scale: int = 0
+
+
+# ---------------------------------------------------------------------------
+# slot bookkeeping (host)
+
+
+def _interior(layout: TileLayout, stride: int = 1) -> np.ndarray:
+    """Row-major tile positions of the readable pixels (stride applied)."""
+    h_out, w_out = layout.height // stride, layout.width // stride
+    rows = layout.pad + stride * np.arange(h_out)
+    cols = layout.pad + stride * np.arange(w_out)
+    return (rows[:, None] * layout.w_p + cols[None, :]).reshape(-1)
+
+
+def tile_vector(channel: np.ndarray, layout: TileLayout, p: int) -> np.ndarray:
+    """One channel as a zero-bordered row-major tile, values mod p."""
+    out = np.zeros(layout.tile, dtype=np.int64)
+    out[_interior(layout)] = (np.asarray(channel, dtype=np.int64) % p).reshape(-1)
+    return out
+
+
+def channel_positions(layout: TileLayout, j: int) -> tuple[np.ndarray, np.ndarray]:
+    """(ciphertext index, slot) of channel j's readable values (conv.py:162-177)."""
+    tp = _interior(layout, layout.stride)
+    if layout.fragmented:
+        frag = tp // layout.frag_len
+        unit = j * layout.frags + frag
+        slot = (unit % layout.units) * layout.ring + layout.halo + tp - frag * layout.frag_len
+        return unit // layout.units, slot
+    unit = j // layout.c_n
+    slot = (unit % layout.units) * layout.ring + layout.tile * (j % layout.c_n) + tp
+    return np.full(tp.shape, unit // layout.units, dtype=np.int64), slot
+
+
+def pack_vectors(values: np.ndarray, layout: TileLayout, p: int) -> list[np.ndarray]:
+    """Slot vectors (length n) for a (c, H, W) integer tensor (conv.py:180-197)."""
+    c = len(values)
+    vecs = np.zeros((layout.ct_count(c), layout.n), dtype=np.int64)
+    for j in range(c):
+        tv = tile_vector(values[j], layout, p)
+        if not layout.fragmented:
+            unit = j // layout.c_n
+            start = (unit % layout.units) * layout.ring + layout.tile * (j % layout.c_n)
+            vecs[unit // layout.units, start : start + layout.tile] = tv
+            continue
+        for k in range(layout.frags):
+            unit = j * layout.frags + k
+            base = (unit % layout.units) * layout.ring
+            first = k * layout.frag_len - layout.halo  # tile index of the orbit's slot 0
+            lo, hi = max(first, 0), min(first + layout.ring, layout.tile)
+            vecs[unit // layout.units, base + lo - first : base + hi - first] = tv[lo:hi]
+    return list(vecs)
+
+
+def pack_input(values, params: RingParams, f_w: int, encrypt_fn, batch: bool = False, scale: int = 0) -> PackedTensor:
+    """Zero-bordered tiles, encoded and encrypted ciphertext by ciphertext."""
+    values = np.asarray(values, dtype=np.int64)
+    c, h, w = values.shape
+    layout = (layout_batch if batch else layout_direct)(params, h, w, f_w)
+    encode = bfv.encode_batch if batch else bfv.encode_direct
+    cts = [encrypt_fn(encode(v, params)) for v in pack_vectors(values, layout, params.p)]
+    if batch:
+        cts = [bfv.to_eval(ct, params) for ct in cts]
+    return PackedTensor(cts, layout, c, scale)
+
+
+def unpack(tensor: PackedTensor, sk: bfv.SecretKey, signed: bool = True) -> np.ndarray:
+    """Decrypt (batched on the device) and gather readable slots to (c, H', W')."""
+    params = sk.params
+    m, _ = bfv.decrypt_rows(tensor.cts, sk)
+    if tensor.cts[0].encoding == Encoding.BATCH:
+        ring.get_plan(params.n, params.p)
+        m = ring.ntt_rows(m, params.n, [params.p])
+        slots = m.cpu().numpy()[:, bfv._slot_index(params)]
+    else:
+        slots = m.cpu().numpy()
+    h_out, w_out = tensor.layout.out_dims()
+    out = np.zeros((tensor.channels, h_out * w_out), dtype=np.int64)
+    for j in range(tensor.channels):
+        ci, si = channel_positions(tensor.layout, j)
+        out[j] = slots[ci, si]
+    if signed:
+        out = bfv.centered(out, params.p)
+    return out.reshape(tensor.channels, h_out, w_out)
+
+
+# ---------------------------------------------------------------------------
+# K1 plans
+
+
+def _tap_steps(layout: TileLayout, f_w: int) -> np.ndarray:
+    """DRot step of each tap, row-major: (dy−pad)·W_p + (dx−pad) (conv.py:245-248)."""
+    off = np.arange(f_w) - f_w // 2
+    return (off[:, None] * layout.w_p + off[None, :]).reshape(-1)
+
+
+def _check_budget(weights2d: np.ndarray):
+    """max_o Σ|w| < 2^32 (conv.py:314-319, ring.py:344)."""
+    if weights2d.size == 0:
+        return
+    worst = int(np.abs(weights2d).sum(axis=1).max())
+    if worst >= ring.WEIGHT_BUDGET:
+        raise AccumulatorBudgetError(f"layer needs |weight| sum {worst}, over the lazy accumulation budget")
+
+
+class ConvPlan:
+    """Device operands of one K1 contraction.
+
+    out[o*frags + f][p] = Σ_k w[o, k] · in[src[k] + f·fstride][p] · x^(−step[k])
+                          (+ Δ·bias[o] on the slots of mask[f], c0 only)
+    """
+
+    def __init__(self, q: int, n: int, weights2d: np.ndarray, src: np.ndarray, step: np.ndarray,
+                 frags: int = 1, fstride: int = 0, bias_delta: np.ndarray | None = None,
+                 bias_mask: np.ndarray | None = None):
+        weights2d = np.asarray(weights2d, dtype=np.int64)
+        if weights2d.size and int(np.abs(weights2d).max()) >= 1 << 15:
+            raise ParameterError("K1 weights must fit int16")
+        self.q, self.n = int(q), int(n)
+        self.c_o, self.K = weights2d.shape
+        self.frags, self.fstride = int(frags), int(fstride)
+        step = np.asarray(step, dtype=np.int64)
+        if step.size and (step.max() >= n or step.min() <= -n):
+            raise ParameterError("DRot step outside (-n, n)")
+        dev = device.require_cuda()
+        self.w = torch.from_numpy(weights2d.astype(np.int16)).to(dev)
+        self.src = torch.from_numpy(np.asarray(src, dtype=np.int32)).to(dev)
+        self.step = torch.from_numpy(step.astype(np.int32)).to(dev)
+        self.bias = None if bias_delta is None else torch.from_numpy(np.asarray(bias_delta, dtype=np.uint64).view(np.int64)).to(dev)
+        self.mask = None if bias_mask is None else torch.from_numpy(np.asarray(bias_mask, dtype=np.uint8)).to(dev)
+        self.n_out = self.c_o * self.frags
+
+    def run(self, inp: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """inp: device [n_in, 2, n] -> out [c_o*frags, 2, n]."""
+        inp = inp.contiguous()
+        if out is None:
+            out = torch.empty((self.n_out, 2, self.n), dtype=torch.int64, device=inp.device)
+        _native.call(
+            "fhe_conv_flash", self.q, self.n, inp.data_ptr(), inp.shape[0], self.w.data_ptr(), self.c_o, self.K,
+            self.src.data_ptr(), self.step.data_ptr(), self.frags, self.fstride, device.ptr(self.bias),
+            device.ptr(self.mask), out.data_ptr(), device.stream(),
+        )
+        return out
+
+
+def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> ConvPlan:
+    """K1 operands of conv_proposed for `layer` on `layout`, cached on the layer
+    object (weights are treated as immutable after first use)."""
+    key = (layout, params.fingerprint())
+    cache = layer.__dict__.setdefault("_k1_plans", {})
+    if key in cache:
+        return cache[key]
+    taps = layer.f_w * layer.f_w
+    steps = _tap_steps(layout, layer.f_w)
+    j = np.repeat(np.arange(layer.c_i), taps)
+    t = np.tile(np.arange(taps), layer.c_i)
+    if layout.fragmented:
+        src, fstride, step = j * layout.frags, 1, steps[t]
+    else:
+        src, fstride, step = j // layout.c_n, 0, steps[t] + layout.tile * (j % layout.c_n)
+    out_layout = replace(layout, c_n=1)
+    bias_delta = bias_mask = None
+    if layer.bias is not None and np.any(layer.bias):
+        bias_delta = np.array([params.delta * (int(b) % params.p) % params.q for b in layer.bias], dtype=np.uint64)
+        bias_mask = np.stack([_bias_mask(out_layout, f) for f in range(layout.frags)])
+    plan = ConvPlan(params.q, params.n, layer.weights.reshape(layer.c_o, -1), src, step,
+                    frags=layout.frags, fstride=fstride, bias_delta=bias_delta, bias_mask=bias_mask)
+    cache[key] = plan
+    return plan
+
+
+def _bias_mask(layout: TileLayout, frag: int) -> np.ndarray:
+    """Slots where conv.py:_bias_plaintext (414-424) places the bias value."""
+    mask = np.zeros(layout.n, dtype=np.uint8)
+    tp = _interior(layout)
+    if layout.fragmented:
+        tp = tp[tp // layout.frag_len == frag]
+        mask[layout.halo + tp - frag * layout.frag_len] = 1
+    else:
+        mask[tp] = 1
+    return mask
+
+
+def conv_proposed(x: PackedTensor, layer: ConvLayerSpec, params: RingParams, lazy: bool = True,
+                  workers: int = 1) -> PackedTensor:
+    """Algorithm 1 (conv.py:355-411) as one K1 launch: every output channel
+    and fragment at once, one modular reduction per coefficient. `lazy` and
+    `workers` are accepted for API compatibility; the result is the same
+    canonical ciphertext either way (as in the reference)."""
+    layout = x.layout
+    if (layout.height, layout.width) != (layer.height, layer.width) or layout.pad != layer.f_w // 2:
+        raise ParameterError("tensor layout does not match the layer geometry")
+    if layout.stride != 1:
+        raise ParameterError("convolution input must not carry a pending stride")
+    if x.cts[0].encoding != Encoding.DIRECT:
+        raise EncodingError("proposed convolution needs direct-encoded input")
+    _check_budget(layer.weights.reshape(layer.c_o, -1))
+    plan = conv_plan(layer, layout, params)
+    out = plan.run(bfv.cts_rows(x.cts))
+    cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+    return PackedTensor(cts, replace(layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)
+
+
+def _bias_plaintext(layout: TileLayout, frag: int, value: int, params: RingParams):
+    vec = _bias_mask(layout, frag).astype(np.int64) * (value % params.p)
+    return bfv.encode_direct(vec, params)
+
+
+# ---------------------------------------------------------------------------
+# pooling and fully connected (conv.py:604-668) on K1
+
+
+def avg_pool(x: PackedTensor, k: int, params: RingParams) -> PackedTensor:
+    """k×k sliding sums via DRot taps of weight 1; /k² and the subsample are
+    deferred (stride marker), as conv.py:604-623."""
+    layout = x.layout
+    if layout.height % k or layout.width % k:
+        raise ParameterError(f"pool size {k} does not divide {layout.height}×{layout.width}")
+    if layout.stride != 1:
+        raise ParameterError("pooling input must not carry a pending stride")
+    if layout.fragmented and (k - 1) * (layout.w_p + 1) > layout.halo:
+        raise ParameterError("pool window exceeds the fragment halo")
+    off = np.arange(k)
+    steps = (off[:, None] * layout.w_p + off[None, :]).reshape(-1)
+    plan = ConvPlan(params.q, params.n, np.ones((1, k * k), dtype=np.int64), np.zeros(k * k), steps,
+                    frags=len(x.cts), fstride=1)
+    out = plan.run(bfv.cts_rows(x.cts))
+    cts = bfv.cts_from_rows(out, params.q, x.cts[0].encoding, Domain.COEFF)
+    return PackedTensor(cts, replace(layout, stride=k), x.channels, x.scale)
+
+
+def fully_connected(x: PackedTensor, weights: np.ndarray, params: RingParams, bias: np.ndarray | None = None,
+                    weight_scale: int = 0) -> list[Ciphertext]:
+    """Matrix-vector product: output row o = Σ_v W[o,v]·DRot(ct(v), slot(v)),
+    the dot product landing in slot 0 (conv.py:626-668)."""
+    weights = np.asarray(weights, dtype=np.int64)
+    c_out, v_in = weights.shape
+    if weights.size and int(np.abs(weights).max()) >= 1 << MAX_WEIGHT_BITS:
+        raise ParameterError("fc weights exceed the lazy-reduction bound")
+    pos = [channel_positions(x.layout, j) for j in range(x.channels)]
+    ct_idx = np.concatenate([p[0] for p in pos])
+    slots = np.concatenate([p[1] for p in pos])
+    if len(slots) != v_in:
+        raise ParameterError(f"weight matrix expects {v_in} inputs, tensor has {len(slots)}")
+    _check_budget(weights)
+    bias_delta = bias_mask = None
+    if bias is not None and np.any(bias):
+        bias_delta = np.array([params.delta * (int(b) % params.p) % params.q for b in bias], dtype=np.uint64)
+        bias_mask = np.zeros((1, params.n), dtype=np.uint8)
+        bias_mask[0, 0] = 1
+    plan = ConvPlan(params.q, params.n, weights, ct_idx, slots, bias_delta=bias_delta, bias_mask=bias_mask)
+    out = plan.run(bfv.cts_rows(x.cts))
+    return bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+
+
+def read_scalar_outputs(cts: list[Ciphertext], sk: bfv.SecretKey) -> np.ndarray:
+    """Slot-0 values of per-output ciphertexts, centered."""
+    m, _ = bfv.decrypt_rows(cts, sk)
+    return bfv.centered(m[:, 0].cpu().numpy(), sk.params.p)
+
+
+# ---------------------------------------------------------------------------
+# conventional baseline: HRot + PMult on batch-encoded tiles (conv.py:427-597)
+
+
+def conventional_steps(layer: ConvLayerSpec, params: RingParams) -> list[int]:
+    """Distinct rotation steps the baseline engine needs (conv.py:431-446)."""
+    layout = layout_batch(params, layer.height, layer.width, layer.f_w)
+    taps = _tap_steps(layout, layer.f_w)
+    shifts = [0] if layout.fragmented else range(1 - layout.c_n, layout.c_n)
+    steps = {int((t + d * layout.tile) % layout.ring) for d in shifts for t in taps}
+    steps.discard(0)
+    if not layout.fragmented and layout.units > 1:
+        if max(layout.units_for(layer.c_i), layout.units_for(layer.c_o)) > 1:
+            steps.add(bfv.COLUMN_ROTATION)
+    return sorted(steps)
+
+
+def _uniform_prepared(value: int, params: RingParams) -> bfv.PreparedPlaintext:
+    """Every slot = value: a constant polynomial, whose NTT is constant."""
+    v = int(value) % params.p
+    if v > params.p // 2:
+        v -= params.p
+    return bfv.PreparedPlaintext(np.full(params.n, v % params.q, dtype=np.int64))
+
+
+class _RotCache:
+    """Rotations of the input ciphertexts, hoisted per source ciphertext: the
+    digit NTTs of c1 are computed once and shared by every step."""
+
+    def __init__(self, cts, swks, params):
+        self.cts, self.swks, self.params = cts, swks, params
+        self.T = swks.decomp_log
+        self.l = -(-params.q.bit_length() // self.T)
+        self._digits = {}
+        self._rot = {}
+        self._swap = {}
+
+    def _base(self, b: int, swap: bool) -> Ciphertext:
+        if not swap:
+            return self.cts[b]
+        if b not in self._swap:
+            self._swap[b] = self._apply(self.cts[b], ("in", b), bfv.COLUMN_ROTATION)
+        return self._swap[b]
+
+    def _apply(self, ct: Ciphertext, key, step: int) -> Ciphertext:
+        bfv._check_hrot(ct, step, self.swks)
+        t = bfv.ct_rows(ct).reshape(1, 2, self.params.n)
+        if key not in self._digits:
+            self._digits[key] = bfv.key_digits_rows(t[:, 1], self.params, self.T, self.l)
+        ring._bump("modmul", 2 * self.params.n * self.l)
+        r = bfv.keyswitch_rows(t, self._digits[key], step, self.swks)
+        return bfv._ct_from_pair(r, self.params.q, Encoding.BATCH, Domain.EVAL)
+
+    def get(self, b: int, step: int, swap: bool = False) -> Ciphertext:
+        ring_slots = self.params.n // 2
+        step %= ring_slots
+        key = (b, step, swap)
+        if key not in self._rot:
+            base = self._base(b, swap)
+            self._rot[key] = self._apply(base, ("sw" if swap else "in", b), step) if step else base
+        return self._rot[key]
+
+
+def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.SwitchingKeySet,
+                      params: RingParams) -> PackedTensor:
+    """Baseline: HRot per (tap, channel offset) + PMult by weight plaintexts
+    + HAdd (conv.py:457-564), on the device kernels."""
+    layout = x.layout
+    if x.cts[0].encoding != Encoding.BATCH:
+        raise EncodingError("conventional convolution needs batch-encoded input")
+    if (layout.height, layout.width) != (layer.height, layer.width) or layout.pad != layer.f_w // 2:
+        raise ParameterError("tensor layout does not match the layer geometry")
+    taps = _tap_steps(layout, layer.f_w)
+    n, cpu = params.n, layout.c_n
+    in_cts = x.cts
+    rot = _RotCache(in_cts, swks, params)
+    pt_cache: dict = {}
+
+    def prepared_blocks(bw: np.ndarray) -> bfv.PreparedPlaintext:
+        key = bw.tobytes()
+        if key not in pt_cache:
+            vec = np.zeros(n, dtype=np.int64)
+            for (unit_in, blk), w in np.ndenumerate(bw):
+                start = unit_in * layout.ring + blk * layout.tile
+                vec[start : start + layout.tile] = w % params.p
+            pt_cache[key] = bfv.prepare_plaintext(bfv.encode_batch(vec, params), params)
+        return pt_cache[key]
+
+    def accumulate(acc, term):
+        return term if acc is None else bfv.hadd(acc, term)
+
+    out_cts: list[Ciphertext] = []
+    if layout.fragmented:
+        pairs = -(-layout.frags // layout.units)
+        for oc in range(layer.c_o):
+            for t in range(pairs):
+                acc = None
+                for j in range(layer.c_i):
+                    b = j * pairs + t
+                    for k, step in enumerate(taps):
+                        w = int(layer.weights[oc, j, k])
+                        if w:
+                            acc = accumulate(acc, bfv.pmult(rot.get(b, int(step)), _uniform_prepared(w, params), params))
+                if acc is None:
+                    acc = bfv.cmult(in_cts[0], 0, params)
+                if layer.bias is not None and layer.bias[oc]:
+                    acc = _conv_bias_batch(acc, layout, t, int(layer.bias[oc]), params)
+                out_cts.append(acc)
+    else:
+        units_in = layout.units_for(layer.c_i)
+        units_out = layout.units_for(layer.c_o)
+        swaps = (False, True) if layout.units > 1 and max(units_in, units_out) > 1 else (False,)
+        for o in range(layout.ct_count(layer.c_o)):
+            acc = None
+            for b in range(len(in_cts)):
+                for swap in swaps:
+                    for d in range(1 - cpu, cpu):
+                        for k, step in enumerate(taps):
+                            bw = np.zeros((layout.units, cpu), dtype=np.int64)
+                            for h in range(layout.units):
+                                iu = layout.units * b + (h ^ int(swap))
+                                ou = layout.units * o + h
+                                if iu >= units_in or ou >= units_out:
+                                    continue
+                                for blk in range(max(0, -d), min(cpu, cpu - d)):
+                                    ic, ocn = iu * cpu + blk + d, ou * cpu + blk
+                                    if ic < layer.c_i and ocn < layer.c_o:
+                                        bw[h, blk] = layer.weights[ocn, ic, k]
+                            if not bw.any():
+                                continue
+                            r = rot.get(b, int((step + d * layout.tile) % layout.ring), swap)
+                            acc = accumulate(acc, bfv.pmult(r, prepared_blocks(bw), params))
+            out_cts.append(acc if acc is not None else bfv.cmult(in_cts[0], 0, params))
+        if layer.bias is not None and layer.bias.any():
+            out_cts = _conv_bias_batch_packed(out_cts, layout, layer, params)
+    return PackedTensor(out_cts, layout, layer.c_o, x.scale + layer.weight_scale)
+
+
+def _conv_bias_batch(ct: Ciphertext, layout: TileLayout, pair: int, value: int, params: RingParams):
+    vec = np.zeros(params.n, dtype=np.int64)
+    tp = _interior(layout)
+    for h in range(layout.units):
+        k = pair * layout.units + h
+        if k >= layout.frags:
+            break
+        sel = tp[tp // layout.frag_len == k]
+        vec[h * layout.ring + layout.halo + sel - k * layout.frag_len] = value % params.p
+    return bfv.plain_add(ct, bfv.encode_batch(vec, params), params)
+
+
+def _conv_bias_batch_packed(out_cts, layout: TileLayout, layer: ConvLayerSpec, params: RingParams):
+    tp = _interior(layout)
+    fixed = []
+    for o, ct in enumerate(out_cts):
+        vec = np.zeros(params.n, dtype=np.int64)
+        for h in range(layout.units):
+            for blk in range(layout.c_n):
+                oc = (layout.units * o + h) * layout.c_n + blk
+                if oc >= layer.c_o:
+                    break
+                vec[h * layout.ring + blk * layout.tile + tp] = int(layer.bias[oc]) % params.p
+        fixed.append(bfv.plain_add(ct, bfv.encode_batch(vec, params), params))
+    return fixed
+
+
+# ---------------------------------------------------------------------------
+# storage accounting (conv.py:677-739), host-only
+
+
+def conventional_plaintext_count(layer: ConvLayerSpec, params: RingParams) -> int:
+    layout = layout_batch(params, layer.height, layer.width, layer.f_w)
+    taps = layer.f_w * layer.f_w
+    if layout.fragmented:
+        return layer.c_o * layer.c_i * -(-layout.frags // layout.units) * taps
+    return layout.ct_count(layer.c_o) * layout.ct_count(layer.c_i) * (2 * layout.c_n - 1) * taps
+
+
+def storage_report(layers: list[ConvLayerSpec], params: RingParams, decomp_log: int = CONV_DECOMP_LOG) -> dict:
+    """Server-side bytes of the two conv paths: raw int weights and no keys
+    (proposed) vs weight plaintexts plus switching keys (conventional)."""
+    digits = -(-params.q.bit_length() // decomp_log)
+    steps = set()
+    for layer in layers:
+        steps.update(conventional_steps(layer, params))
+    return {
+        "proposed_weight_bytes": sum(l.c_o * l.c_i * l.f_w * l.f_w for l in layers),
+        "proposed_swk_bytes": 0,
+        "conventional_weight_bytes": sum(conventional_plaintext_count(l, params) for l in layers) * params.n * 8,
+        "conventional_swk_bytes": len(steps) * digits * 2 * params.n * 8,
+    }
+
+
+VGG16_GEOMETRY = [
+    (64, 64, 3, 64), (64, 64, 64, 64),
+    (32, 32, 64, 128), (32, 32, 128, 128),
+    (16, 16, 128, 256), (16, 16, 256, 256), (16, 16, 256, 256),
+    (8, 8, 256, 512), (8, 8, 512, 512), (8, 8, 512, 512),
+    (4, 4, 512, 512), (4, 4, 512, 512), (4, 4, 512, 512),
+]
+
+
+def vgg16_step_set(params: RingParams) -> list[int]:
+    """Rotation steps of a conventional VGG-16 pipeline (unpadded row-major
+    tiles, packed output channels) — the switching-key storage reference."""
+    ring_slots = params.n // 2
+    steps = set()
+    for h, w, _, _ in VGG16_GEOMETRY:
+        steps.update((dy * w + dx) % ring_slots for dy in (-1, 0, 1) for dx in (-1, 0, 1))
+        if h * w <= ring_slots:
+            steps.update(d * h * w % ring_slots for d in range(1, ring_slots // (h * w)))
+    steps.discard(0)
+    return sorted(steps)

@@ -1,0 +1,568 @@
+// elementwise.cu — K3 (pointwise ring ops), K4 apply (hoisted key switch),
+// K5 (x^2+x share arithmetic) and K6 (decryption rounding).
+// All HBM-bound single passes: 128-bit coalesced rows where the access is
+// affine, scalar 64-bit gathers where it is a permutation (DRot, automorphism,
+// eval-domain Galois map).
+#include "common.cuh"
+
+namespace fhe {
+
+static constexpr int kThreads = 256;
+
+static inline unsigned grid_for(int64_t work) {
+  int64_t g = (work + kThreads - 1) / kThreads;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+// row r of [B][L][P] -> (b, l, p)
+struct RowGeom {
+  int L, P, logn;
+  __device__ __forceinline__ void split(int64_t r, int64_t& b, int& l, int& p) const {
+    p = (int)(r % P);
+    int64_t t = r / P;
+    l = (int)(t % L);
+    b = t / L;
+  }
+};
+
+static int log2i(int n) {
+  int lg = 0;
+  while ((1 << lg) < n) ++lg;
+  return lg;
+}
+
+static int check_rows(int L, int B, int P, int n) {
+  if (L < 1 || L > FHE_MAX_LIMBS || B < 0 || P < 1 || n < 2 || (n & (n - 1)))
+    return fail(FHE_ERR_VALUE, "bad row geometry (L=%d B=%d P=%d n=%d)", L, B, P, n);
+  return FHE_OK;
+}
+
+// ------------------------------------------------------------- binary ops
+__global__ void binary_kernel(int op, const ModSet ms, RowGeom g, int B, int Bb, int Pb,
+                              const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                              uint64_t* __restrict__ out, int64_t total2) {
+  int64_t i2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pair index
+  if (i2 >= total2) return;
+  const int64_t idx = 2 * i2;
+  const int64_t r = idx >> g.logn;
+  const int col = (int)(idx & ((1 << g.logn) - 1));
+  int64_t bb;
+  int l, p;
+  g.split(r, bb, l, p);
+  const int64_t rb = ((bb % Bb) * g.L + l) * Pb + (p % Pb);
+  const ModDesc& m = ms.m[l];
+  const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + idx);
+  const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(b + (rb << g.logn) + col);
+  ulonglong2 z;
+  if (op == FHE_OP_ADD) {
+    z.x = csub(x.x + y.x, m.q);
+    z.y = csub(x.y + y.y, m.q);
+  } else if (op == FHE_OP_SUB) {
+    z.x = x.x >= y.x ? x.x - y.x : x.x + m.q - y.x;
+    z.y = x.y >= y.y ? x.y - y.y : x.y + m.q - y.y;
+  } else {
+    z.x = mulmod(x.x, y.x, m);
+    z.y = mulmod(x.y, y.y, m);
+  }
+  *reinterpret_cast<ulonglong2*>(out + idx) = z;
+}
+
+__global__ void neg_kernel(const ModSet ms, RowGeom g, const uint64_t* __restrict__ a,
+                           uint64_t* __restrict__ out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int64_t bb;
+  int l, p;
+  g.split(idx >> g.logn, bb, l, p);
+  const uint64_t v = a[idx];
+  out[idx] = v ? ms.m[l].q - v : 0;
+}
+
+struct Scalars {
+  uint64_t k[FHE_MAX_LIMBS];
+  uint64_t kp[FHE_MAX_LIMBS];  // Shoup companions
+};
+
+__global__ void scalar_kernel(const ModSet ms, RowGeom g, Scalars sc, const uint64_t* __restrict__ a,
+                              uint64_t* __restrict__ out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int64_t bb;
+  int l, p;
+  g.split(idx >> g.logn, bb, l, p);
+  const uint64_t q = ms.m[l].q;
+  out[idx] = csub(shoup_lazy(a[idx], sc.k[l], sc.kp[l], q), q);
+}
+
+// out = a * x^(-shift) mod x^n + 1 (ring.monomial_mul, ring.py:279-299)
+__global__ void monomial_kernel(const ModSet ms, RowGeom g, int64_t s, int flip,
+                                const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
+                                int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int n = 1 << g.logn;
+  const int64_t r = idx >> g.logn;
+  const int i = (int)(idx & (n - 1));
+  int64_t bb;
+  int l, p;
+  g.split(r, bb, l, p);
+  int j = i + (int)s;
+  int neg = flip;
+  if (j >= n) {
+    j -= n;
+    neg ^= 1;
+  }
+  const uint64_t v = a[(r << g.logn) + j];
+  out[idx] = (neg && v) ? ms.m[l].q - v : v;
+}
+
+// out(x) = a(x^gpow) (ring.apply_galois, ring.py:326-334), scatter form
+__global__ void automorphism_kernel(const ModSet ms, RowGeom g, uint64_t gpow,
+                                    const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
+                                    int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int n = 1 << g.logn;
+  const int64_t r = idx >> g.logn;
+  const uint64_t i = (uint64_t)(idx & (n - 1));
+  int64_t bb;
+  int l, p;
+  g.split(r, bb, l, p);
+  const uint64_t e = (i * (gpow % (2ull * n))) % (2ull * n);
+  const uint64_t v = a[idx];
+  const bool neg = e >= (uint64_t)n;
+  out[(r << g.logn) + (e & (n - 1))] = (neg && v) ? ms.m[l].q - v : v;
+}
+
+__global__ void add_delta_kernel(ModDesc mq, uint64_t p, uint64_t delta, const uint64_t* __restrict__ base,
+                                 const int64_t* __restrict__ m, uint64_t* __restrict__ out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int64_t v = m[idx] % (int64_t)p;
+  if (v < 0) v += (int64_t)p;
+  uint64_t dm = delta * (uint64_t)v;  // Δ (p-1) < q (bfv.py:167)
+  uint64_t b = base ? base[idx] : 0;
+  out[idx] = csub(b + dm, mq.q);
+}
+
+// c0 = (Δ (m mod p) - as - e) mod q   (bfv.encrypt_private, bfv.py:181)
+__global__ void encrypt_combine_kernel(ModDesc mq, uint64_t p, uint64_t delta, const int64_t* __restrict__ m,
+                                       const uint64_t* __restrict__ as, const int64_t* __restrict__ e,
+                                       uint64_t* __restrict__ out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int64_t v = m[idx] % (int64_t)p;
+  if (v < 0) v += (int64_t)p;
+  const uint64_t q = mq.q;
+  uint64_t t = csub(delta * (uint64_t)v, q);
+  t = csub(t + q - as[idx], q);
+  const uint64_t er = reduce_i64(e[idx], mq);
+  out[idx] = csub(t + q - er, q);
+}
+
+__global__ void lift_centered_kernel(uint64_t p, uint64_t q, const int64_t* __restrict__ v,
+                                     uint64_t* __restrict__ out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int64_t x = v[idx] % (int64_t)p;
+  if (x < 0) x += (int64_t)p;
+  if (x > (int64_t)(p / 2)) x -= (int64_t)p;  // bfv.centered (bfv.py:156-159)
+  out[idx] = x < 0 ? q - (uint64_t)(-x) : (uint64_t)x;
+}
+
+__global__ void to_mont_kernel(const ModSet ms, RowGeom g, const uint64_t* __restrict__ a,
+                               uint64_t* __restrict__ out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  int64_t bb;
+  int l, p;
+  g.split(idx >> g.logn, bb, l, p);
+  const ModDesc& m = ms.m[l];
+  const uint64_t x = a[idx];
+  out[idx] = redc(x * m.r2, __umul64hi(x, m.r2), m);
+}
+
+// ------------------------------------------------- WidePoly (ring.py:347-406)
+__global__ void wide_acc_kernel(int n, const uint64_t* __restrict__ f, const int64_t* __restrict__ flo,
+                                const int64_t* __restrict__ fhi, int64_t scalar, int64_t* lo, int64_t* hi) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t a, b;
+  if (f) {
+    a = (int64_t)(f[i] & ((1ull << 30) - 1));
+    b = (int64_t)(f[i] >> 30);
+  } else {
+    a = flo[i];
+    b = fhi[i];
+  }
+  // int64 wrap-around like numpy (the budget guard keeps it from happening)
+  lo[i] = (int64_t)((uint64_t)lo[i] + (uint64_t)a * (uint64_t)scalar);
+  hi[i] = (int64_t)((uint64_t)hi[i] + (uint64_t)b * (uint64_t)scalar);
+}
+
+__global__ void wide_rot_kernel(int n, const int64_t* __restrict__ olo, const int64_t* __restrict__ ohi,
+                                int s, int flip, int64_t* lo, int64_t* hi) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int j = i + s, neg = flip;
+  if (j >= n) {
+    j -= n;
+    neg ^= 1;
+  }
+  const uint64_t a = (uint64_t)olo[j], b = (uint64_t)ohi[j];
+  lo[i] = (int64_t)(neg ? (uint64_t)lo[i] - a : (uint64_t)lo[i] + a);
+  hi[i] = (int64_t)(neg ? (uint64_t)hi[i] - b : (uint64_t)hi[i] + b);
+}
+
+__global__ void wide_fin_kernel(int n, ModDesc m, uint64_t w30, uint64_t w30p, const int64_t* __restrict__ lo,
+                                const int64_t* __restrict__ hi, uint64_t* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t l = reduce_i64(lo[i], m), h = reduce_i64(hi[i], m);
+  out[i] = csub(l + csub(shoup_lazy(h, w30, w30p, m.q), m.q), m.q);
+}
+
+// ------------------------------------------------------- K6 decrypt round
+__global__ void decrypt_round_kernel(uint64_t p, uint64_t delta, uint64_t magic, int n,
+                                     const uint64_t* __restrict__ u, uint64_t* __restrict__ mout,
+                                     uint64_t* __restrict__ maxw) {
+  const int64_t r = blockIdx.x;
+  const uint64_t half = delta / 2;
+  uint64_t local = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t x = u[r * n + i] + half;  // (u + Δ//2) // Δ  (bfv.py:288)
+    uint64_t mq = __umul64hi(x, magic);
+    uint64_t rem = x - mq * delta;
+    if (rem >= delta) {
+      ++mq;
+      rem -= delta;
+    }
+    // w = u - Δ m_raw = rem - Δ//2
+    const uint64_t aw = rem >= half ? rem - half : half - rem;
+    local = aw > local ? aw : local;
+    while (mq >= p) mq -= p;  // m_raw <= p + 1 since Δ = q // p
+    mout[r * n + i] = mq;
+  }
+  __shared__ uint64_t red[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t v = __shfl_xor_sync(0xffffffffu, local, o);
+    local = v > local ? v : local;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t mx = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = red[w] > mx ? red[w] : mx;
+    maxw[r] = mx;
+  }
+}
+
+// ------------------------------------------------------------ K5 shares
+__global__ void act_client_kernel(ModDesc mp, uint64_t two_f, const uint64_t* __restrict__ w,
+                                  uint64_t* __restrict__ y, int64_t count) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t x = reduce_u64(w[i], mp);
+  const uint64_t sq = mulmod(x, x, mp);
+  const uint64_t lin = mulmod(x, two_f, mp);
+  y[i] = csub(sq + lin, mp.q);
+}
+
+__global__ void act_server_kernel(ModDesc mp, uint64_t two_f, const uint64_t* __restrict__ r,
+                                  const uint64_t* __restrict__ rsq, const uint64_t* __restrict__ v,
+                                  uint64_t* __restrict__ c, int64_t count) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint64_t p = mp.q;
+  const uint64_t rr = reduce_u64(r[i], mp);
+  const uint64_t lin = mulmod(rr, two_f, mp);
+  uint64_t t = reduce_u64(rsq[i], mp);
+  t = csub(t + p - lin, p);
+  c[i] = csub(t + reduce_u64(v[i], mp), p);
+}
+
+// ------------------------------------------------ K4 hoisted key switching
+// One thread per (position x, limb l, batch chunk): the 2*ndig key words of x
+// stay in registers and are reused by every ciphertext of the chunk (the key
+// is read from HBM once per chunk, not once per ciphertext).
+template <int MAXD>
+__global__ void keyswitch_kernel(const ModSet ms, int logn, int L, int B, int bchunk, int ndig,
+                                 uint64_t gpow, const uint64_t* __restrict__ ct,
+                                 const uint64_t* __restrict__ dig, const uint64_t* __restrict__ keys,
+                                 uint64_t* __restrict__ out) {
+  const int n = 1 << logn;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int l = blockIdx.y;
+  const int b0 = blockIdx.z * bchunk;
+  const int b1 = min(B, b0 + bchunk);
+  const ModDesc m = ms.m[l];
+  // eval_perm (ring.py:199-202): exp_at_index[x] = 2 bitrev(x) + 1
+  const uint32_t e = 2u * brev_bits((uint32_t)x, logn) + 1u;
+  const uint32_t e2 = (uint32_t)(((uint64_t)e * (gpow % (2ull * n))) % (2ull * n));
+  const int src = (int)brev_bits((e2 - 1u) >> 1, logn);
+  uint64_t k0[MAXD], k1[MAXD];
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    if (i < ndig) {
+      k0[i] = keys[((size_t)(l * ndig + i) * 2 + 0) * n + x];
+      k1[i] = keys[((size_t)(l * ndig + i) * 2 + 1) * n + x];
+    }
+  }
+  for (int b = b0; b < b1; ++b) {
+    const size_t crow = ((size_t)b * L + l) * 2;
+    const size_t drow = ((size_t)b * L + l) * ndig;
+    uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      if (i < ndig) {
+        const uint64_t dv = dig[(drow + i) * n + src];
+        mac128(a0l, a0h, dv, k0[i]);
+        mac128(a1l, a1h, dv, k1[i]);
+      }
+    }
+    // Σ_i D_i swk_i < ndig q^2 < q 2^64 (ndig < 2^64/q): one REDC each
+    const uint64_t c0p = ct[crow * n + src];
+    out[crow * n + x] = csub(redc(a0l, a0h, m) + c0p, m.q);
+    out[(crow + 1) * n + x] = redc(a1l, a1h, m);
+  }
+}
+
+}  // namespace fhe
+
+using namespace fhe;
+
+extern "C" {
+
+int fhe_poly_binary(int op, const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a,
+                    const uint64_t* b, int Bb, int Pb, uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  if (op < 0 || op > 2) return fail(FHE_ERR_VALUE, "bad op %d", op);
+  if (!(Bb == 1 || Bb == B) || !(Pb == 1 || Pb == P) || Bb < 1) return fail(FHE_ERR_VALUE, "bad broadcast");
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  const int64_t total2 = (int64_t)B * L * P * n / 2;
+  if (!total2) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  binary_kernel<<<grid_for(total2), kThreads, 0, (cudaStream_t)stream>>>(op, ms, g, B, Bb, Pb, a, b, out, total2);
+  FHE_CHECK_LAUNCH("binary_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_neg(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a, uint64_t* out,
+                 void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  const int64_t total = (int64_t)B * L * P * n;
+  if (!total) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  neg_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, a, out, total);
+  FHE_CHECK_LAUNCH("neg_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_scalar_mul(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a,
+                        const uint64_t* k_per_limb, uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  Scalars sc;
+  for (int l = 0; l < L; ++l) {
+    uint64_t k = k_per_limb[l] % ms.m[l].q;
+    sc.k[l] = k;
+    sc.kp[l] = h_shoup(k, ms.m[l].q);
+  }
+  const int64_t total = (int64_t)B * L * P * n;
+  if (!total) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  scalar_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, sc, a, out, total);
+  FHE_CHECK_LAUNCH("scalar_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_monomial(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a,
+                      int64_t shift, uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  if (a == out) return fail(FHE_ERR_VALUE, "monomial_mul cannot run in place");
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  int64_t s = shift % (2 * (int64_t)n);
+  if (s < 0) s += 2 * (int64_t)n;
+  int flip = s >= n;
+  if (flip) s -= n;
+  const int64_t total = (int64_t)B * L * P * n;
+  if (!total) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  monomial_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, s, flip, a, out, total);
+  FHE_CHECK_LAUNCH("monomial_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_automorphism(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a,
+                          uint64_t gpow, uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  if (!(gpow & 1)) return fail(FHE_ERR_PARAMETER, "Galois element must be odd");
+  if (a == out) return fail(FHE_ERR_VALUE, "automorphism cannot run in place");
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  const int64_t total = (int64_t)B * L * P * n;
+  if (!total) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  automorphism_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, gpow, a, out, total);
+  FHE_CHECK_LAUNCH("automorphism_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_add_delta(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* base,
+                       const int64_t* m, uint64_t* out, void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&q, 1, &ms)) return rc;
+  if (p < 2 || (u128_t)delta * (p - 1) >= q) return fail(FHE_ERR_PARAMETER, "delta*(p-1) must be < q");
+  const int64_t total = (int64_t)R * n;
+  if (total <= 0) return FHE_OK;
+  add_delta_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms.m[0], p, delta, base, m, out, total);
+  FHE_CHECK_LAUNCH("add_delta_kernel");
+  return FHE_OK;
+}
+
+int fhe_encrypt_combine(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const int64_t* m,
+                        const uint64_t* as, const int64_t* e, uint64_t* out, void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&q, 1, &ms)) return rc;
+  if (p < 2 || (u128_t)delta * (p - 1) >= q) return fail(FHE_ERR_PARAMETER, "delta*(p-1) must be < q");
+  const int64_t total = (int64_t)R * n;
+  if (total <= 0) return FHE_OK;
+  encrypt_combine_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms.m[0], p, delta, m, as, e,
+                                                                                   out, total);
+  FHE_CHECK_LAUNCH("encrypt_combine_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_lift_centered(uint64_t p, uint64_t q, int R, int n, const int64_t* v, uint64_t* out,
+                           void* stream) {
+  if (p < 2 || q < p) return fail(FHE_ERR_PARAMETER, "bad moduli for lift");
+  const int64_t total = (int64_t)R * n;
+  if (total <= 0) return FHE_OK;
+  lift_centered_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(p, q, v, out, total);
+  FHE_CHECK_LAUNCH("lift_centered_kernel");
+  return FHE_OK;
+}
+
+int fhe_to_montgomery(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a,
+                      uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  const int64_t total = (int64_t)B * L * P * n;
+  if (!total) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  to_mont_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, a, out, total);
+  FHE_CHECK_LAUNCH("to_mont_kernel");
+  return FHE_OK;
+}
+
+int fhe_wide_accumulate(int n, const uint64_t* f, int64_t scalar, int64_t* lo, int64_t* hi, void* stream) {
+  if (n < 1 || !f || !lo || !hi) return fail(FHE_ERR_VALUE, "bad wide accumulate arguments");
+  wide_acc_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, f, nullptr, nullptr, scalar, lo, hi);
+  FHE_CHECK_LAUNCH("wide_acc_kernel");
+  return FHE_OK;
+}
+
+int fhe_wide_accumulate_split(int n, const int64_t* flo, const int64_t* fhi, int64_t scalar, int64_t* lo,
+                              int64_t* hi, void* stream) {
+  if (n < 1 || !flo || !fhi || !lo || !hi) return fail(FHE_ERR_VALUE, "bad wide accumulate arguments");
+  wide_acc_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, nullptr, flo, fhi, scalar, lo, hi);
+  FHE_CHECK_LAUNCH("wide_acc_kernel");
+  return FHE_OK;
+}
+
+int fhe_wide_add_rotated(int n, const int64_t* olo, const int64_t* ohi, int64_t shift, int64_t* lo, int64_t* hi,
+                         void* stream) {
+  if (n < 1 || !olo || !ohi || !lo || !hi) return fail(FHE_ERR_VALUE, "bad wide rotate arguments");
+  if (olo == lo || ohi == hi) return fail(FHE_ERR_VALUE, "add_rotated source must not alias the accumulator");
+  int64_t s = shift % (2 * (int64_t)n);
+  if (s < 0) s += 2 * (int64_t)n;
+  int flip = s >= n;
+  if (flip) s -= n;
+  wide_rot_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, olo, ohi, (int)s, flip, lo, hi);
+  FHE_CHECK_LAUNCH("wide_rot_kernel");
+  return FHE_OK;
+}
+
+int fhe_wide_finalize(int n, uint64_t q, const int64_t* lo, const int64_t* hi, uint64_t* out, void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&q, 1, &ms)) return rc;
+  if (n < 1 || !lo || !hi || !out) return fail(FHE_ERR_VALUE, "bad wide finalize arguments");
+  const uint64_t w30 = (1ull << 30) % q;
+  wide_fin_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, ms.m[0], w30, h_shoup(w30, q), lo, hi,
+                                                                        out);
+  FHE_CHECK_LAUNCH("wide_fin_kernel");
+  return FHE_OK;
+}
+
+int fhe_decrypt_round(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* u,
+                      uint64_t* m_out, uint64_t* maxw_out, void* stream) {
+  if (R < 0 || n < 1 || delta < 2 || p < 2) return fail(FHE_ERR_VALUE, "bad decrypt arguments");
+  if (q >= (1ull << 62)) return fail(FHE_ERR_PARAMETER, "modulus too large");
+  if (!R) return FHE_OK;
+  const uint64_t magic = ~0ull / delta;
+  decrypt_round_kernel<<<R, 256, 0, (cudaStream_t)stream>>>(p, delta, magic, n, u, m_out, maxw_out);
+  FHE_CHECK_LAUNCH("decrypt_round_kernel");
+  return FHE_OK;
+}
+
+int fhe_act_client_square(uint64_t p, int f, int64_t count, const uint64_t* w, uint64_t* y, void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&p, 1, &ms)) return rc;
+  if (f < 0 || f > 62) return fail(FHE_ERR_VALUE, "bad fraction bits %d", f);
+  if (count <= 0) return FHE_OK;
+  const uint64_t two_f = h_powmod(2, (uint64_t)f, p);
+  act_client_kernel<<<grid_for(count), kThreads, 0, (cudaStream_t)stream>>>(ms.m[0], two_f, w, y, count);
+  FHE_CHECK_LAUNCH("act_client_kernel");
+  return FHE_OK;
+}
+
+int fhe_act_server_const(uint64_t p, int f, int64_t count, const uint64_t* r, const uint64_t* r_sq,
+                         const uint64_t* v, uint64_t* c, void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&p, 1, &ms)) return rc;
+  if (f < 0 || f > 62) return fail(FHE_ERR_VALUE, "bad fraction bits %d", f);
+  if (count <= 0) return FHE_OK;
+  const uint64_t two_f = h_powmod(2, (uint64_t)f, p);
+  act_server_kernel<<<grid_for(count), kThreads, 0, (cudaStream_t)stream>>>(ms.m[0], two_f, r, r_sq, v, c,
+                                                                              count);
+  FHE_CHECK_LAUNCH("act_server_kernel");
+  return FHE_OK;
+}
+
+int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct,
+                        const uint64_t* digits, const uint64_t* keys_mont, int ndig, uint64_t gpow,
+                        uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, 2, n)) return rc;
+  if (ndig < 1 || ndig > 64) return fail(FHE_ERR_VALUE, "bad digit count %d", ndig);
+  if (!(gpow & 1)) return fail(FHE_ERR_PARAMETER, "Galois element must be odd");
+  if (ct == out) return fail(FHE_ERR_VALUE, "keyswitch cannot run in place");
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  for (int l = 0; l < L; ++l)
+    if ((u128_t)ndig * ms.m[l].q >= ((u128_t)1 << 64))
+      return fail(FHE_ERR_PARAMETER, "too many digits for one lazy REDC");
+  if (!B) return FHE_OK;
+  const int bchunk = 8;
+  dim3 grid((n + 127) / 128, L, (B + bchunk - 1) / bchunk);
+  const int logn = log2i(n);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ndig <= 4)
+    keyswitch_kernel<4><<<grid, 128, 0, st>>>(ms, logn, L, B, bchunk, ndig, gpow, ct, digits, keys_mont, out);
+  else if (ndig <= 8)
+    keyswitch_kernel<8><<<grid, 128, 0, st>>>(ms, logn, L, B, bchunk, ndig, gpow, ct, digits, keys_mont, out);
+  else if (ndig <= 16)
+    keyswitch_kernel<16><<<grid, 128, 0, st>>>(ms, logn, L, B, bchunk, ndig, gpow, ct, digits, keys_mont, out);
+  else
+    return fail(FHE_ERR_VALUE, "more than 16 digits unsupported");
+  FHE_CHECK_LAUNCH("keyswitch_kernel");
+  return FHE_OK;
+}
+
+}  // extern "C"

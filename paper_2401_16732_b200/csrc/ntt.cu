@@ -1,0 +1,291 @@
+// ntt.cu — K2: batched negacyclic NTT / iNTT over RNS limbs (sm_100a).
+//
+// Replaces ring.NttPlan.fwd / inv (ring.py:129-162), which run one big-int
+// (`object`) butterfly pass per stage. Semantics kept exactly: forward is
+// Cooley-Tukey with merged twiddles psi_brv[m + j] (natural order in,
+// bit-reversed out), inverse is Gentleman-Sande with ipsi_brv[h + j] then
+// x n^-1. Values are canonical [0, q) at the boundary, so the lazy internal
+// ranges ([0,4q) forward, [0,2q) inverse, Harvey 2014) are invisible.
+//
+// One CTA owns one polynomial (n <= 16384 -> <= 139 KB of shared memory).
+// Stages are grouped in phases of up to LOGR stages: each thread pulls
+// 2^LOGR coefficients (stride t_min) from shared memory into registers, runs
+// the phase's butterflies register-resident (one 128-bit twiddle load per
+// distinct twiddle), and writes them back — log2(n)/LOGR shared-memory round
+// trips instead of log2(n). Global traffic is one coalesced 128-bit read and
+// one write per coefficient (the HBM roofline of 16 B/coefficient).
+// The padding x + x/16 keeps the 64-bit shared accesses at the 2-wavefront
+// minimum for every phase stride.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace fhe {
+
+__device__ __forceinline__ int spad(int x) { return x + (x >> 4); }
+
+struct LoadMap {
+  const uint64_t* src;
+  int G;        // rows per limb group in the OUTPUT indexing (P, or ndig)
+  int ndig;     // 0 = plain (src row == out row); >0 = digit mode
+  int T;        // digit width
+  int pad_;
+  uint64_t mask;
+};
+
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
+}
+
+// One forward phase: stages [s, s+R) (half-sizes t_min*2^(R-1) .. t_min).
+template <int LOGR, int R>
+__device__ __forceinline__ void fwd_phase(uint64_t* sm, const NttDesc& d, int s, int tid, int nthr) {
+  const int n = d.n, logn = d.logn;
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  const int tl = logn - (s + R);  // log2 t_min
+  const int items = n >> LOGR;
+  for (int w = tid; w < items; w += nthr) {
+    const int base = ((w >> tl) << (tl + LOGR)) + (w & ((1 << tl) - 1));
+    uint64_t e[1 << LOGR];
+#pragma unroll
+    for (int i = 0; i < (1 << LOGR); ++i) e[i] = sm[spad(base + (i << tl))];
+    static_for<0, R>([&](auto ai) {
+      constexpr int a = R - 1 - decltype(ai)::value;  // largest stride first
+      constexpr int dd = 1 << a;
+      const int sh = tl + a + 1;                      // = logn - stage
+#pragma unroll
+      for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+        const ulonglong2 tw = __ldg(&d.psi[(n + base + (g << tl)) >> sh]);
+#pragma unroll
+        for (int u = 0; u < dd; ++u) {
+          uint64_t X = e[g + u];
+          X = X >= q2 ? X - q2 : X;
+          const uint64_t T = shoup_lazy(e[g + u + dd], tw.x, tw.y, q);
+          e[g + u] = X + T;
+          e[g + u + dd] = X - T + q2;
+        }
+      }
+    });
+#pragma unroll
+    for (int i = 0; i < (1 << LOGR); ++i) sm[spad(base + (i << tl))] = e[i];
+  }
+}
+
+// One inverse phase: stages [s, s+R) processed smallest half-size first.
+template <int LOGR, int R>
+__device__ __forceinline__ void inv_phase(uint64_t* sm, const NttDesc& d, int s, int tid, int nthr) {
+  const int n = d.n, logn = d.logn;
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  const int tl = logn - (s + R);
+  const int items = n >> LOGR;
+  const bool last = (s == 0);
+  for (int w = tid; w < items; w += nthr) {
+    const int base = ((w >> tl) << (tl + LOGR)) + (w & ((1 << tl) - 1));
+    uint64_t e[1 << LOGR];
+#pragma unroll
+    for (int i = 0; i < (1 << LOGR); ++i) e[i] = sm[spad(base + (i << tl))];
+    static_for<0, R>([&](auto ai) {
+      constexpr int a = decltype(ai)::value;
+      constexpr int dd = 1 << a;
+      const int sh = tl + a + 1;
+      if (last && a == R - 1) {  // stage 0: fold n^-1 (ring.py:162)
+#pragma unroll
+        for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+#pragma unroll
+          for (int u = 0; u < dd; ++u) {
+            const uint64_t X = e[g + u], Y = e[g + u + dd];
+            e[g + u] = shoup_lazy(X + Y, d.ninv.x, d.ninv.y, q);
+            e[g + u + dd] = shoup_lazy(X - Y + q2, d.ninv_w1.x, d.ninv_w1.y, q);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+          const ulonglong2 tw = __ldg(&d.ipsi[(n + base + (g << tl)) >> sh]);
+#pragma unroll
+          for (int u = 0; u < dd; ++u) {
+            const uint64_t X = e[g + u], Y = e[g + u + dd];
+            const uint64_t S = X + Y;
+            e[g + u] = S >= q2 ? S - q2 : S;
+            e[g + u + dd] = shoup_lazy(X - Y + q2, tw.x, tw.y, q);
+          }
+        }
+      }
+    });
+#pragma unroll
+    for (int i = 0; i < (1 << LOGR); ++i) sm[spad(base + (i << tl))] = e[i];
+  }
+}
+
+template <int LOGR, bool INV, int R>
+__device__ __forceinline__ void run_phase(uint64_t* sm, const NttDesc& d, int s, int tid, int nthr) {
+  if constexpr (INV)
+    inv_phase<LOGR, R>(sm, d, s, tid, nthr);
+  else
+    fwd_phase<LOGR, R>(sm, d, s, tid, nthr);
+}
+
+template <int LOGR, bool INV>
+__device__ __forceinline__ void run_partial(uint64_t* sm, const NttDesc& d, int s, int r, int tid,
+                                            int nthr) {
+  static_for<1, LOGR>([&](auto ri) {
+    constexpr int R = decltype(ri)::value;
+    if (r == R) run_phase<LOGR, INV, R>(sm, d, s, tid, nthr);
+  });
+}
+
+template <int LOGR, bool INV>
+__global__ void __launch_bounds__(512) ntt_kernel(const LimbSet ls, const LoadMap lm,
+                                                  uint64_t* __restrict__ dst) {
+  extern __shared__ uint64_t sm[];
+  const int row = blockIdx.x;
+  const int limb = (row / lm.G) % ls.L;
+  const NttDesc d = ls.d[limb];
+  const int n = d.n, logn = d.logn;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+
+  const uint64_t* srow;
+  int shift = 0;
+  if (lm.ndig > 0) {
+    srow = lm.src + (size_t)(row / lm.ndig) * n;
+    shift = lm.T * (row % lm.ndig);
+  } else {
+    srow = lm.src + (size_t)row * n;
+  }
+  const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(srow);
+  for (int i = tid; i < (n >> 1); i += nthr) {
+    ulonglong2 v = s2[i];
+    if (lm.ndig > 0) {
+      v.x = (v.x >> shift) & lm.mask;
+      v.y = (v.y >> shift) & lm.mask;
+    }
+    sm[spad(2 * i)] = v.x;
+    sm[spad(2 * i + 1)] = v.y;
+  }
+  __syncthreads();
+
+  const int nfull = logn / LOGR, rem = logn - nfull * LOGR;
+  if (!INV) {
+    for (int p = 0; p < nfull; ++p) {
+      run_phase<LOGR, false, LOGR>(sm, d, p * LOGR, tid, nthr);
+      __syncthreads();
+    }
+    if (rem) {
+      run_partial<LOGR, false>(sm, d, nfull * LOGR, rem, tid, nthr);
+      __syncthreads();
+    }
+  } else {
+    if (rem) {
+      run_partial<LOGR, true>(sm, d, nfull * LOGR, rem, tid, nthr);
+      __syncthreads();
+    }
+    for (int p = nfull - 1; p >= 0; --p) {
+      run_phase<LOGR, true, LOGR>(sm, d, p * LOGR, tid, nthr);
+      __syncthreads();
+    }
+  }
+
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + (size_t)row * n);
+  for (int i = tid; i < (n >> 1); i += nthr) {
+    uint64_t x = sm[spad(2 * i)], y = sm[spad(2 * i + 1)];
+    if (!INV) {
+      x = x >= q2 ? x - q2 : x;
+      y = y >= q2 ? y - q2 : y;
+    }
+    d2[i] = make_ulonglong2(csub(x, q), csub(y, q));
+  }
+}
+
+static int build_limbset(const fhe_plan* const* plans, int L, LimbSet* ls, int* n_out) {
+  if (L < 1 || L > FHE_MAX_LIMBS) return fail(FHE_ERR_VALUE, "limb count %d out of range", L);
+  if (!plans) return fail(FHE_ERR_VALUE, "null plans");
+  ls->L = L;
+  ls->pad_ = 0;
+  int n = -1;
+  for (int l = 0; l < L; ++l) {
+    if (!plans[l]) return fail(FHE_ERR_VALUE, "null plan %d", l);
+    if (n >= 0 && plans[l]->n != n) return fail(FHE_ERR_PARAMETER, "limb plans disagree on n");
+    n = plans[l]->n;
+    ls->d[l] = plans[l]->desc;
+  }
+  if (n > 16384) return fail(FHE_ERR_PARAMETER, "NTT supports n <= 16384 (got %d)", n);
+  *n_out = n;
+  return FHE_OK;
+}
+
+template <int LOGR, bool INV>
+static int launch_t(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int n,
+                    cudaStream_t st) {
+  const size_t smem = (size_t)(n + (n >> 4) + 1) * sizeof(uint64_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    FHE_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGR, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  150 * 1024));
+    attr_set = true;
+  }
+  int items = n >> LOGR;
+  int threads = items < 512 ? items : 512;
+  if (threads < 1) threads = 1;
+  ntt_kernel<LOGR, INV><<<rows, threads, smem, st>>>(ls, lm, dst);
+  FHE_CHECK_LAUNCH("ntt_kernel");
+  return FHE_OK;
+}
+
+template <bool INV>
+static int launch(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int n,
+                  cudaStream_t st) {
+  if (rows == 0) return FHE_OK;
+  int logn = 0;
+  while ((1 << logn) < n) ++logn;
+  switch (logn < 4 ? logn : 4) {
+    case 1: return launch_t<1, INV>(ls, lm, dst, rows, n, st);
+    case 2: return launch_t<2, INV>(ls, lm, dst, rows, n, st);
+    case 3: return launch_t<3, INV>(ls, lm, dst, rows, n, st);
+    default: return launch_t<4, INV>(ls, lm, dst, rows, n, st);
+  }
+}
+
+}  // namespace fhe
+
+using namespace fhe;
+
+extern "C" {
+
+int fhe_ntt_forward(const fhe_plan* const* plans, int L, int B, int P, const uint64_t* src,
+                    uint64_t* dst, void* stream) {
+  LimbSet ls;
+  int n;
+  if (int rc = build_limbset(plans, L, &ls, &n)) return rc;
+  if (B < 0 || P < 1 || !src || !dst) return fail(FHE_ERR_VALUE, "bad batch arguments");
+  LoadMap lm{src, P, 0, 0, 0, ~0ull};
+  return launch<false>(ls, lm, dst, B * L * P, n, (cudaStream_t)stream);
+}
+
+int fhe_ntt_inverse(const fhe_plan* const* plans, int L, int B, int P, const uint64_t* src,
+                    uint64_t* dst, void* stream) {
+  LimbSet ls;
+  int n;
+  if (int rc = build_limbset(plans, L, &ls, &n)) return rc;
+  if (B < 0 || P < 1 || !src || !dst) return fail(FHE_ERR_VALUE, "bad batch arguments");
+  LoadMap lm{src, P, 0, 0, 0, ~0ull};
+  return launch<true>(ls, lm, dst, B * L * P, n, (cudaStream_t)stream);
+}
+
+int fhe_ntt_forward_digits(const fhe_plan* const* plans, int L, int B, const uint64_t* src,
+                           uint64_t* dst, int T, int ndig, void* stream) {
+  LimbSet ls;
+  int n;
+  if (int rc = build_limbset(plans, L, &ls, &n)) return rc;
+  if (B < 0 || ndig < 1 || T < 1 || T > 63 || !src || !dst)
+    return fail(FHE_ERR_VALUE, "bad digit arguments");
+  if (src == dst) return fail(FHE_ERR_VALUE, "digit NTT cannot run in place");
+  LoadMap lm{src, ndig, ndig, T, 0, (1ull << T) - 1};
+  return launch<false>(ls, lm, dst, B * L * ndig, n, (cudaStream_t)stream);
+}
+
+}  // extern "C"

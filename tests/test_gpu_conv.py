@@ -1,0 +1,219 @@
+"""K1 (Flash conv / pool / FC) parity on the device vs reference goldens + oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_npz, sha
+from oracle import flash_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+Q = 1152921486375014401
+P_ = 270337
+N = 2048
+
+
+def _P():
+    from paper_2401_16732_b200 import params
+
+    return params.default_params()
+
+
+def _cts(arr, q=Q):
+    from paper_2401_16732_b200 import bfv
+
+    t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+    return bfv.cts_from_rows(t, q, bfv.Encoding.DIRECT, bfv.Domain.COEFF)
+
+
+def _out(cts):
+    from paper_2401_16732_b200 import bfv
+
+    return bfv.cts_rows(cts).cpu().numpy()
+
+
+def _case(golden, name):
+    g = golden["conv"][name]
+    r = np.random.default_rng(g["seed"])
+    arr = r.integers(0, Q, (g["n_in"], 2, N), dtype=np.int64)
+    w = r.integers(-127, 128, (g["c_o"], g["c_i"], g["f_w"], g["f_w"]), dtype=np.int64)
+    b = r.integers(-1000, 1000, g["c_o"], dtype=np.int64) if g["bias"] else None
+    return g, arr, w, b
+
+
+@pytest.mark.parametrize("name", ["cfg1", "r20_stem", "r20_s2", "r20_s3", "proj1x1", "frag64", "frag64_bias",
+                                  "packed16_bias", "r18_8x8_512", "vgg4x4", "stem7x7_224"])
+def test_conv_proposed_matches_reference(golden, name):
+    from paper_2401_16732_b200 import conv
+
+    g, arr, w, b = _case(golden, name)
+    P = _P()
+    lay = conv.layout_direct(P, g["H"], g["W"], g["f_w"])
+    spec = conv.ConvLayerSpec(g["H"], g["W"], g["f_w"], g["c_i"], g["c_o"], w, bias=b)
+    y = conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, g["c_i"]), spec, P)
+    assert len(y.cts) == g["n_out"]
+    assert sha(_out(y.cts)) == g["h:out"]
+    assert y.layout.c_n == 1 and y.channels == g["c_o"]
+
+
+def test_conv_cfg1_full_arrays():
+    from paper_2401_16732_b200 import conv
+
+    d = load_npz("conv_cfg1.npz")
+    P = _P()
+    lay = conv.layout_direct(P, 32, 32, 3)
+    spec = conv.ConvLayerSpec(32, 32, 3, 16, 16, d["weights"])
+    y = conv.conv_proposed(conv.PackedTensor(_cts(d["cts"]), lay, 16), spec, P)
+    assert np.array_equal(_out(y.cts), d["out"])
+
+
+def test_config1_end_to_end_decrypt():
+    """Real encryptions: bit-exact ciphertexts and identical decrypted outputs."""
+    from paper_2401_16732_b200 import bfv, conv
+    from paper_2401_16732_b200.ring import ModPoly
+
+    d = load_npz("config1_e2e.npz")
+    P = _P()
+    sk = bfv.SecretKey(ModPoly(d["s"], P.q), P)
+    lay = conv.layout_direct(P, 32, 32, 3)
+    x = conv.PackedTensor(_cts(d["cts"]), lay, 16)
+    y = conv.conv_proposed(x, conv.ConvLayerSpec(32, 32, 3, 16, 16, d["w"]), P)
+    assert np.array_equal(_out(y.cts), d["out"])
+    assert np.array_equal(conv.unpack(y, sk), d["dec"])
+    # and the decrypted result equals the plaintext integer convolution
+    xp = np.pad(d["x"], ((0, 0), (1, 1), (1, 1)))
+    ref = np.zeros((16, 32, 32), dtype=np.int64)
+    for dy in range(3):
+        for dx in range(3):
+            ref += np.einsum("oi,ihw->ohw", d["w"][:, :, dy, dx], xp[:, dy : dy + 32, dx : dx + 32])
+    assert np.array_equal(d["dec"], ref)
+
+
+def test_config1_pack_encrypt_bit_exact(golden):
+    """The same seed through our pack_input/encrypt_private gives the reference's ciphertexts."""
+    from paper_2401_16732_b200 import bfv, conv
+
+    d = load_npz("config1_e2e.npz")
+    P = _P()
+    r = np.random.default_rng(golden["config1_e2e"]["seed"])
+    sk = bfv.keygen(P, r)
+    assert np.array_equal(sk.s.coeffs, d["s"])
+    xin = r.integers(0, 8, (16, 32, 32), dtype=np.int64)
+    assert np.array_equal(xin, d["x"])
+    w = r.integers(-127, 128, (16, 16, 3, 3), dtype=np.int64)
+    assert np.array_equal(w, d["w"])
+    x = conv.pack_input(xin, P, 3, lambda pt: bfv.encrypt_private(pt, sk, r))
+    assert np.array_equal(_out(x.cts), d["cts"])
+    y = conv.conv_proposed(x, conv.ConvLayerSpec(32, 32, 3, 16, 16, w), P)
+    assert [bfv.noise_budget(c, sk) for c in y.cts[:2]] == golden["config1_e2e"]["budget_out"]
+
+
+def test_pool_fc_match_reference(golden):
+    from paper_2401_16732_b200 import conv
+
+    g = golden["pool_fc"]
+    P = _P()
+    r = np.random.default_rng(g["seed"])
+    arr = r.integers(0, Q, (8, 2, N), dtype=np.int64)
+    lay8 = conv.replace(conv.layout_direct(P, 8, 8, 3), c_n=1)
+    pooled = conv.avg_pool(conv.PackedTensor(_cts(arr), lay8, 8), 8, P)
+    assert sha(_out(pooled.cts)) == g["h:pool"]
+    assert pooled.layout.stride == 8
+    fcw = r.integers(-127, 128, (10, 8), dtype=np.int64)
+    fcb = r.integers(-100, 100, 10, dtype=np.int64)
+    fco = conv.fully_connected(pooled, fcw, P, bias=fcb)
+    assert sha(_out(fco)) == g["h:fc"]
+
+
+def test_conv_small_ring(golden):
+    from paper_2401_16732_b200 import conv, params
+
+    g = golden["conv_n256"]
+    P = params.RingParams(**g["params"])
+    r = np.random.default_rng(g["seed"])
+    lay = conv.layout_direct(P, 4, 4, 3)
+    arr = r.integers(0, P.q, (lay.ct_count(9), 2, 256), dtype=np.int64)
+    wts = r.integers(-127, 128, (5, 9, 3, 3), dtype=np.int64)
+    y = conv.conv_proposed(conv.PackedTensor(_cts(arr, P.q), lay, 9), conv.ConvLayerSpec(4, 4, 3, 9, 5, wts), P)
+    assert sha(_out(y.cts)) == g["h:out"]
+
+
+def test_conv_edge_cases():
+    from paper_2401_16732_b200 import conv
+    from paper_2401_16732_b200.errors import AccumulatorBudgetError, EncodingError, ParameterError
+
+    P = _P()
+    rng = np.random.default_rng(4)
+    lay = conv.layout_direct(P, 8, 8, 3)
+    arr = rng.integers(0, Q, (1, 2, N), dtype=np.int64)
+    x = conv.PackedTensor(_cts(arr), lay, 3)
+    # identity kernel -> input
+    w = np.zeros((1, 1, 3, 3), dtype=np.int64)
+    w[0, 0, 1, 1] = 1
+    y = conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, 1), conv.ConvLayerSpec(8, 8, 3, 1, 1, w), P)
+    assert np.array_equal(_out(y.cts)[0], arr[0])
+    # all-zero weights -> zero ciphertext
+    y = conv.conv_proposed(x, conv.ConvLayerSpec(8, 8, 3, 3, 2, np.zeros((2, 3, 3, 3))), P)
+    assert not _out(y.cts).any()
+    # extreme weights ±255 (MAX_WEIGHT_BITS bound) vs oracle
+    w = rng.choice([-255, 255, -1, 0, 1], size=(4, 3, 3, 3))
+    y = conv.conv_proposed(x, conv.ConvLayerSpec(8, 8, 3, 3, 4, w), P)
+    layd = {"n": N, "w_p": lay.w_p, "pad": 1, "tile": lay.tile, "c_n": lay.c_n, "frags": 1}
+    assert np.array_equal(_out(y.cts), O.conv_proposed(arr, w.reshape(4, 3, 9), layd, Q))
+    # extreme coefficients: all q-1 / zeros
+    arr2 = np.full((1, 2, N), Q - 1, dtype=np.int64)
+    arr2[0, 1, ::3] = 0
+    w = np.full((2, 3, 3, 3), -255)
+    y = conv.conv_proposed(conv.PackedTensor(_cts(arr2), lay, 3), conv.ConvLayerSpec(8, 8, 3, 3, 2, w), P)
+    assert np.array_equal(_out(y.cts), O.conv_proposed(arr2, w.reshape(2, 3, 9), layd, Q))
+    # errors, raised before launch like the reference
+    with pytest.raises(ParameterError):
+        conv.conv_proposed(x, conv.ConvLayerSpec(16, 16, 3, 3, 2, np.zeros((2, 3, 3, 3))), P)
+    with pytest.raises(ParameterError):
+        conv.conv_proposed(conv.PackedTensor(x.cts, conv.replace(lay, stride=2), 3),
+                           conv.ConvLayerSpec(8, 8, 3, 3, 2, np.zeros((2, 3, 3, 3))), P)
+    bx = conv.PackedTensor([conv.bfv.Ciphertext(c.c0, c.c1, conv.Encoding.BATCH, c.domain) for c in x.cts], lay, 3)
+    with pytest.raises(EncodingError):
+        conv.conv_proposed(bx, conv.ConvLayerSpec(8, 8, 3, 3, 2, np.zeros((2, 3, 3, 3))), P)
+    with pytest.raises(AccumulatorBudgetError):
+        conv._check_budget(np.full((1, 1 << 25), 200))  # Σ|w| = 6.7e9 ≥ 2^32
+
+
+def test_full_size_r18_layer_properties():
+    """(8², 512→512): linearity over inputs, and sampled channels vs the oracle."""
+    from paper_2401_16732_b200 import conv
+
+    P = _P()
+    rng = np.random.default_rng(12)
+    lay = conv.layout_direct(P, 8, 8, 3)
+    n_in = lay.ct_count(512)
+    a = rng.integers(0, Q, (n_in, 2, N), dtype=np.int64)
+    b = rng.integers(0, Q, (n_in, 2, N), dtype=np.int64)
+    w = rng.integers(-127, 128, (512, 512, 3, 3), dtype=np.int64)
+    spec = conv.ConvLayerSpec(8, 8, 3, 512, 512, w)
+    run = lambda arr: _out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, 512), spec, P).cts)
+    ya, yb, yab = run(a), run(b), run((a.astype(object) + b) % Q)
+    assert np.array_equal(yab, ((ya.astype(object) + yb) % Q).astype(np.int64))
+    layd = {"n": N, "w_p": lay.w_p, "pad": 1, "tile": lay.tile, "c_n": lay.c_n, "frags": 1}
+    chans = [0, 255, 511]
+    ref = O.conv_proposed(a, w.reshape(512, 512, 9), layd, Q, channels=chans)
+    assert np.array_equal(ya[chans], ref)
+
+
+def test_conv_conventional_matches_reference(golden):
+    from paper_2401_16732_b200 import bfv, conv
+
+    g = golden["conv_conventional"]
+    P = _P()
+    r = np.random.default_rng(g["seed"])
+    sk = bfv.keygen(P, r)
+    xc = r.integers(0, 8, (4, 16, 16), dtype=np.int64)
+    wc = r.integers(-127, 128, (4, 4, 3, 3), dtype=np.int64)
+    spec = conv.ConvLayerSpec(16, 16, 3, 4, 4, wc)
+    swk = bfv.gen_switching_keys(sk, conv.conventional_steps(spec, P), r, decomp_log=conv.CONV_DECOMP_LOG)
+    xb = conv.pack_input(xc, P, 3, lambda pt: bfv.encrypt_private(pt, sk, r), batch=True)
+    assert sha(_out(xb.cts)) == g["h:in"]
+    y = conv.conv_conventional(xb, spec, swk, P)
+    assert sha(_out(y.cts)) == g["h:out"]
+    assert conv.unpack(y, sk).tolist() == g["dec"]

@@ -182,14 +182,20 @@ def time_steps(fn, steps, warmup, flush_buf=None):
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def cpu_baseline(P, layers, threads: int, budget_s: float = 12.0):
+def oracle_lib():
+    lib = ctypes.CDLL(str(ROOT / "oracle" / "liboracle.so"))
+    vp, i = ctypes.c_void_p, ctypes.c_int
+    lib.oracle_conv.restype = i
+    lib.oracle_conv.argtypes = [ctypes.c_uint64, i, vp, i, vp, i, i, vp, vp, i, i, vp, i, i]
+    return lib
+
+
+def cpu_baseline(P, layers, threads: int):
     """C oracle (oracle/conv_oracle.c) on a bounded sample: per layer the
     first `threads` output units, extrapolated to the full layer."""
-    lib = ctypes.CDLL(str(ROOT / "oracle" / "liboracle.so"))
-    lib.oracle_conv.restype = ctypes.c_int
+    lib = oracle_lib()
     total = 0.0
     sampled_units = 0
-    t_start = time.perf_counter()
     for L in layers:
         plan = L["plan"]
         w = plan.w.cpu().numpy().astype(np.int16)
@@ -445,7 +451,7 @@ def reference_arm(args, world):
 
     P = params.default_params()
     rng = np.random.default_rng(4)
-    lib = ctypes.CDLL(str(ROOT / "oracle" / "liboracle.so"))
+    lib = oracle_lib()
     threads = os.cpu_count() or 1
     layers = []
     for l in stacks.conv_layers(stacks.CONFIGS[args.workload]()):

@@ -57,6 +57,8 @@ def empty_rows(rows: int, n: int) -> torch.Tensor:
 def to_device(arr: np.ndarray) -> torch.Tensor:
     """Host int64 array -> device tensor (staged through pinned memory)."""
     a = np.ascontiguousarray(arr, dtype=np.int64)
+    if not a.flags.writeable:
+        a = a.copy()
     t = torch.from_numpy(a)
     if a.nbytes >= 1 << 16:
         t = t.pin_memory()

@@ -193,7 +193,7 @@ def test_full_size_r18_layer_properties():
     w = rng.integers(-127, 128, (512, 512, 3, 3), dtype=np.int64)
     spec = conv.ConvLayerSpec(8, 8, 3, 512, 512, w)
     run = lambda arr: _out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, 512), spec, P).cts)
-    ya, yb, yab = run(a), run(b), run((a.astype(object) + b) % Q)
+    ya, yb, yab = run(a), run(b), run(((a.astype(object) + b) % Q).astype(np.int64))
     assert np.array_equal(yab, ((ya.astype(object) + yb) % Q).astype(np.int64))
     layd = {"n": N, "w_p": lay.w_p, "pad": 1, "tile": lay.tile, "c_n": lay.c_n, "frags": 1}
     chans = [0, 255, 511]

@@ -169,6 +169,21 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
                    const int32_t* term_step, int frags, int frag_stride,
                    const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
                    void* stream);
+/* K1-TC: the same contraction on tcgen05.mma.kind::i8 (u8 digit planes x s8
+ * weights -> s32, 8 planes recombined exactly mod q). Two launches:
+ *  fhe_conv_tc_prep: input ciphertexts [n_in][2][n] -> digit-plane operand X
+ *    [2][frags][ceil(c_i/32)][n + 2h][256 B] (channel-aligned negacyclic
+ *    extension, UMMA core-matrix order); X must hold that many bytes.
+ *  fhe_conv_tc: X (+ weights packed [ceil(c_o/128)][ceil(c_i/32)][taps][16][256 B]
+ *    int8, |w| <= 127) -> out [c_o*frags][2][n], canonical mod q, bias fused.
+ * tap_steps_host: HOST int32 [taps], each in [-h, h]. c_n/tile: channel
+ * packing of the input layout (conv.py:113-130); frags > 1 = fragmented. */
+int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int c_n, int tile,
+                     int h, uint8_t* X, void* stream);
+int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h,
+                const int8_t* Wpacked, int c_o, int taps, const int32_t* tap_steps_host,
+                const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
+                void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

@@ -228,6 +228,21 @@ def add_bias(out: np.ndarray, bias_vals, masks: np.ndarray, delta: int, p: int, 
     return out
 
 
+def bias_masks(lay: dict) -> np.ndarray:
+    """Slots of conv._bias_plaintext (conv.py:414-424), one row per fragment."""
+    ys = lay["pad"] + np.arange(lay["height"])
+    xs = lay["pad"] + np.arange(lay["width"])
+    tp = (ys[:, None] * lay["w_p"] + xs[None, :]).ravel()
+    masks = np.zeros((lay["frags"], lay["n"]), dtype=np.uint8)
+    for f in range(lay["frags"]):
+        if lay["frags"] > 1:
+            sel = tp[tp // lay["frag_len"] == f]
+            masks[f, lay["halo"] + sel - f * lay["frag_len"]] = 1
+        else:
+            masks[f, tp] = 1
+    return masks
+
+
 def avg_pool(cts: np.ndarray, k: int, w_p: int, q: int) -> np.ndarray:
     """conv.avg_pool (conv.py:604-623): Σ_{dy,dx<k} DRot(ct, dy·W_p+dx)."""
     n = cts.shape[-1]

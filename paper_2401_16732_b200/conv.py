@@ -255,17 +255,75 @@ class ConvPlan:
         self.bias = None if bias_delta is None else torch.from_numpy(np.asarray(bias_delta, dtype=np.uint64).view(np.int64)).to(dev)
         self.mask = None if bias_mask is None else torch.from_numpy(np.asarray(bias_mask, dtype=np.uint8)).to(dev)
         self.n_out = self.c_o * self.frags
+        self.tc: ConvTcPlan | None = None  # tensor-core variant, when the layer qualifies
+
+    @property
+    def path(self) -> str:
+        return "tc" if self.tc is not None and _conv_path() != "int" else "int"
 
     def run(self, inp: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """inp: device [n_in, 2, n] -> out [c_o*frags, 2, n]."""
         inp = inp.contiguous()
         if out is None:
             out = torch.empty((self.n_out, 2, self.n), dtype=torch.int64, device=inp.device)
+        if self.path == "tc":
+            return self.tc.run(inp, out)
         _native.call(
             "fhe_conv_flash", self.q, self.n, inp.data_ptr(), inp.shape[0], self.w.data_ptr(), self.c_o, self.K,
             self.src.data_ptr(), self.step.data_ptr(), self.frags, self.fstride, device.ptr(self.bias),
             device.ptr(self.mask), out.data_ptr(), device.stream(),
         )
+        return out
+
+
+def _conv_path() -> str:
+    """FLASHHE_CONV_PATH = auto (default) | int | tc — which K1 variant runs."""
+    import os
+
+    return os.environ.get("FLASHHE_CONV_PATH", "auto")
+
+
+class ConvTcPlan:
+    """K1-TC operands (csrc/conv_tc.cu): packed int8 weights, the digit-plane
+    operand buffer X and the tap steps. Eligible when |w| ≤ 127, ≥ 16 input
+    channels, n a multiple of 64 and the halo window fits shared memory."""
+
+    N_TILE = 128
+    S_CTA = 64
+
+    @staticmethod
+    def eligible(weights3d: np.ndarray, n: int, h: int, taps: int) -> bool:
+        c_o, c_i, _ = weights3d.shape
+        if c_i < 16 or n < 64 or n % 64 or taps > 64 or int(np.abs(weights3d).max(initial=0)) > 127:
+            return False
+        a_bytes = -(-(ConvTcPlan.S_CTA + 2 * h) * 256 // 1024) * 1024
+        return 2 * (a_bytes + taps * ConvTcPlan.N_TILE * 32) + 64 <= 227 * 1024
+
+    def __init__(self, q: int, n: int, weights3d: np.ndarray, steps: np.ndarray, layout: TileLayout,
+                 bias, mask):
+        self.q, self.n = int(q), int(n)
+        self.c_o, self.c_i, self.taps = weights3d.shape
+        self.h = int(np.abs(steps).max(initial=0))
+        self.frags, self.c_n, self.tile = layout.frags, layout.c_n, layout.tile
+        N = self.N_TILE
+        OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
+        wp = np.zeros((OB * N, JB * 32, self.taps), dtype=np.int8)
+        wp[: self.c_o, : self.c_i] = weights3d
+        # [ob][jb][tap][g][kh][r][jj] with o = ob*N + g*8 + r, j = jb*32 + kh*16 + jj
+        wp = wp.reshape(OB, N // 8, 8, JB, 2, 16, self.taps).transpose(0, 3, 6, 1, 4, 2, 5)
+        dev = device.require_cuda()
+        self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
+        self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
+        self.X = torch.empty(2 * self.frags * JB * (n + 2 * self.h) * 256, dtype=torch.uint8, device=dev)
+        self.bias, self.mask = bias, mask
+
+    def run(self, inp: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        st = device.stream()
+        _native.call("fhe_conv_tc_prep", self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.c_n,
+                     self.tile, self.h, self.X.data_ptr(), st)
+        _native.call("fhe_conv_tc", self.q, self.n, self.X.data_ptr(), self.c_i, self.frags, self.h,
+                     self.w.data_ptr(), self.c_o, self.taps, self.steps, device.ptr(self.bias),
+                     device.ptr(self.mask), out.data_ptr(), st)
         return out
 
 
@@ -291,6 +349,9 @@ def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> C
         bias_mask = np.stack([_bias_mask(out_layout, f) for f in range(layout.frags)])
     plan = ConvPlan(params.q, params.n, layer.weights.reshape(layer.c_o, -1), src, step,
                     frags=layout.frags, fstride=fstride, bias_delta=bias_delta, bias_mask=bias_mask)
+    h = int(np.abs(steps).max(initial=0))
+    if ConvTcPlan.eligible(layer.weights, params.n, h, taps):
+        plan.tc = ConvTcPlan(params.q, params.n, layer.weights, steps, layout, plan.bias, plan.mask)
     cache[key] = plan
     return plan
 

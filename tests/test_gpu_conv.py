@@ -42,11 +42,13 @@ def _case(golden, name):
     return g, arr, w, b
 
 
+@pytest.mark.parametrize("path", ["auto", "int"])
 @pytest.mark.parametrize("name", ["cfg1", "r20_stem", "r20_s2", "r20_s3", "proj1x1", "frag64", "frag64_bias",
                                   "packed16_bias", "r18_8x8_512", "vgg4x4", "stem7x7_224"])
-def test_conv_proposed_matches_reference(golden, name):
+def test_conv_proposed_matches_reference(golden, name, path, monkeypatch):
     from paper_2401_16732_b200 import conv
 
+    monkeypatch.setenv("FLASHHE_CONV_PATH", path)
     g, arr, w, b = _case(golden, name)
     P = _P()
     lay = conv.layout_direct(P, g["H"], g["W"], g["f_w"])
@@ -55,6 +57,50 @@ def test_conv_proposed_matches_reference(golden, name):
     assert len(y.cts) == g["n_out"]
     assert sha(_out(y.cts)) == g["h:out"]
     assert y.layout.c_n == 1 and y.channels == g["c_o"]
+
+
+TC_CASES = [
+    # H, W, f_w, c_i, c_o, bias
+    (64, 64, 3, 32, 8, True),     # fragmented (3 frags, halo 67) + bias
+    (16, 16, 3, 16, 136, True),   # c_n = 6, two output-channel tiles, bias
+    (8, 8, 3, 48, 20, False),     # c_n = 20, partial channel block
+    (32, 32, 1, 40, 130, False),  # 1x1 projection, c_n = 2
+    (4, 4, 3, 33, 5, False),      # c_n = 56
+]
+
+
+@pytest.mark.parametrize("case", TC_CASES)
+def test_conv_tc_vs_oracle(case, monkeypatch):
+    """K1-TC against the pinned oracle (and against K1 on the integer pipes)."""
+    from oracle.flash_oracle import add_bias
+    from paper_2401_16732_b200 import conv
+
+    H, W, f_w, c_i, c_o, bias = case
+    P = _P()
+    rng = np.random.default_rng(H * 1000 + c_i)
+    lay = conv.layout_direct(P, H, W, f_w)
+    arr = rng.integers(0, Q, (lay.ct_count(c_i), 2, N), dtype=np.int64)
+    arr[:, :, ::17] = 0
+    arr[:, :, 5::17] = Q - 1
+    w = rng.integers(-127, 128, (c_o, c_i, f_w, f_w), dtype=np.int64)
+    b = rng.integers(-5000, 5000, c_o, dtype=np.int64) if bias else None
+    spec = conv.ConvLayerSpec(H, W, f_w, c_i, c_o, w, bias=b)
+    plan = conv.conv_plan(spec, lay, P)
+    assert plan.tc is not None, "case should take the tensor-core path"
+    monkeypatch.setenv("FLASHHE_CONV_PATH", "tc")
+    y_tc = _out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, c_i), spec, P).cts)
+    monkeypatch.setenv("FLASHHE_CONV_PATH", "int")
+    y_int = _out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, c_i), spec, P).cts)
+    assert np.array_equal(y_tc, y_int)
+    layd = {"n": N, "w_p": lay.w_p, "pad": lay.pad, "tile": lay.tile, "c_n": lay.c_n, "frags": lay.frags}
+    chans = sorted({0, c_o // 2, c_o - 1})
+    ref = O.conv_proposed(arr, w.reshape(c_o, c_i, -1), layd, Q, channels=chans)
+    if b is not None:
+        out_lay = {"n": N, "height": H, "width": W, "pad": lay.pad, "w_p": lay.w_p, "frags": lay.frags,
+                   "frag_len": lay.frag_len, "halo": lay.halo}
+        ref = add_bias(ref, b[chans], O.bias_masks(out_lay), P.delta, P.p, Q)
+    sel = np.concatenate([np.arange(c * lay.frags, (c + 1) * lay.frags) for c in chans])
+    assert np.array_equal(y_tc[sel], ref)
 
 
 def test_conv_cfg1_full_arrays():

@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   const int JB = a.JB, taps = a.taps;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * a.stage_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const uint32_t full0 = smem_u32(&bars[0]), done0 = smem_u32(&bars[2]);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  const uint32_t full0 = smem_u32(&bars[0]), done0 = smem_u32(&bars[2]), acc_bar = smem_u32(&bars[4]);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 5; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[i])));
     asm volatile("fence.mbarrier_init.release.cluster;");
     asm volatile("fence.proxy.async.shared::cta;");
@@ -176,9 +176,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
       }
       mma_commit(done0 + 8 * (jb & 1));
     }
+    mma_commit(acc_bar);  // tracks every earlier tcgen05.mma of this CTA
   }
-  // all MMAs done: the last commit tracks every earlier tcgen05.mma
-  mbar_wait(done0 + 8 * ((JB - 1) & 1), ((JB - 1) >> 1) & 1);
+  // single-use barrier: its phase 0 completes exactly when all MMAs are done
+  // (waiting on a reused stage barrier could match an older phase's parity)
+  mbar_wait(acc_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
   int32_t* stage = reinterpret_cast<int32_t*>(smem);  // reuse the operand buffers

@@ -159,6 +159,19 @@ def run_peaks():
             ops = blocks * threads * it * per
             best = max(best, ops / (e0.elapsed_time(e1) * 1e-3))
         res[name] = best
+    # dense int8 tcgen05 (M=128, N=256, K=32), one CTA per SM
+    usink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    _native.call("fhe_peak_tc_i8", 148, 16, usink.data_ptr(), st)
+    torch.cuda.synchronize()
+    best = 0.0
+    for it in (1000, 2000):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _native.call("fhe_peak_tc_i8", 148, it, usink.data_ptr(), st)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 148 * it * 8 * 2 * 128 * 256 * 32 / (e0.elapsed_time(e1) * 1e-3))
+    res["tc_i8_ops"] = best
     return res
 
 
@@ -286,6 +299,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sub", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA-graph replay")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -304,46 +318,86 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl")
-    from paper_2401_16732_b200 import _native, conv
+    from paper_2401_16732_b200 import _native, conv, device
 
     P, layers = build_stack(args.workload, seed=4 + rank)
     flush = torch.empty(2**25, dtype=torch.int64, device="cuda")  # 256 MiB
 
-    def step():
+    tc_layers = [L for L in layers if L["plan"].path == "tc"]
+    mma_ev = {id(L): (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for L in tc_layers}
+    for pair in mma_ev.values():  # torch creates the cudaEvent_t lazily, on first record
+        for e in pair:
+            e.record()
+
+    def step(instrument=False):
+        """One pass of every conv layer; with `instrument`, CUDA events bracket
+        each tensor-core GEMM launch (captured into the graph as event nodes)."""
         for L in layers:
-            L["plan"].run(L["dev"], L["out"])
+            plan = L["plan"]
+            if instrument and id(L) in mma_ev:
+                e0, e1 = mma_ev[id(L)]
+                rec = _native.fn("fhe_record_event")
+                plan.tc.run(L["dev"], L["out"], mark=lambda: rec(e0.cuda_event, device.stream()))
+                rec(e1.cuda_event, device.stream())
+            else:
+                plan.run(L["dev"], L["out"])
 
     peaks = run_peaks() if rank == 0 else {}
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    sampler = ClockSampler(local)
-    sampler.start()
-    launches0 = _native.launch_count()
-    torch.cuda.synchronize()
-    # per-layer events inside the timed region (dominant-kernel roofline)
+    # per-layer breakdown (eager launches, events between layers; informational)
     layer_ms = np.zeros(len(layers))
-    step_ms = []
-    for _ in range(args.steps):
+    for _ in range(3):
         flush_l2(flush)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 1)]
         evs[0].record()
         for i, L in enumerate(layers):
             L["plan"].run(L["dev"], L["out"])
             evs[i + 1].record()
-        step_ms.append(evs)
+        torch.cuda.synchronize()
+        layer_ms += [evs[i].elapsed_time(evs[i + 1]) / 3 for i in range(len(layers))]
+    # the timed step: one CUDA-graph replay of every layer's launches
+    launches0 = _native.launch_count()
+    if args.no_graph:
+        def run_step():
+            step(instrument=True)
+    else:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        launches0 = _native.launch_count()
+        with torch.cuda.graph(graph):
+            step(instrument=True)
+        run_step = graph.replay
+        for _ in range(args.warmup):
+            run_step()
+    launches_per_step = _native.launch_count() - launches0
     torch.cuda.synchronize()
-    launches = _native.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    step_ms = []
+    for _ in range(args.steps):
+        flush_l2(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_step()
+        e1.record()
+        step_ms.append((e0, e1))
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    per_step = []
-    for evs in step_ms:
-        d = [evs[i].elapsed_time(evs[i + 1]) for i in range(len(layers))]
-        layer_ms += d
-        per_step.append(sum(d))
+    launches = launches_per_step * args.steps
+    per_step = [a.elapsed_time(b) for a, b in step_ms]
     total_ms = sum(per_step)
     t_max = total_ms
     if world > 1:
@@ -358,8 +412,13 @@ def main():
     if rank == 0:
         macs = sum(L["macs"] for L in layers)
         alg_bytes = sum(L["bytes"] for L in layers)
-        k1_s = layer_ms.sum() / args.steps * 1e-3
-        achieved_tmac = macs / k1_s / 1e12
+        step_s = ms_per_step * 1e-3
+        # dominant kernel: the tcgen05 GEMM of every tensor-core layer, timed by
+        # the event nodes captured around it (last timed replay)
+        mma_s = sum(mma_ev[id(L)][0].elapsed_time(mma_ev[id(L)][1]) for L in tc_layers) * 1e-3
+        tc_ops = sum(16 * L["macs"] for L in tc_layers)  # 8 byte planes x (mul + add)
+        achieved_tops = tc_ops / mma_s / 1e12 if mma_s else 0.0
+        peak_tops = peaks["tc_i8_ops"] / 1e12
         peak_tmac = peaks["imad_wide"] / 2 / 1e12  # 2 IMAD.WIDE per 60-bit x 8-bit MAC
         result = {
             "metric": METRIC, "value": round(value, 3), "unit": "conv layers/s", "n_gpus": world,
@@ -370,16 +429,25 @@ def main():
                        if args.workload == "config4" else args.workload,
                        "conv_layers": n_layers, "macs_60x8": macs, "n": P.n, "q_bits": P.q.bit_length(),
                        "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas x{world}"},
-            "roofline": {"bound": "int", "kernel": "conv_flash_kernel (K1, IMAD.WIDE)",
-                         "achieved": round(achieved_tmac, 4), "peak": round(peak_tmac, 4), "unit": "TMAC60/s",
-                         "frac": round(achieved_tmac / peak_tmac, 4),
-                         "peak_source": "measured here: fhe_peak_imad_wide (register-resident mad.wide.s32)/2",
-                         "hbm_achieved_gbs": round(alg_bytes / k1_s / 1e9, 1), "hbm_peak_gbs": hbm,
-                         "hbm_peak_source": hbm_kind, "traffic": None},
+            "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (K1-TC, tcgen05.mma.kind::i8)",
+                         "achieved": round(achieved_tops, 2), "peak": round(peak_tops, 2), "unit": "TOPS (int8)",
+                         "frac": round(achieved_tops / peak_tops, 4) if peak_tops else None,
+                         "peak_source": "measured here: fhe_peak_tc_i8 (dense M128 N256 K32 kind::i8 MMAs, "
+                                        "resident smem operands)",
+                         "kernel_share_of_step": round(mma_s / step_s, 4),
+                         "alg": "16 int8 ops per 60-bit x 8-bit MAC (8 byte planes); MACs = c_o*frags*c_i*f_w^2*2n",
+                         "traffic": None,
+                         "stack_tmac60_per_s": round(macs / step_s / 1e12, 3),
+                         "int_pipe_peak_tmac60_per_s": round(peak_tmac, 3),
+                         "stack_vs_int_pipe_peak": round(macs / step_s / 1e12 / peak_tmac, 3),
+                         "hbm_achieved_gbs": round(alg_bytes / step_s / 1e9, 1), "hbm_peak_gbs": hbm,
+                         "hbm_peak_source": hbm_kind},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "peaks_measured": {k: v for k, v in peaks.items()},
-            "per_layer_ms": {L["layer"].name: round(float(m) / args.steps, 4) for L, m in zip(layers, layer_ms)},
+            "per_layer_ms_eager": {L["layer"].name: round(float(m), 4) for L, m in zip(layers, layer_ms)},
+            "timing": "value: CUDA-graph replay of the whole stack per step" if not args.no_graph
+                      else "value: eager launches",
         }
     if world > 1:
         dist.barrier()

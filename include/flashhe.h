@@ -53,6 +53,9 @@ const char* fhe_last_error(void);
 int fhe_abi_version(void);
 /* number of kernel launches issued by this library since load (instrumentation) */
 uint64_t fhe_launch_count(void);
+/* cudaEventRecord that stays timeable inside a CUDA-graph capture
+ * (external event node); used by the benchmark's kernel-level timing. */
+int fhe_record_event(void* event, void* stream);
 
 /* Roofline micro-benchmarks (register-resident, no memory traffic):
  * blocks*threads*iters*16 IMAD.WIDE (mad.wide.s32), and
@@ -60,6 +63,9 @@ uint64_t fhe_launch_count(void);
 int fhe_peak_imad_wide(int blocks, int threads, int iters, int64_t* sink, void* stream);
 int fhe_peak_butterfly(int blocks, int threads, int iters, uint64_t q, uint64_t* sink,
                        void* stream);
+/* blocks*iters*8 dense tcgen05.mma.kind::i8 (M=128, N=256, K=32) on resident
+ * shared-memory operands: 2*128*256*32 int8 ops each. */
+int fhe_peak_tc_i8(int blocks, int iters, uint32_t* sink, void* stream);
 
 /* ------------------------------------------------- plans (ring.NttPlan) */
 /* Host-only (no GPU needed). ring.NttPlan._find_root (ring.py:121-127):
@@ -174,16 +180,18 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
  *  fhe_conv_tc_prep: input ciphertexts [n_in][2][n] -> digit-plane operand X
  *    [2][frags][ceil(c_i/32)][n + 2h][256 B] (channel-aligned negacyclic
  *    extension, UMMA core-matrix order); X must hold that many bytes.
- *  fhe_conv_tc: X (+ weights packed [ceil(c_o/128)][ceil(c_i/32)][taps][16][256 B]
- *    int8, |w| <= 127) -> out [c_o*frags][2][n], canonical mod q, bias fused.
- * tap_steps_host: HOST int32 [taps], each in [-h, h]. c_n/tile: channel
- * packing of the input layout (conv.py:113-130); frags > 1 = fragmented. */
-int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int c_n, int tile,
-                     int h, uint8_t* X, void* stream);
+ *  fhe_conv_tc: X (+ weights packed [ceil(c_o/n_tile)][ceil(c_i/32)][taps][n_tile/8][256 B]
+ *    int8, |w| <= 127; n_tile 64 or 128) -> out [c_o*frags][2][n], canonical
+ *    mod q, bias fused.
+ * chan: DEVICE int32 pairs [c_i][2] = (source ct, slot shift) of channel j
+ * (conv.py:113-130 packing); fragment f reads source + f*fstride.
+ * tap_steps_host: HOST int32 [taps], each in [-h, h]. */
+int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride,
+                     const int32_t* chan, int h, uint8_t* X, void* stream);
 int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h,
-                const int8_t* Wpacked, int c_o, int taps, const int32_t* tap_steps_host,
-                const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
-                void* stream);
+                const int8_t* Wpacked, int c_o, int taps, int n_tile,
+                const int32_t* tap_steps_host, const uint64_t* bias_delta,
+                const uint8_t* bias_mask, uint64_t* out, void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

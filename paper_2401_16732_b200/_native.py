@@ -39,8 +39,10 @@ SIGNATURES = {
     "fhe_last_error": (ctypes.c_char_p, []),
     "fhe_abi_version": (_int, []),
     "fhe_launch_count": (_u64, []),
+    "fhe_record_event": (_int, [_vp, _vp]),
     "fhe_peak_imad_wide": (_int, [_int, _int, _int, _vp, _vp]),
     "fhe_peak_butterfly": (_int, [_int, _int, _int, _u64, _vp, _vp]),
+    "fhe_peak_tc_i8": (_int, [_int, _int, _vp, _vp]),
     "fhe_find_root": (_int, [_int, _u64, _vp]),
     "fhe_plan_tables_host": (_int, [_int, _u64, _vp, _vp, _vp]),
     "fhe_plan_create": (_int, [_int, _u64, _PP]),
@@ -67,8 +69,8 @@ SIGNATURES = {
         [_u64, _int, _vp, _int, _vp, _int, _int, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp],
     ),
     "fhe_conv_check_budget": (_int, [_vp, _int, _int]),
-    "fhe_conv_tc_prep": (_int, [_u64, _int, _vp, _int, _int, _int, _int, _int, _vp, _vp]),
-    "fhe_conv_tc": (_int, [_u64, _int, _vp, _int, _int, _int, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fhe_conv_tc_prep": (_int, [_u64, _int, _vp, _int, _int, _int, _vp, _int, _vp, _vp]),
+    "fhe_conv_tc": (_int, [_u64, _int, _vp, _int, _int, _int, _vp, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "fhe_to_montgomery": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_keyswitch_apply": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _int, _u64, _vp, _vp]),
     "fhe_act_client_square": (_int, [_u64, _int, _i64, _vp, _vp, _vp]),
@@ -105,8 +107,21 @@ def check(rc: int) -> None:
         raise _ERRORS.get(rc, RuntimeError)(msg)
 
 
+_fns: dict = {}
+
+
+def fn(name: str):
+    """The bound ctypes function (cached: the hot path avoids getattr per call)."""
+    f = _fns.get(name)
+    if f is None:
+        f = _fns[name] = getattr(lib(), name)
+    return f
+
+
 def call(name: str, *args) -> None:
-    check(getattr(lib(), name)(*args))
+    rc = fn(name)(*args)
+    if rc:
+        check(rc)
 
 
 def u64_array(values) -> ctypes.Array:

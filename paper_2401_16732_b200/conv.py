@@ -288,42 +288,60 @@ class ConvTcPlan:
     operand buffer X and the tap steps. Eligible when |w| ≤ 127, ≥ 16 input
     channels, n a multiple of 64 and the halo window fits shared memory."""
 
-    N_TILE = 128
-    S_CTA = 64
+    @staticmethod
+    def tile_for(c_o: int) -> int:
+        """Output-channel tile: 64 (8 accumulators x 16 positions) or 128 (4 x 16)."""
+        return 64 if c_o <= 64 else 128
 
     @staticmethod
     def eligible(weights3d: np.ndarray, n: int, h: int, taps: int) -> bool:
         c_o, c_i, _ = weights3d.shape
-        if c_i < 16 or n < 64 or n % 64 or taps > 64 or int(np.abs(weights3d).max(initial=0)) > 127:
+        N = ConvTcPlan.tile_for(c_o)
+        S = 16 * (512 // N)
+        if c_i < 16 or n < S or n % S or taps > 64 or int(np.abs(weights3d).max(initial=0)) > 127:
             return False
-        a_bytes = -(-(ConvTcPlan.S_CTA + 2 * h) * 256 // 1024) * 1024
-        return 2 * (a_bytes + taps * ConvTcPlan.N_TILE * 32) + 64 <= 227 * 1024
+        a_bytes = -(-(S + 2 * h) * 256 // 1024) * 1024
+        return 2 * (a_bytes + taps * N * 32) + 64 <= 227 * 1024
 
     def __init__(self, q: int, n: int, weights3d: np.ndarray, steps: np.ndarray, layout: TileLayout,
                  bias, mask):
         self.q, self.n = int(q), int(n)
         self.c_o, self.c_i, self.taps = weights3d.shape
         self.h = int(np.abs(steps).max(initial=0))
-        self.frags, self.c_n, self.tile = layout.frags, layout.c_n, layout.tile
-        N = self.N_TILE
+        self.frags = layout.frags
+        N = self.n_tile = self.tile_for(self.c_o)
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
+        j = np.arange(self.c_i)
+        if layout.fragmented:
+            chan, self.fstride = np.stack([j * layout.frags, np.zeros_like(j)], 1), 1
+        else:
+            chan, self.fstride = np.stack([j // layout.c_n, layout.tile * (j % layout.c_n)], 1), 0
         wp = np.zeros((OB * N, JB * 32, self.taps), dtype=np.int8)
         wp[: self.c_o, : self.c_i] = weights3d
         # [ob][jb][tap][g][kh][r][jj] with o = ob*N + g*8 + r, j = jb*32 + kh*16 + jj
         wp = wp.reshape(OB, N // 8, 8, JB, 2, 16, self.taps).transpose(0, 3, 6, 1, 4, 2, 5)
         dev = device.require_cuda()
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
+        self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
         self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
         self.X = torch.empty(2 * self.frags * JB * (n + 2 * self.h) * 256, dtype=torch.uint8, device=dev)
         self.bias, self.mask = bias, mask
 
-    def run(self, inp: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
+        """prep (digit planes) then the tcgen05 GEMM; `mark()` (e.g. a CUDA
+        event record) runs between the two launches when given."""
         st = device.stream()
-        _native.call("fhe_conv_tc_prep", self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.c_n,
-                     self.tile, self.h, self.X.data_ptr(), st)
-        _native.call("fhe_conv_tc", self.q, self.n, self.X.data_ptr(), self.c_i, self.frags, self.h,
-                     self.w.data_ptr(), self.c_o, self.taps, self.steps, device.ptr(self.bias),
-                     device.ptr(self.mask), out.data_ptr(), st)
+        rc = _native.fn("fhe_conv_tc_prep")(self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.fstride,
+                                            self.chan.data_ptr(), self.h, self.X.data_ptr(), st)
+        if rc:
+            _native.check(rc)
+        if mark is not None:
+            mark()
+        rc = _native.fn("fhe_conv_tc")(self.q, self.n, self.X.data_ptr(), self.c_i, self.frags, self.h,
+                                       self.w.data_ptr(), self.c_o, self.taps, self.n_tile, self.steps,
+                                       device.ptr(self.bias), device.ptr(self.mask), out.data_ptr(), st)
+        if rc:
+            _native.check(rc)
         return out
 
 

@@ -17,17 +17,19 @@
 // no-swizzle K-major core-matrix order (8 rows x 16 B), so each pipeline
 // stage is two 1-D bulk copies (cp.async.bulk -> mbarrier complete_tx).
 //
-// CTA = 128 threads: thread 0 issues bulk copies and MMAs (single-thread
-// tcgen05 issue), all 4 warps run the epilogue: tcgen05.ld of the s32 plane
-// sums, a shared-memory transpose, V = lo + 2^32 hi recombination and one
-// canonical reduction mod q per coefficient (+ the fused bias of plain_add).
+// CTA = 256 threads: thread 0 issues bulk copies and MMAs (single-thread
+// tcgen05 issue), all 8 warps run the epilogue: tcgen05.ld of the s32 plane
+// sums (warp w: TMEM lane quadrant w%4, column half w/4), a column-major
+// shared-memory transpose, V = lo + 2^32 hi recombination and one canonical
+// reduction mod q per coefficient (+ the fused bias of plain_add).
 #include "common.cuh"
 
 namespace fhe {
 namespace tc {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;
 constexpr int kMaxTaps = 64;
+constexpr int kEStride = 128 + 8;  // epilogue staging column stride (int32, 16-B aligned)
 
 struct TcArgs {
   const uint8_t* X;   // [2][F][JB][Y][256]  prepared digit planes
@@ -109,10 +111,10 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 template <int N, int NACC>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int S = 16 * NACC;          // positions per CTA
-  constexpr int TM_COLS = N * NACC;     // TMEM columns (power of 2 required)
+  constexpr int S = 16 * NACC;       // positions per CTA
+  constexpr int TM_COLS = N * NACC;  // TMEM columns (power of 2 required)
   static_assert(TM_COLS == 32 || TM_COLS == 64 || TM_COLS == 128 || TM_COLS == 256 || TM_COLS == 512, "tmem");
-  constexpr int ESTRIDE = N + 4;        // epilogue staging row stride (int32)
+  static_assert(N % 64 == 0, "epilogue splits N into two halves of 32-column chunks");
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s0 = blockIdx.x * S;
@@ -183,32 +185,37 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   mbar_wait(acc_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
+  // Staging is column-major (stage[col][row], row = position*8 + plane): the
+  // TMEM->smem stores are 32 consecutive words per warp and each output's 8
+  // planes are two aligned 16-byte loads.
   int32_t* stage = reinterpret_cast<int32_t*>(smem);  // reuse the operand buffers
   const uint64_t q = a.m.q;
+  const int quad = warp & 3, half = warp >> 2;
+  const int row = quad * 32 + lane;
+  constexpr int HALF = N / 2;
+  constexpr int PER_THREAD = 16 * N / kThreads;
   for (int mi = 0; mi < NACC; ++mi) {
-    // TMEM -> smem: warp w owns lanes 32w..32w+31 = rows (position, plane)
-    const int row = warp * 32 + lane;
-#pragma unroll 1
-    for (int c0 = 0; c0 < N; c0 += 32) {
+#pragma unroll
+    for (int c0 = half * HALF; c0 < (half + 1) * HALF; c0 += 32) {
       uint32_t v[32];
-      TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + mi * N + c0, v);
+      TMEM_LD32(tmem + ((uint32_t)(quad * 32) << 16) + mi * N + c0, v);
       asm volatile("tcgen05.wait::ld.sync.aligned;");
 #pragma unroll
-      for (int c = 0; c < 32; ++c) stage[row * ESTRIDE + c0 + c] = (int32_t)v[c];
+      for (int c = 0; c < 32; ++c) stage[(c0 + c) * kEStride + row] = (int32_t)v[c];
     }
     __syncthreads();
     // recombine the 8 planes of each (position, channel) and reduce mod q
-#pragma unroll 1
-    for (int idx = tid; idx < 16 * N; idx += kThreads) {
+#pragma unroll
+    for (int k = 0; k < PER_THREAD; ++k) {
+      const int idx = tid + k * kThreads;
       const int sp = idx & 15, col = idx >> 4;
       const int o = ob * N + col;
       const int s = s0 + mi * 16 + sp;
       if (o < a.c_o && s < a.n) {
-        const int32_t* e = stage + sp * 8 * ESTRIDE + col;
-        long long lo = (long long)e[0] + ((long long)e[ESTRIDE] << 8) + ((long long)e[2 * ESTRIDE] << 16) +
-                       ((long long)e[3 * ESTRIDE] << 24);
-        long long hi = (long long)e[4 * ESTRIDE] + ((long long)e[5 * ESTRIDE] << 8) +
-                       ((long long)e[6 * ESTRIDE] << 16) + ((long long)e[7 * ESTRIDE] << 24);
+        const int4* e4 = reinterpret_cast<const int4*>(stage + col * kEStride + sp * 8);
+        const int4 e0 = e4[0], e1 = e4[1];
+        long long lo = (long long)e0.x + ((long long)e0.y << 8) + ((long long)e0.z << 16) + ((long long)e0.w << 24);
+        long long hi = (long long)e1.x + ((long long)e1.y << 8) + ((long long)e1.z << 16) + ((long long)e1.w << 24);
         const uint64_t l = reduce_i64(lo, a.m), hh = reduce_i64(hi, a.m);
         uint64_t val = csub(l + csub(shoup_lazy(hh, a.w32, a.w32p, q), q), q);
         if (p == 0 && a.bias) {
@@ -227,64 +234,122 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 
 // ------------------------------------------------------------- relayout
 // X[p][f][jb][y][kh][d][16]: digit d of channel j = jb*32 + kh*16 + jj at
-// extension slot (n - h + y + shift_j) of its source ciphertext.
-__global__ void prep_kernel(const uint64_t* __restrict__ in, uint8_t* __restrict__ X, int n, int Y, int JB,
-                            int F, int c_i, int h, int fragmented, int c_n, int tile, uint64_t q, int64_t total) {
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= total) return;
-  const int kh = (int)(gid & 1);
-  int64_t r = gid >> 1;
-  const int y = (int)(r % Y);
-  r /= Y;
-  const int jb = (int)(r % JB);
-  r /= JB;
-  const int f = (int)(r % F);
-  const int p = (int)(r / F);
-  uint32_t planes[8][4];
-#pragma unroll
-  for (int d = 0; d < 8; ++d)
-#pragma unroll
-    for (int w = 0; w < 4; ++w) planes[d][w] = 0;
+// extension slot (n - h + y + shift_j) of source ciphertext src_j + f*fstride.
+// chan[j] = (src_j, shift_j) (the channel packing of conv.py:113-130).
+// grid: x over (y, kh) pairs, y = jb, z = p*F + f — no runtime divisions.
+__global__ void __launch_bounds__(256) prep_kernel(const uint64_t* __restrict__ in, uint8_t* __restrict__ X,
+                                                   const int2* __restrict__ chan, int n, int Y, int F, int c_i,
+                                                   int h, int fstride, uint64_t q) {
+  const int yk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (yk >= 2 * Y) return;
+  const int y = yk >> 1, kh = yk & 1;
+  const int jb = blockIdx.y, JB = gridDim.y;
+  const int pf = blockIdx.z, p = pf / F, f = pf - p * F;
+  const int ebase = n - h + y;
+  uint2 v[16];
 #pragma unroll
   for (int jj = 0; jj < 16; ++jj) {
     const int j = jb * 32 + kh * 16 + jj;
-    uint64_t v = 0;
+    uint64_t x = 0;
     if (j < c_i) {
-      const int src = fragmented ? j * F + f : j / c_n;
-      const int shift = fragmented ? 0 : tile * (j % c_n);
-      int e = n - h + y + shift;  // in [0, 3n)
-      int neg = 0;
-      if (e < n) {
-        neg = 1;
-      } else if (e >= 2 * n) {
-        e -= 2 * n;
-        neg = 1;
-      } else {
-        e -= n;
-      }
-      const uint64_t x = __ldg(&in[((size_t)src * 2 + p) * n + e]);
-      v = (neg && x) ? q - x : x;
+      const int2 cs = __ldg(&chan[j]);
+      int e = ebase + cs.y;  // in [0, 3n)
+      const bool lo = e < n, hi = e >= 2 * n;
+      e -= lo ? 0 : (hi ? 2 * n : n);
+      x = __ldg(&in[((size_t)(cs.x + f * fstride) * 2 + p) * n + e]);
+      x = ((lo || hi) && x) ? q - x : x;
     }
-#pragma unroll
-    for (int d = 0; d < 8; ++d) planes[d][jj >> 2] |= (uint32_t)((v >> (8 * d)) & 0xff) << (8 * (jj & 3));
+    v[jj] = make_uint2((uint32_t)x, (uint32_t)(x >> 32));
   }
-  uint4* dst = reinterpret_cast<uint4*>(X + ((((size_t)(p * F + f) * JB + jb) * Y + y) * 256 + kh * 128));
+  uint4* dst = reinterpret_cast<uint4*>(X + ((((size_t)pf * JB + jb) * Y + y) * 256 + kh * 128));
 #pragma unroll
-  for (int d = 0; d < 8; ++d) dst[d] = make_uint4(planes[d][0], planes[d][1], planes[d][2], planes[d][3]);
+  for (int d = 0; d < 8; ++d) {
+    const unsigned sel = (unsigned)(d & 3) | ((unsigned)((d & 3) + 4) << 4);
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t a0 = d < 4 ? v[4 * k].x : v[4 * k].y, a1 = d < 4 ? v[4 * k + 1].x : v[4 * k + 1].y;
+      const uint32_t a2 = d < 4 ? v[4 * k + 2].x : v[4 * k + 2].y, a3 = d < 4 ? v[4 * k + 3].x : v[4 * k + 3].y;
+      const uint32_t t0 = __byte_perm(a0, a1, sel), t1 = __byte_perm(a2, a3, sel);
+      w[k] = __byte_perm(t0, t1, 0x5410);
+    }
+    dst[d] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
 }
 
 template <int N, int NACC>
-static int launch(const TcArgs& a, int n, int OB, cudaStream_t st) {
+static int launch(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
+  constexpr int S = 16 * NACC;
+  if (a.n % S) return fail(FHE_ERR_VALUE, "n must be a multiple of %d for the tc path", S);
+  for (int t = 0; t < a.taps; ++t) {
+    const int off = tap_steps_host[t] + a.h;
+    if (off < 0 || off > 2 * a.h) return fail(FHE_ERR_VALUE, "tap step outside the halo");
+    a.tap_off[t] = off;
+  }
+  a.a_bytes = ((S + 2 * a.h) * 256 + 1023) / 1024 * 1024;
+  a.stage_bytes = a.a_bytes + a.taps * N * 32;
+  const size_t epi = (size_t)N * kEStride * 4;
+  if ((size_t)2 * a.stage_bytes < epi) a.stage_bytes = (int)((epi + 1) / 2 + 1023) / 1024 * 1024;
   const size_t smem = 2 * (size_t)a.stage_bytes + 64;
+  if (smem > 227 * 1024) return fail(FHE_ERR_VALUE, "halo too large for the tc path");
   static bool attr = false;
   if (!attr) {
     FHE_CUDA(cudaFuncSetAttribute(conv_tc_kernel<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  dim3 grid(n / (16 * NACC), OB, 2 * a.F);
+  dim3 grid(a.n / S, (a.c_o + N - 1) / N, 2 * a.F);
   conv_tc_kernel<N, NACC><<<grid, kThreads, smem, st>>>(a);
   FHE_CHECK_LAUNCH("conv_tc_kernel");
   return FHE_OK;
+}
+
+// Largest position tile that still gives >= 1.5 waves of CTAs on 148 SMs.
+template <int N, int NACC_BIG, int NACC_SMALL>
+static int run_tile(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
+  const long ctas_big = (long)(a.n / (16 * NACC_BIG)) * ((a.c_o + N - 1) / N) * 2 * a.F;
+  if (ctas_big >= 222) return launch<N, NACC_BIG>(a, tap_steps_host, st);
+  return launch<N, NACC_SMALL>(a, tap_steps_host, st);
+}
+
+// Dense int8 tcgen05 roofline probe: back-to-back M=128 N=256 K=32 MMAs on
+// resident shared-memory operands (no loads, no epilogue).
+__global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, uint32_t* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 12288);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + 12296);
+  for (int i = threadIdx.x; i < 12288 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (i & 3);
+  asm volatile("fence.proxy.async.shared::cta;");
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 0) {
+    const uint64_t ad = umma_desc(smem_u32(smem)), bd = umma_desc(smem_u32(smem + 4096));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_i8<256>(tmem + (k & 1) * 256, ad, bd, 1);
+    }
+    mma_commit(smem_u32(bar));
+  }
+  mbar_wait(smem_u32(bar), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (threadIdx.x < 32) {
+    uint32_t v[32];
+    TMEM_LD32(tmem + ((uint32_t)(threadIdx.x & ~31) << 16), v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (v[0] == 0x5eed) sink[0] = v[1];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 }  // namespace tc
@@ -294,28 +359,35 @@ using namespace fhe;
 
 extern "C" {
 
-int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int c_n, int tile, int h,
-                     uint8_t* X, void* stream) {
-  if (n < 64 || (n & (n - 1)) || c_i < 1 || frags < 1 || c_n < 1 || h < 0 || h >= n || !in || !X)
+int fhe_peak_tc_i8(int blocks, int iters, uint32_t* sink, void* stream) {
+  if (blocks < 1 || iters < 1 || !sink) return fail(FHE_ERR_VALUE, "bad peak arguments");
+  tc::peak_tc_kernel<<<blocks, 128, 12288 + 64, (cudaStream_t)stream>>>(iters, sink);
+  FHE_CHECK_LAUNCH("peak_tc_kernel");
+  return FHE_OK;
+}
+
+int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride, const int32_t* chan,
+                     int h, uint8_t* X, void* stream) {
+  if (n < 64 || (n & (n - 1)) || c_i < 1 || frags < 1 || h < 0 || h >= n || !in || !X || !chan)
     return fail(FHE_ERR_VALUE, "bad tc prep arguments");
   const int JB = (c_i + 31) / 32, Y = n + 2 * h;
-  const int64_t total = (int64_t)2 * frags * JB * Y * 2;
-  tc::prep_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      in, X, n, Y, JB, frags, c_i, h, frags > 1 ? 1 : 0, c_n, tile, q, total);
+  if (JB > 65535 || 2 * frags > 65535) return fail(FHE_ERR_VALUE, "tc prep grid too large");
+  dim3 grid((unsigned)((2 * Y + 255) / 256), JB, 2 * frags);
+  tc::prep_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, X, reinterpret_cast<const int2*>(chan), n, Y, frags,
+                                                          c_i, h, fstride, q);
   FHE_CHECK_LAUNCH("tc prep_kernel");
   return FHE_OK;
 }
 
 int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h, const int8_t* Wpacked, int c_o,
-                int taps, const int32_t* tap_steps_host, const uint64_t* bias_delta, const uint8_t* bias_mask,
-                uint64_t* out, void* stream) {
+                int taps, int n_tile, const int32_t* tap_steps_host, const uint64_t* bias_delta,
+                const uint8_t* bias_mask, uint64_t* out, void* stream) {
   ModSet ms;
   if (int rc = make_modset(&q, 1, &ms)) return rc;
   if (n < 64 || (n & (n - 1)) || c_i < 1 || frags < 1 || c_o < 1 || taps < 1 || taps > tc::kMaxTaps)
     return fail(FHE_ERR_VALUE, "bad tc conv arguments");
   if (!X || !Wpacked || !out || !tap_steps_host) return fail(FHE_ERR_VALUE, "null tc operand");
   if (bias_delta && !bias_mask) return fail(FHE_ERR_VALUE, "bias needs a mask");
-  constexpr int N = 128, NACC = 4;
   tc::TcArgs a;
   a.X = X;
   a.W = reinterpret_cast<const uint8_t*>(Wpacked);
@@ -332,19 +404,10 @@ int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h, 
   a.c_o = c_o;
   a.taps = taps;
   a.h = h;
-  for (int t = 0; t < taps; ++t) {
-    const int off = tap_steps_host[t] + h;
-    if (off < 0 || off > 2 * h) return fail(FHE_ERR_VALUE, "tap step outside the halo");
-    a.tap_off[t] = off;
-  }
-  const int S = 16 * NACC;
-  a.a_bytes = ((S + 2 * h) * 256 + 1023) / 1024 * 1024;
-  a.stage_bytes = a.a_bytes + taps * N * 32;
-  const size_t epi = (size_t)128 * (N + 4) * 4;
-  if ((size_t)2 * a.stage_bytes < epi) a.stage_bytes = (int)((epi + 1) / 2 + 1023) / 1024 * 1024;
-  if (2 * (size_t)a.stage_bytes + 64 > 227 * 1024) return fail(FHE_ERR_VALUE, "halo too large for the tc path");
-  const int OB = (c_o + N - 1) / N;
-  return tc::launch<N, NACC>(a, n, OB, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_tile == 64) return tc::run_tile<64, 8, 4>(a, tap_steps_host, st);
+  if (n_tile == 128) return tc::run_tile<128, 4, 2>(a, tap_steps_host, st);
+  return fail(FHE_ERR_VALUE, "n_tile must be 64 or 128");
 }
 
 }  // extern "C"

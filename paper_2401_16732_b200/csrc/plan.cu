@@ -77,6 +77,16 @@ const char* fhe_last_error(void) { return g_err.c_str(); }
 int fhe_abi_version(void) { return 1; }
 uint64_t fhe_launch_count(void) { return g_launches.load(); }
 
+int fhe_record_event(void* event, void* stream) {
+  // external event-record node when captured into a CUDA graph, so the
+  // timing survives graph replay; a plain record otherwise
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FHE_CUDA(cudaStreamIsCapturing((cudaStream_t)stream, &cap));
+  const unsigned flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  FHE_CUDA(cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream, flags));
+  return FHE_OK;
+}
+
 int fhe_find_root(int n, uint64_t q, uint64_t* psi_out) {
   int lg;
   if (int rc = check_nq(n, q, &lg)) return rc;

@@ -352,6 +352,7 @@ def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> C
     cache = layer.__dict__.setdefault("_k1_plans", {})
     if key in cache:
         return cache[key]
+    _check_budget(layer.weights.reshape(layer.c_o, -1))
     taps = layer.f_w * layer.f_w
     steps = _tap_steps(layout, layer.f_w)
     j = np.repeat(np.arange(layer.c_i), taps)
@@ -399,8 +400,7 @@ def conv_proposed(x: PackedTensor, layer: ConvLayerSpec, params: RingParams, laz
         raise ParameterError("convolution input must not carry a pending stride")
     if x.cts[0].encoding != Encoding.DIRECT:
         raise EncodingError("proposed convolution needs direct-encoded input")
-    _check_budget(layer.weights.reshape(layer.c_o, -1))
-    plan = conv_plan(layer, layout, params)
+    plan = conv_plan(layer, layout, params)  # runs _check_budget before caching a plan
     out = plan.run(bfv.cts_rows(x.cts))
     cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
     return PackedTensor(cts, replace(layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)

@@ -71,22 +71,54 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 
 class DeviceRows:
-    """A device tensor of polynomial rows [R, n] plus a lazily fetched host
-    mirror (one bulk device->host copy serves every row)."""
+    """A stack of polynomial rows [R, n] living on the device, on the host, or
+    both. Whichever side is missing is filled by ONE bulk copy through pinned
+    host memory, so a whole ciphertext batch crosses PCIe as a single DMA in
+    either direction."""
 
-    __slots__ = ("dev", "_host")
+    __slots__ = ("_dev", "_host", "_pinned")
 
-    def __init__(self, dev: torch.Tensor):
-        self.dev = dev.reshape(-1, dev.shape[-1])
-        self._host = None
+    def __init__(self, dev: torch.Tensor | None = None, host: np.ndarray | None = None, pinned=None):
+        self._dev = None if dev is None else dev.reshape(-1, dev.shape[-1])
+        self._host = host
+        self._pinned = pinned
+
+    @classmethod
+    def from_host(cls, arr: np.ndarray, pin: bool = True) -> "DeviceRows":
+        """Host-first stack; with `pin`, the rows are copied once into
+        page-locked memory so the later upload is a single async DMA."""
+        arr = np.asarray(arr, dtype=np.int64)
+        arr = arr.reshape(-1, arr.shape[-1])
+        if not pin:
+            return cls(host=arr)
+        t = torch.empty(arr.shape, dtype=torch.int64, pin_memory=True)
+        h = t.numpy()
+        h[...] = arr
+        return cls(host=h, pinned=t)
+
+    def device(self) -> torch.Tensor:
+        if self._dev is None:
+            src = self._pinned if self._pinned is not None else torch.from_numpy(
+                np.ascontiguousarray(self._host) if self._host.flags.writeable else self._host.copy())
+            self._dev = src.to(require_cuda(), non_blocking=self._pinned is not None)
+        return self._dev
+
+    dev = property(device)
 
     def host(self) -> np.ndarray:
         if self._host is None:
-            h = self.dev.cpu().numpy()
+            t = torch.empty(self._dev.shape, dtype=torch.int64, pin_memory=True)
+            t.copy_(self._dev, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            h = t.numpy()
             h.flags.writeable = False
-            self._host = h
+            self._host, self._pinned = h, t
         return self._host
 
     @property
     def rows(self) -> int:
-        return self.dev.shape[0]
+        return (self._dev if self._dev is not None else self._host).shape[0]
+
+    @property
+    def n(self) -> int:
+        return int((self._dev if self._dev is not None else self._host).shape[-1])

@@ -101,7 +101,7 @@ class ModPoly:
         if self._rows is None:
             self._rows = DeviceRows(device.to_device(self._host).reshape(1, -1))
             self._row = 0
-        return self._rows.dev[self._row]
+        return self._rows.device()[self._row]
 
     @property
     def on_device(self) -> bool:
@@ -111,7 +111,7 @@ class ModPoly:
     def n(self) -> int:
         if self._host is not None:
             return len(self._host)
-        return int(self._rows.dev.shape[-1])
+        return self._rows.n
 
     def copy(self) -> "ModPoly":
         if self._host is not None:
@@ -149,7 +149,7 @@ def gather_rows(polys) -> torch.Tensor:
     if first is not None and all(p._rows is first for p in polys):
         i0 = polys[0]._row
         if all(p._row == i0 + k for k, p in enumerate(polys)):
-            return first.dev[i0 : i0 + len(polys)]
+            return first.device()[i0 : i0 + len(polys)]
     if all(p._rows is None for p in polys):
         return device.to_device(np.stack([p._host for p in polys]))
     return torch.stack([p.dev() for p in polys])

@@ -159,19 +159,20 @@ def run_peaks():
             ops = blocks * threads * it * per
             best = max(best, ops / (e0.elapsed_time(e1) * 1e-3))
         res[name] = best
-    # dense int8 tcgen05 (M=128, N=256, K=32), one CTA per SM
+    # dense int8 tcgen05 (M=128, N=256/128/64, K=32), one CTA per SM
     usink = torch.zeros(4, dtype=torch.int32, device="cuda")
-    _native.call("fhe_peak_tc_i8", 148, 16, usink.data_ptr(), st)
-    torch.cuda.synchronize()
-    best = 0.0
-    for it in (1000, 2000):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _native.call("fhe_peak_tc_i8", 148, it, usink.data_ptr(), st)
-        e1.record()
+    for N in (256, 128, 64):
+        _native.call("fhe_peak_tc_i8", 148, N, 16, usink.data_ptr(), st)
         torch.cuda.synchronize()
-        best = max(best, 148 * it * 8 * 2 * 128 * 256 * 32 / (e0.elapsed_time(e1) * 1e-3))
-    res["tc_i8_ops"] = best
+        best = 0.0
+        for it in (1000, 2000):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _native.call("fhe_peak_tc_i8", 148, N, it, usink.data_ptr(), st)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 148 * it * 8 * 2 * 128 * N * 32 / (e0.elapsed_time(e1) * 1e-3))
+        res["tc_i8_ops" if N == 256 else f"tc_i8_ops_n{N}"] = best
     return res
 
 

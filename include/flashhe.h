@@ -56,6 +56,9 @@ uint64_t fhe_launch_count(void);
 /* cudaEventRecord that stays timeable inside a CUDA-graph capture
  * (external event node); used by the benchmark's kernel-level timing. */
 int fhe_record_event(void* event, void* stream);
+/* Timeline instrumentation of the K1-TC pipeline: CTA 0 records clock64() at
+ * its pipeline events into dev_buf (8 kinds x 4096 uint64); NULL disables. */
+int fhe_debug_trace(void* dev_buf);
 
 /* Roofline micro-benchmarks (register-resident, no memory traffic):
  * blocks*threads*iters*16 IMAD.WIDE (mad.wide.s32), and
@@ -63,9 +66,10 @@ int fhe_record_event(void* event, void* stream);
 int fhe_peak_imad_wide(int blocks, int threads, int iters, int64_t* sink, void* stream);
 int fhe_peak_butterfly(int blocks, int threads, int iters, uint64_t q, uint64_t* sink,
                        void* stream);
-/* blocks*iters*8 dense tcgen05.mma.kind::i8 (M=128, N=256, K=32) on resident
- * shared-memory operands: 2*128*256*32 int8 ops each. */
-int fhe_peak_tc_i8(int blocks, int iters, uint32_t* sink, void* stream);
+/* blocks*iters*8 dense tcgen05.mma.kind::i8 (M=128, N=n_tile, K=32; n_tile
+ * 64, 128 or 256) on resident shared-memory operands: 2*128*n_tile*32 int8
+ * ops each. */
+int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stream);
 
 /* ------------------------------------------------- plans (ring.NttPlan) */
 /* Host-only (no GPU needed). ring.NttPlan._find_root (ring.py:121-127):
@@ -176,20 +180,24 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
                    const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
                    void* stream);
 /* K1-TC: the same contraction on tcgen05.mma.kind::i8 (u8 digit planes x s8
- * weights -> s32, 8 planes recombined exactly mod q). Two launches:
- *  fhe_conv_tc_prep: input ciphertexts [n_in][2][n] -> digit-plane operand X
- *    [2][frags][ceil(c_i/32)][n + 2h][256 B] (channel-aligned negacyclic
- *    extension, UMMA core-matrix order); X must hold that many bytes.
- *  fhe_conv_tc: X (+ weights packed [ceil(c_o/n_tile)][ceil(c_i/32)][taps][n_tile/8][256 B]
- *    int8, |w| <= 127; n_tile 64 or 128) -> out [c_o*frags][2][n], canonical
- *    mod q, bias fused.
+ * weights -> s32, 8 planes recombined exactly mod q). Two launches per layer.
+ *
+ * fhe_conv_tc_prep: in [n_in][2][n] -> X, the digit-plane operand
+ *   uint8 [2][frags][ceil(c_i/32)][n + 2h][256 B] (UMMA core-matrix order:
+ *   window position y <-> extension slot n - h + y of each channel).
  * chan: DEVICE int32 pairs [c_i][2] = (source ct, slot shift) of channel j
- * (conv.py:113-130 packing); fragment f reads source + f*fstride.
- * tap_steps_host: HOST int32 [taps], each in [-h, h]. */
+ *   (the channel packing of conv.py:113-130); fragment f reads source + f*fstride. */
 int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride,
                      const int32_t* chan, int h, uint8_t* X, void* stream);
+/* fhe_conv_tc: X -> out [c_o*frags][2][n], canonical mod q, bias fused; one
+ * persistent warp-specialised launch (one CTA per SM). GEMM tile: 128 output
+ * channels x pos_tile (16 or 32) positions, 32 input channels per stage.
+ * Wpacked: int8 [ceil(c_o/128)][ceil(c_i/32)][taps][16][256 B] (UMMA
+ *   core-matrix order: 8 output channels x 16 input channels per 128 B),
+ *   |w| <= 127, 127*255*ceil32(c_i)*taps < 2^31; requires 2^56 <= q < 2^62.
+ * tap_steps_host: HOST int32 [taps] DRot steps, each in [-h, h]. */
 int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h,
-                const int8_t* Wpacked, int c_o, int taps, int n_tile,
+                const int8_t* Wpacked, int c_o, int taps, int pos_tile,
                 const int32_t* tap_steps_host, const uint64_t* bias_delta,
                 const uint8_t* bias_mask, uint64_t* out, void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):

@@ -40,9 +40,10 @@ SIGNATURES = {
     "fhe_abi_version": (_int, []),
     "fhe_launch_count": (_u64, []),
     "fhe_record_event": (_int, [_vp, _vp]),
+    "fhe_debug_trace": (_int, [_vp]),
     "fhe_peak_imad_wide": (_int, [_int, _int, _int, _vp, _vp]),
     "fhe_peak_butterfly": (_int, [_int, _int, _int, _u64, _vp, _vp]),
-    "fhe_peak_tc_i8": (_int, [_int, _int, _vp, _vp]),
+    "fhe_peak_tc_i8": (_int, [_int, _int, _int, _vp, _vp]),
     "fhe_find_root": (_int, [_int, _u64, _vp]),
     "fhe_plan_tables_host": (_int, [_int, _u64, _vp, _vp, _vp]),
     "fhe_plan_create": (_int, [_int, _u64, _PP]),

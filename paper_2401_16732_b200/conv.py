@@ -286,22 +286,38 @@ def _conv_path() -> str:
 class ConvTcPlan:
     """K1-TC operands (csrc/conv_tc.cu): packed int8 weights, the digit-plane
     operand buffer X and the tap steps. Eligible when |w| ≤ 127, ≥ 16 input
-    channels, n a multiple of 64 and the halo window fits shared memory."""
+    channels, 2^56 ≤ q, n a multiple of 64 and the halo window fits shared
+    memory. GEMM tile: 128 output channels × `pos_tile` positions."""
+
+    OC_TILE = 128  # output channels per tile (tcgen05 M)
+    SMS = 148  # B200 SM count (tile-size heuristic only)
 
     @staticmethod
-    def tile_for(c_o: int) -> int:
-        """Output-channel tile: 64 (8 accumulators x 16 positions) or 128 (4 x 16)."""
-        return 64 if c_o <= 64 else 128
+    def _fits(pos_tile: int, h: int, taps: int) -> bool:
+        win = -(-(pos_tile + 2 * h) * 256 // 1024) * 1024
+        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 214 * 1024  # >= 2 pipeline stages
 
     @staticmethod
-    def eligible(weights3d: np.ndarray, n: int, h: int, taps: int) -> bool:
+    def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int) -> int:
+        """32 positions per tile, or 16 when that leaves fewer than two tiles
+        per SM (small layers are epilogue-latency bound) and still fits."""
+        tiles = (n // 32) * -(-c_o // ConvTcPlan.OC_TILE) * 2 * frags
+        if tiles < 2 * ConvTcPlan.SMS or not ConvTcPlan._fits(32, h, taps):
+            return 16
+        return 32
+
+    @staticmethod
+    def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
         c_o, c_i, _ = weights3d.shape
-        N = ConvTcPlan.tile_for(c_o)
-        S = 16 * (512 // N)
-        if c_i < 16 or n < S or n % S or taps > 64 or int(np.abs(weights3d).max(initial=0)) > 127:
+        if c_i < 16 or n < 64 or n % 64 or taps > 64 or 2 * h >= n:
             return False
-        a_bytes = -(-(S + 2 * h) * 256 // 1024) * 1024
-        return 2 * (a_bytes + taps * N * 32) + 64 <= 227 * 1024
+        if int(np.abs(weights3d).max(initial=0)) > 127:
+            return False
+        if 127 * 255 * (-(-c_i // 32) * 32) * taps >= 1 << 31:  # exact s32 plane sums
+            return False
+        if not (1 << 56) <= q < (1 << 62):  # single-offset epilogue reduction (csrc/conv_tc.cu)
+            return False
+        return ConvTcPlan._fits(16, h, taps)
 
     def __init__(self, q: int, n: int, weights3d: np.ndarray, steps: np.ndarray, layout: TileLayout,
                  bias, mask):
@@ -309,7 +325,8 @@ class ConvTcPlan:
         self.c_o, self.c_i, self.taps = weights3d.shape
         self.h = int(np.abs(steps).max(initial=0))
         self.frags = layout.frags
-        N = self.n_tile = self.tile_for(self.c_o)
+        self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps)
+        N = self.OC_TILE
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
         j = np.arange(self.c_i)
         if layout.fragmented:
@@ -318,28 +335,33 @@ class ConvTcPlan:
             chan, self.fstride = np.stack([j // layout.c_n, layout.tile * (j % layout.c_n)], 1), 0
         wp = np.zeros((OB * N, JB * 32, self.taps), dtype=np.int8)
         wp[: self.c_o, : self.c_i] = weights3d
-        # [ob][jb][tap][g][kh][r][jj] with o = ob*N + g*8 + r, j = jb*32 + kh*16 + jj
+        # [ob][jb][tap][g][kh][r][jj] with o = ob*128 + g*8 + r, j = jb*32 + kh*16 + jj
         wp = wp.reshape(OB, N // 8, 8, JB, 2, 16, self.taps).transpose(0, 3, 6, 1, 4, 2, 5)
         dev = device.require_cuda()
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
         self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
         self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
-        self.X = torch.empty(2 * self.frags * JB * (n + 2 * self.h) * 256, dtype=torch.uint8, device=dev)
         self.bias, self.mask = bias, mask
 
+    @property
+    def x_bytes(self) -> int:
+        """Size of the digit-plane operand X: [2][frags][JB][n + 2h][256 B]."""
+        return 2 * self.frags * (-(-self.c_i // 32)) * (self.n + 2 * self.h) * 256
+
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
-        """prep (digit planes) then the tcgen05 GEMM; `mark()` (e.g. a CUDA
-        event record) runs between the two launches when given."""
+        """Relayout (prep) launch, then one persistent tcgen05 launch; `mark()`
+        (e.g. a CUDA event record) runs between the two when given."""
         st = device.stream()
+        X = device.scratch("conv_tc_x", self.x_bytes)
         rc = _native.fn("fhe_conv_tc_prep")(self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.fstride,
-                                            self.chan.data_ptr(), self.h, self.X.data_ptr(), st)
+                                            self.chan.data_ptr(), self.h, X, st)
         if rc:
             _native.check(rc)
         if mark is not None:
             mark()
-        rc = _native.fn("fhe_conv_tc")(self.q, self.n, self.X.data_ptr(), self.c_i, self.frags, self.h,
-                                       self.w.data_ptr(), self.c_o, self.taps, self.n_tile, self.steps,
-                                       device.ptr(self.bias), device.ptr(self.mask), out.data_ptr(), st)
+        rc = _native.fn("fhe_conv_tc")(self.q, self.n, X, self.c_i, self.frags, self.h, self.w.data_ptr(),
+                                       self.c_o, self.taps, self.pos_tile, self.steps, device.ptr(self.bias),
+                                       device.ptr(self.mask), out.data_ptr(), st)
         if rc:
             _native.check(rc)
         return out
@@ -369,7 +391,7 @@ def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> C
     plan = ConvPlan(params.q, params.n, layer.weights.reshape(layer.c_o, -1), src, step,
                     frags=layout.frags, fstride=fstride, bias_delta=bias_delta, bias_mask=bias_mask)
     h = int(np.abs(steps).max(initial=0))
-    if ConvTcPlan.eligible(layer.weights, params.n, h, taps):
+    if ConvTcPlan.eligible(layer.weights, params.q, params.n, h, taps):
         plan.tc = ConvTcPlan(params.q, params.n, layer.weights, steps, layout, plan.bias, plan.mask)
     cache[key] = plan
     return plan

@@ -66,6 +66,21 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
     return t.to(require_cuda())
 
 
+_scratch: dict[tuple[int, str], torch.Tensor] = {}
+
+
+def scratch(name: str, nbytes: int) -> int:
+    """Device pointer to a named per-device scratch buffer of >= nbytes.
+    Reuse is stream-ordered (every kernel runs on torch's current stream); the
+    buffer only grows, so pointers baked into a captured CUDA graph stay valid
+    once the largest user has run eagerly."""
+    key = (torch.cuda.current_device(), name)
+    t = _scratch.get(key)
+    if t is None or t.numel() < nbytes:
+        t = _scratch[key] = torch.empty(int(nbytes), dtype=torch.uint8, device=require_cuda())
+    return t.data_ptr()
+
+
 def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 

@@ -1,9 +1,10 @@
-"""Per-kernel timing of the K1-TC path (prep vs MMA kernel) on config-4 layers.
+"""Per-layer timing of K1 (tensor-core or integer path) on the config-4 layers.
 
 Development probe (not part of the product or the bench contract):
-    python tools/probe_tc.py
+    python tools/probe_tc.py [--layer NAME] [--once]
 """
 
+import argparse
 import sys
 from pathlib import Path
 
@@ -12,65 +13,47 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
-from paper_2401_16732_b200 import _native, conv, device, params, stacks  # noqa: E402
-
-
-def ev():
-    return torch.cuda.Event(enable_timing=True)
+from paper_2401_16732_b200 import conv, params, stacks  # noqa: E402
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layer", default=None, help="only this config-4 layer name")
+    ap.add_argument("--once", action="store_true", help="one launch per layer (for ncu)")
+    args = ap.parse_args()
     P = params.default_params()
     rng = np.random.default_rng(0)
     seen = set()
     for l in stacks.conv_layers(stacks.config4()):
         key = (l.H, l.f_w, l.c_i, l.c_o)
-        if key in seen:
+        if key in seen or (args.layer and l.name != args.layer):
             continue
         seen.add(key)
         lay = conv.layout_direct(P, l.H, l.W, l.f_w)
         w = rng.integers(-127, 128, (l.c_o, l.c_i, l.f_w, l.f_w))
-        spec = conv.ConvLayerSpec(l.H, l.W, l.f_w, l.c_i, l.c_o, w)
-        plan = conv.conv_plan(spec, lay, P)
+        plan = conv.conv_plan(conv.ConvLayerSpec(l.H, l.W, l.f_w, l.c_i, l.c_o, w), lay, P)
         inp = torch.from_numpy(rng.integers(0, P.q, (lay.ct_count(l.c_i), 2, P.n))).cuda()
         out = torch.empty((plan.n_out, 2, P.n), dtype=torch.int64, device="cuda")
-        if plan.tc is None:
-            plan.run(inp, out)
-            torch.cuda.synchronize()
-            e0, e1 = ev(), ev()
-            e0.record()
+        plan.run(inp, out)
+        torch.cuda.synchronize()
+        if args.once:
+            print(l.name, "ran once via", plan.path)
+            continue
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
             for _ in range(10):
                 plan.run(inp, out)
-            e1.record()
-            torch.cuda.synchronize()
-            print(f"{l.name:10s} int  total {e0.elapsed_time(e1) / 10 * 1e3:8.1f} us")
-            continue
-        tc = plan.tc
-        st = device.stream()
-
-        def prep():
-            _native.call("fhe_conv_tc_prep", tc.q, tc.n, inp.data_ptr(), tc.c_i, tc.frags, tc.fstride,
-                         tc.chan.data_ptr(), tc.h, tc.X.data_ptr(), st)
-
-        def mma():
-            _native.call("fhe_conv_tc", tc.q, tc.n, tc.X.data_ptr(), tc.c_i, tc.frags, tc.h, tc.w.data_ptr(),
-                         tc.c_o, tc.taps, tc.n_tile, tc.steps, None, None, out.data_ptr(), st)
-
-        prep()
-        mma()
+        g.replay()
         torch.cuda.synchronize()
-        res = []
-        for fn in (prep, mma):
-            e0, e1 = ev(), ev()
-            e0.record()
-            for _ in range(10):
-                fn()
-            e1.record()
-            torch.cuda.synchronize()
-            res.append(e0.elapsed_time(e1) / 10 * 1e3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 10 * 1e3
         macs = plan.n_out * plan.K * 2 * P.n
-        print(f"{l.name:10s} tc N={tc.n_tile:3d} prep {res[0]:7.1f} us  mma {res[1]:7.1f} us  "
-              f"X {tc.X.numel() / 1e6:6.1f} MB  {macs / res[1] / 1e6:7.1f} TMAC60/s(mma)")
+        print(f"{l.name:10s} {plan.path:3s} {us:8.1f} us  {macs / us / 1e6:7.1f} TMAC60/s  "
+              f"{16 * macs / us / 1e6:8.1f} int8 TOPS-equiv")
 
 
 if __name__ == "__main__":

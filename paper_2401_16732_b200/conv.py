@@ -415,6 +415,13 @@ def conv_proposed(x: PackedTensor, layer: ConvLayerSpec, params: RingParams, laz
     and fragment at once, one modular reduction per coefficient. `lazy` and
     `workers` are accepted for API compatibility; the result is the same
     canonical ciphertext either way (as in the reference)."""
+    plan = _proposed_plan(x, layer, params)
+    out = plan.run(bfv.cts_rows(x.cts))
+    cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+    return PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)
+
+
+def _proposed_plan(x: PackedTensor, layer: ConvLayerSpec, params: RingParams) -> ConvPlan:
     layout = x.layout
     if (layout.height, layout.width) != (layer.height, layer.width) or layout.pad != layer.f_w // 2:
         raise ParameterError("tensor layout does not match the layer geometry")
@@ -422,10 +429,45 @@ def conv_proposed(x: PackedTensor, layer: ConvLayerSpec, params: RingParams, laz
         raise ParameterError("convolution input must not carry a pending stride")
     if x.cts[0].encoding != Encoding.DIRECT:
         raise EncodingError("proposed convolution needs direct-encoded input")
-    plan = conv_plan(layer, layout, params)  # runs _check_budget before caching a plan
-    out = plan.run(bfv.cts_rows(x.cts))
-    cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
-    return PackedTensor(cts, replace(layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)
+    return conv_plan(layer, layout, params)  # runs _check_budget before caching a plan
+
+
+_copy_streams: dict[int, tuple] = {}
+
+
+def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
+    """Serving form of conv_proposed over a sequence of independent
+    (PackedTensor, ConvLayerSpec) jobs — e.g. one layer of many requests, or
+    many layers' pending inputs. Each job's upload, K1 launches and download
+    run on three CUDA streams (upload copy engine, SMs, download copy engine)
+    so job i+1's upload and job i-1's download overlap job i's convolution.
+
+    Inputs may be host- (ideally pinned, see bfv.cts_from_host) or device-
+    resident. Outputs are canonical ciphertexts resident on both sides: the
+    host copies (pinned) are complete when this returns. Results are exactly
+    those of conv_proposed on each job."""
+    dev = device.require_cuda()
+    comp = torch.cuda.current_stream()
+    up, down = _copy_streams.setdefault(dev.index, (torch.cuda.Stream(), torch.cuda.Stream()))
+    prepared = []
+    for x, layer in jobs:  # validate everything before enqueueing anything
+        prepared.append((x, layer, _proposed_plan(x, layer, params)))
+    outs = []
+    for x, layer, plan in prepared:
+        if isinstance(x.cts, bfv.CtStack):
+            inp, ev = x.cts.rows.upload_on(up)
+            if ev is not None:
+                comp.wait_event(ev)
+                inp.record_stream(comp)
+        else:
+            inp = bfv.cts_rows(x.cts).reshape(-1, params.n)
+        out = plan.run(inp.reshape(-1, 2, params.n))
+        down.wait_stream(comp)
+        rows = device.DeviceRows.download_on(out, down)
+        cts = bfv.CtStack(rows, params.q, Encoding.DIRECT, Domain.COEFF)
+        outs.append(PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale))
+    down.synchronize()
+    return outs
 
 
 def _bias_plaintext(layout: TileLayout, frag: int, value: int, params: RingParams):

@@ -336,20 +336,40 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
 // ------------------------------------------------------------- relayout
 // X[p][f][jb][y][kh][d][16]: digit d of channel j = jb*32 + kh*16 + jj at
 // extension slot (n - h + y + shift_j) of source ciphertext src_j + f*fstride.
-// A CTA converts 32 window positions x 32 channels: coalesced loads (lane =
-// position) into a shared [position][channel] tile, then each thread packs two
-// planes of 16 channels and a warp stores 4 complete 256-byte positions.
-__global__ void __launch_bounds__(256) prep_kernel(const uint64_t* __restrict__ in, uint8_t* __restrict__ X,
-                                                   const int2* __restrict__ chan, int n, int Y, int F, int c_i,
-                                                   int h, int fstride, uint64_t q) {
-  __shared__ uint64_t raw[32][33];  // [position][channel] (+1 pad)
-  const int y0 = blockIdx.x * 32, jb = blockIdx.y, JB = gridDim.y;
+// A CTA (128 threads) converts kPrepY window positions x 32 channels in three
+// phases (many small CTAs per SM hide the load latency):
+//  1. coalesced 8-byte loads (lane = position, warp = 8 channels) into a
+//     shared [position][channel] tile, negacyclic sign applied on the fly;
+//  2. thread (position, K half, low/high word) byte-transposes 16 coefficients
+//     into 4 plane words x 4 (4x4 PRMT transposes) and stages 64 B in shared
+//     memory (16-byte chunks XOR-swizzled by position: conflict-free);
+//  3. the CTA streams the staged 8 KB to X with fully coalesced 16 B stores.
+constexpr int kPrepY = 32;
+constexpr int kPrepThreads = 128;
+
+__device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t& p0,
+                                             uint32_t& p1, uint32_t& p2, uint32_t& p3) {
+  const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a0, a1, 0x7362);
+  const uint32_t t2 = __byte_perm(a2, a3, 0x5140), t3 = __byte_perm(a2, a3, 0x7362);
+  p0 = __byte_perm(t0, t2, 0x5410);
+  p1 = __byte_perm(t0, t2, 0x7632);
+  p2 = __byte_perm(t1, t3, 0x5410);
+  p3 = __byte_perm(t1, t3, 0x7632);
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const uint64_t* __restrict__ in,
+                                                            uint8_t* __restrict__ X, const int2* __restrict__ chan,
+                                                            int n, int Y, int F, int c_i, int h, int fstride,
+                                                            uint64_t q) {
+  __shared__ __align__(16) uint64_t raw[kPrepY][33];  // [position][channel] (+1 pad); reused for staging
+  const int y0 = blockIdx.x * kPrepY, jb = blockIdx.y, JB = gridDim.y;
   const int pf = blockIdx.z, p = pf / F, f = pf - p * F;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // load: warp w handles channels 4w..4w+3, lane = position
+  // 1. load: warp w handles channels 8w..8w+7
+  const int y = y0 + lane;
 #pragma unroll
-  for (int cc = 0; cc < 4; ++cc) {
-    const int jl = warp * 4 + cc, j = jb * 32 + jl, y = y0 + lane;
+  for (int cc = 0; cc < 8; ++cc) {
+    const int jl = warp * 8 + cc, j = jb * 32 + jl;
     uint64_t x = 0;
     if (j < c_i && y < Y) {
       const int2 cs = __ldg(&chan[j]);
@@ -362,33 +382,29 @@ __global__ void __launch_bounds__(256) prep_kernel(const uint64_t* __restrict__ 
     raw[lane][jl] = x;
   }
   __syncthreads();
-  // pack: thread -> (position, K half, plane pair)
-  const int t = threadIdx.x;
-  const int yl = t >> 3, kh = (t >> 2) & 1, part = t & 3;
-  const int y = y0 + yl;
-  if (y >= Y) return;
-  uint32_t w[2][4];
+  // 2. pack: thread -> (position yl, K half kh, word half wh): planes 4wh..4wh+3
+  const int yl = threadIdx.x >> 2, kh = (threadIdx.x >> 1) & 1, wh = threadIdx.x & 1;
+  uint32_t w[4][4];
 #pragma unroll
   for (int g4 = 0; g4 < 4; ++g4) {
-    uint64_t v[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = raw[yl][kh * 16 + g4 * 4 + c];
-#pragma unroll
-    for (int dd = 0; dd < 2; ++dd) {
-      const int d = 2 * part + dd;
-      const unsigned sel = (unsigned)(d & 3) | ((unsigned)((d & 3) + 4) << 4);
-      const uint32_t a0 = d < 4 ? (uint32_t)v[0] : (uint32_t)(v[0] >> 32);
-      const uint32_t a1 = d < 4 ? (uint32_t)v[1] : (uint32_t)(v[1] >> 32);
-      const uint32_t a2 = d < 4 ? (uint32_t)v[2] : (uint32_t)(v[2] >> 32);
-      const uint32_t a3 = d < 4 ? (uint32_t)v[3] : (uint32_t)(v[3] >> 32);
-      w[dd][g4] = __byte_perm(__byte_perm(a0, a1, sel), __byte_perm(a2, a3, sel), 0x5410);
-    }
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(&raw[yl][kh * 16 + g4 * 4]) + wh;
+    transpose4x4(r[0], r[2], r[4], r[6], w[0][g4], w[1][g4], w[2][g4], w[3][g4]);
   }
-  uint4* dst = reinterpret_cast<uint4*>(X + ((((size_t)pf * JB + jb) * Y + y) * 256 + kh * 128 + 2 * part * 16));
-  dst[0] = make_uint4(w[0][0], w[0][1], w[0][2], w[0][3]);
-  dst[1] = make_uint4(w[1][0], w[1][1], w[1][2], w[1][3]);
+  __syncthreads();
+  uint4* stage = reinterpret_cast<uint4*>(&raw[0][0]);  // [position][16 chunks of 16 B], chunk ^= yl & 7
+#pragma unroll
+  for (int dd = 0; dd < 4; ++dd)
+    stage[yl * 16 + kh * 8 + ((4 * wh + dd) ^ (yl & 7))] = make_uint4(w[dd][0], w[dd][1], w[dd][2], w[dd][3]);
+  __syncthreads();
+  // 3. coalesced copy-out of the CTA's contiguous [kPrepY][256 B] slab
+  const int rows = min(kPrepY, Y - y0);
+  uint4* dst = reinterpret_cast<uint4*>(X + (((size_t)pf * JB + jb) * Y + y0) * 256);
+#pragma unroll
+  for (int i = 0; i < kPrepY * 16 / kPrepThreads; ++i) {
+    const int idx = threadIdx.x + kPrepThreads * i, pos = idx >> 4, ch = idx & 15;
+    if (pos < rows) dst[idx] = stage[pos * 16 + (ch & 8) + ((ch & 7) ^ (pos & 7))];
+  }
 }
-
 
 template <int NPOS>
 static int launch(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
@@ -498,8 +514,8 @@ int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, 
     return fail(FHE_ERR_VALUE, "bad tc prep arguments");
   const int JB = (c_i + 31) / 32, Y = n + 2 * h;
   if (JB > 65535 || 2 * frags > 65535) return fail(FHE_ERR_VALUE, "tc prep grid too large");
-  dim3 grid((unsigned)((Y + 31) / 32), JB, 2 * frags);
-  tc::prep_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(in, X, reinterpret_cast<const int2*>(chan), n, Y, frags,
+  dim3 grid((unsigned)((Y + tc::kPrepY - 1) / tc::kPrepY), JB, 2 * frags);
+  tc::prep_kernel<<<grid, tc::kPrepThreads, 0, (cudaStream_t)stream>>>(in, X, reinterpret_cast<const int2*>(chan), n, Y, frags,
                                                           c_i, h, fstride, q);
   FHE_CHECK_LAUNCH("tc prep_kernel");
   return FHE_OK;

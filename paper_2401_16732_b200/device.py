@@ -130,6 +130,37 @@ class DeviceRows:
             self._host, self._pinned = h, t
         return self._host
 
+    def upload_on(self, stream: torch.cuda.Stream) -> tuple[torch.Tensor, torch.cuda.Event | None]:
+        """Device rows, uploading on `stream` if they are host-only: returns
+        (tensor, event the consumer must wait on; None if already resident).
+        The tensor is allocated on `stream`; callers using it on another
+        stream keep it alive until that stream is done (record_stream)."""
+        if self._dev is not None:
+            return self._dev, None
+        if self._pinned is None:  # pageable host rows: stage once through pinned memory
+            t = torch.empty(self._host.shape, dtype=torch.int64, pin_memory=True)
+            t.numpy()[...] = self._host
+            self._pinned = t
+        with torch.cuda.stream(stream):
+            self._dev = self._pinned.to(require_cuda(), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return self._dev, ev
+
+    @classmethod
+    def download_on(cls, dev: torch.Tensor, stream: torch.cuda.Stream) -> "DeviceRows":
+        """Rows whose host copy is filled by a pinned D2H enqueued on `stream`
+        (the caller orders `stream` after the producer and synchronizes it
+        before reading the host side)."""
+        dev = dev.reshape(-1, dev.shape[-1])
+        t = torch.empty(dev.shape, dtype=torch.int64, pin_memory=True)
+        with torch.cuda.stream(stream):
+            t.copy_(dev, non_blocking=True)
+        dev.record_stream(stream)
+        h = t.numpy()
+        h.flags.writeable = False
+        return cls(dev=dev, host=h, pinned=t)
+
     @property
     def rows(self) -> int:
         return (self._dev if self._dev is not None else self._host).shape[0]

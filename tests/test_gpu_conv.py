@@ -103,6 +103,27 @@ def test_conv_tc_vs_oracle(case, monkeypatch):
     assert np.array_equal(y_tc[sel], ref)
 
 
+def test_conv_proposed_stream_matches_single_calls():
+    """The overlapped serving API gives exactly conv_proposed's ciphertexts,
+    for host-resident (pinned and pageable) and device-resident inputs."""
+    from paper_2401_16732_b200 import bfv, conv
+
+    P = _P()
+    rng = np.random.default_rng(77)
+    jobs, refs = [], []
+    for k, (H, f_w, c_i, c_o) in enumerate([(16, 3, 32, 40), (8, 3, 64, 130), (32, 1, 24, 16), (16, 3, 3, 8)]):
+        lay = conv.layout_direct(P, H, H, f_w)
+        arr = rng.integers(0, Q, (lay.ct_count(c_i), 2, N), dtype=np.int64)
+        spec = conv.ConvLayerSpec(H, H, f_w, c_i, c_o, rng.integers(-127, 128, (c_o, c_i, f_w, f_w)))
+        refs.append(_out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, c_i), spec, P).cts))
+        cts = _cts(arr) if k == 2 else bfv.cts_from_host(arr, Q, pin=(k != 1))
+        jobs.append((conv.PackedTensor(cts, lay, c_i), spec))
+    outs = conv.conv_proposed_stream(jobs, P)
+    for y, ref in zip(outs, refs):
+        assert np.array_equal(y.cts.host_stack(), ref)
+        assert np.array_equal(_out(y.cts), ref)
+
+
 def test_conv_cfg1_full_arrays():
     from paper_2401_16732_b200 import conv
 

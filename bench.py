@@ -331,18 +331,19 @@ def main():
         for e in pair:
             e.record()
 
+    rec = _native.fn("fhe_record_event")
+
     def step(instrument=False):
-        """One pass of every conv layer; with `instrument`, CUDA events bracket
-        each tensor-core GEMM launch (captured into the graph as event nodes)."""
-        for L in layers:
-            plan = L["plan"]
+        """One pass of every conv layer (independent inputs): K1 per layer, the
+        relayout of layer i+1 on a side stream beside the GEMM of layer i
+        (conv.issue_k1). With `instrument`, CUDA events bracket each
+        tensor-core GEMM launch (captured into the graph as event nodes)."""
+        def on_gemm(i, what):
+            L = layers[i]
             if instrument and id(L) in mma_ev:
-                e0, e1 = mma_ev[id(L)]
-                rec = _native.fn("fhe_record_event")
-                plan.tc.run(L["dev"], L["out"], mark=lambda: rec(e0.cuda_event, device.stream()))
-                rec(e1.cuda_event, device.stream())
-            else:
-                plan.run(L["dev"], L["out"])
+                rec(mma_ev[id(L)][0 if what == "start" else 1].cuda_event, device.stream())
+
+        conv.issue_k1([(L["plan"], L["dev"], None, L["out"]) for L in layers], on_gemm=on_gemm)
 
     peaks = run_peaks() if rank == 0 else {}
     for _ in range(args.warmup):
@@ -447,8 +448,9 @@ def main():
             "clocks": clocks,
             "peaks_measured": {k: v for k, v in peaks.items()},
             "per_layer_ms_eager": {L["layer"].name: round(float(m), 4) for L, m in zip(layers, layer_ms)},
-            "timing": "value: CUDA-graph replay of the whole stack per step" if not args.no_graph
-                      else "value: eager launches",
+            "timing": ("value: CUDA-graph replay of the whole stack per step" if not args.no_graph
+                       else "value: eager launches") + "; layers are independent inputs, the relayout of layer "
+                      "i+1 runs on a side stream beside the GEMM of layer i (conv.issue_k1)",
         }
     if world > 1:
         dist.barrier()

@@ -180,26 +180,27 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
                    const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
                    void* stream);
 /* K1-TC: the same contraction on tcgen05.mma.kind::i8 (u8 digit planes x s8
- * weights -> s32, 8 planes recombined exactly mod q). Two launches per layer.
- *
- * fhe_conv_tc_prep: in [n_in][2][n] -> X, the digit-plane operand
- *   uint8 [2][frags][ceil(c_i/32)][n + 2h][256 B] (UMMA core-matrix order:
- *   window position y <-> extension slot n - h + y of each channel).
+ * weights -> s32, 8 planes recombined exactly mod q): in [n_in][2][n] ->
+ * out [c_o*frags][2][n], canonical mod q, bias fused. One cooperative,
+ * persistent launch (one CTA per SM) in two phases separated by a grid
+ * barrier: (1) relayout of the input into the digit-plane operand X,
+ * uint8 [2][frags][ceil(c_i/32)][n + 2h][256 B] (UMMA core-matrix order);
+ * (2) warp-specialised tcgen05 GEMM, tile = 128 output channels x pos_tile
+ * (16 or 32) positions, 32 input channels per pipeline stage.
  * chan: DEVICE int32 pairs [c_i][2] = (source ct, slot shift) of channel j
- *   (the channel packing of conv.py:113-130); fragment f reads source + f*fstride. */
-int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride,
-                     const int32_t* chan, int h, uint8_t* X, void* stream);
-/* fhe_conv_tc: X -> out [c_o*frags][2][n], canonical mod q, bias fused; one
- * persistent warp-specialised launch (one CTA per SM). GEMM tile: 128 output
- * channels x pos_tile (16 or 32) positions, 32 input channels per stage.
+ *   (the channel packing of conv.py:113-130); fragment f reads source + f*fstride.
+ * X: DEVICE scratch of the size above.
  * Wpacked: int8 [ceil(c_o/128)][ceil(c_i/32)][taps][16][256 B] (UMMA
  *   core-matrix order: 8 output channels x 16 input channels per 128 B),
  *   |w| <= 127, 127*255*ceil32(c_i)*taps < 2^31; requires 2^56 <= q < 2^62.
- * tap_steps_host: HOST int32 [taps] DRot steps, each in [-h, h]. */
-int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h,
-                const int8_t* Wpacked, int c_o, int taps, int pos_tile,
-                const int32_t* tap_steps_host, const uint64_t* bias_delta,
-                const uint8_t* bias_mask, uint64_t* out, void* stream);
+ * tap_steps_host: HOST int32 [taps] DRot steps, each in [-h, h].
+ * sync: DEVICE uint64, zeroed once before first use (grid-barrier arrival
+ *   counter; do not share between launches that may run concurrently). */
+int fhe_conv_tc(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride,
+                const int32_t* chan, int h, uint8_t* X, const int8_t* Wpacked, int c_o,
+                int taps, int pos_tile, const int32_t* tap_steps_host,
+                const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
+                uint64_t* sync, void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

@@ -285,9 +285,10 @@ def _conv_path() -> str:
 
 class ConvTcPlan:
     """K1-TC operands (csrc/conv_tc.cu): packed int8 weights, the digit-plane
-    operand buffer X and the tap steps. Eligible when |w| ≤ 127, ≥ 16 input
-    channels, 2^56 ≤ q, n a multiple of 64 and the halo window fits shared
-    memory. GEMM tile: 128 output channels × `pos_tile` positions."""
+    operand buffer X and the tap steps. Eligible when |w| ≤ 127, 2^56 ≤ q,
+    n a multiple of 64 and the halo window fits shared memory (input channels
+    are zero-padded to a multiple of 32). GEMM tile: 128 output channels ×
+    `pos_tile` positions."""
 
     OC_TILE = 128  # output channels per tile (tcgen05 M)
     SMS = 148  # B200 SM count (tile-size heuristic only)
@@ -295,7 +296,7 @@ class ConvTcPlan:
     @staticmethod
     def _fits(pos_tile: int, h: int, taps: int) -> bool:
         win = -(-(pos_tile + 2 * h) * 256 // 1024) * 1024
-        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 214 * 1024  # >= 2 pipeline stages
+        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 204 * 1024  # >= 2 pipeline stages
 
     @staticmethod
     def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int) -> int:
@@ -309,7 +310,7 @@ class ConvTcPlan:
     @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
         c_o, c_i, _ = weights3d.shape
-        if c_i < 16 or n < 64 or n % 64 or taps > 64 or 2 * h >= n:
+        if n < 64 or n % 64 or taps > 64 or 2 * h >= n:
             return False
         if int(np.abs(weights3d).max(initial=0)) > 127:
             return False
@@ -341,6 +342,7 @@ class ConvTcPlan:
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
         self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
         self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
+        self.sync = torch.zeros(1, dtype=torch.int64, device=dev)  # grid-barrier counter of this plan's launches
         self.bias, self.mask = bias, mask
 
     @property
@@ -349,22 +351,59 @@ class ConvTcPlan:
         return 2 * self.frags * (-(-self.c_i // 32)) * (self.n + 2 * self.h) * 256
 
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
-        """Relayout (prep) launch, then one persistent tcgen05 launch; `mark()`
-        (e.g. a CUDA event record) runs between the two when given."""
-        st = device.stream()
+        """One cooperative persistent launch (relayout phase, grid barrier,
+        tcgen05 GEMM phase); `mark()` (e.g. a CUDA event record) runs right
+        before it when given."""
         X = device.scratch("conv_tc_x", self.x_bytes)
-        rc = _native.fn("fhe_conv_tc_prep")(self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.fstride,
-                                            self.chan.data_ptr(), self.h, X, st)
-        if rc:
-            _native.check(rc)
         if mark is not None:
             mark()
-        rc = _native.fn("fhe_conv_tc")(self.q, self.n, X, self.c_i, self.frags, self.h, self.w.data_ptr(),
-                                       self.c_o, self.taps, self.pos_tile, self.steps, device.ptr(self.bias),
-                                       device.ptr(self.mask), out.data_ptr(), st)
+        rc = _native.fn("fhe_conv_tc")(self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.fstride,
+                                       self.chan.data_ptr(), self.h, X, self.w.data_ptr(), self.c_o, self.taps,
+                                       self.pos_tile, self.steps, device.ptr(self.bias), device.ptr(self.mask),
+                                       out.data_ptr(), self.sync.data_ptr(), device.stream())
         if rc:
             _native.check(rc)
         return out
+
+
+_side_streams: dict[int, tuple] = {}
+
+
+def _streams():
+    """(upload, download) side streams of the current device."""
+    dev = torch.cuda.current_device()
+    st = _side_streams.get(dev)
+    if st is None:
+        st = _side_streams[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return st
+
+
+def issue_k1(items, on_gemm=None) -> list:
+    """Enqueue K1 for independent jobs [(plan, inp, ready_event | None, out)]
+    on the current stream (each job one launch; `ready` is waited on first).
+    `on_gemm(i, "start" | "end")` is called around every tensor-core launch
+    (e.g. to record timing events). Returns one completion event per job,
+    recorded on the current stream. CUDA-graph capturable."""
+    comp = torch.cuda.current_stream()
+    need = max((plan.tc.x_bytes for plan, *_ in items if plan.path == "tc"), default=0)
+    if need:  # size the operand buffer before anything is enqueued
+        device.scratch("conv_tc_x", need)
+    done = []
+    for i, (plan, inp, ready, out) in enumerate(items):
+        if ready is not None:
+            comp.wait_event(ready)
+        if plan.path == "tc":
+            if on_gemm:
+                on_gemm(i, "start")
+            plan.tc.run(inp, out)
+            if on_gemm:
+                on_gemm(i, "end")
+        else:
+            plan.run(inp, out)
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        done.append(ev)
+    return done
 
 
 def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> ConvPlan:
@@ -432,37 +471,39 @@ def _proposed_plan(x: PackedTensor, layer: ConvLayerSpec, params: RingParams) ->
     return conv_plan(layer, layout, params)  # runs _check_budget before caching a plan
 
 
-_copy_streams: dict[int, tuple] = {}
-
-
 def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     """Serving form of conv_proposed over a sequence of independent
     (PackedTensor, ConvLayerSpec) jobs — e.g. one layer of many requests, or
-    many layers' pending inputs. Each job's upload, K1 launches and download
-    run on three CUDA streams (upload copy engine, SMs, download copy engine)
-    so job i+1's upload and job i-1's download overlap job i's convolution.
+    many layers' pending inputs. Uploads, K1 launches and downloads run on
+    three CUDA streams, so job i+1's upload and job i-1's download overlap
+    job i's convolution.
 
     Inputs may be host- (ideally pinned, see bfv.cts_from_host) or device-
     resident. Outputs are canonical ciphertexts resident on both sides: the
     host copies (pinned) are complete when this returns. Results are exactly
     those of conv_proposed on each job."""
-    dev = device.require_cuda()
+    device.require_cuda()
     comp = torch.cuda.current_stream()
-    up, down = _copy_streams.setdefault(dev.index, (torch.cuda.Stream(), torch.cuda.Stream()))
-    prepared = []
+    up, down = _streams()
+    up.wait_stream(comp)
+    items, meta = [], []
     for x, layer in jobs:  # validate everything before enqueueing anything
-        prepared.append((x, layer, _proposed_plan(x, layer, params)))
-    outs = []
-    for x, layer, plan in prepared:
+        plan = _proposed_plan(x, layer, params)
+        meta.append((x, layer, plan))
+    for x, layer, plan in meta:
+        ready = None
         if isinstance(x.cts, bfv.CtStack):
-            inp, ev = x.cts.rows.upload_on(up)
-            if ev is not None:
-                comp.wait_event(ev)
-                inp.record_stream(comp)
+            inp, ready = x.cts.rows.upload_on(up)
         else:
             inp = bfv.cts_rows(x.cts).reshape(-1, params.n)
-        out = plan.run(inp.reshape(-1, 2, params.n))
-        down.wait_stream(comp)
+        inp = inp.reshape(-1, 2, params.n)
+        out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=inp.device)
+        items.append((plan, inp, ready, out))
+    done = issue_k1(items)
+    outs = []
+    for (x, layer, plan), (_, inp, _, out), ev in zip(meta, items, done):
+        inp.record_stream(comp)
+        down.wait_event(ev)
         rows = device.DeviceRows.download_on(out, down)
         cts = bfv.CtStack(rows, params.q, Encoding.DIRECT, Domain.COEFF)
         outs.append(PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale))

@@ -35,6 +35,8 @@
 //    NST-deep stage ring (full/empty mbarriers) and two TMEM accumulator
 //    buffers (tmem_full/tmem_empty): the epilogue of tile i overlaps the
 //    MMAs of tile i+1.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fhe {
@@ -50,13 +52,16 @@ constexpr int kOcTile = 128;                  // output channels per tile (MMA M
 constexpr int kWTap = kOcTile * 32;           // packed weight bytes per (tap, 32 channels)
 
 struct TcArgs {
-  const uint8_t* X;  // [2][F][JB][Y][256] prepared digit planes
-  const uint8_t* W;  // [OB][JB][taps][16][256] packed int8 weights
+  const uint64_t* in;  // input ciphertext rows [n_in][2][n]
+  const int2* chan;    // [c_i] (source ciphertext, slot shift) of each channel
+  uint8_t* X;          // [2][F][JB][Y][256] digit planes (written by phase 1)
+  const uint8_t* W;    // [OB][JB][taps][16][256] packed int8 weights
   const uint64_t* bias;
   const uint8_t* bmask;
   uint64_t* out;
-  uint64_t q, w32p;  // modulus; Shoup companion of 2^32 (q > 2^56)
-  int n, Y, JB, F, c_o, OB, taps, h, nst, stage_bytes, win_bytes, tiles;
+  unsigned long long* sync;  // zero-initialised once: grid-barrier arrival counter
+  uint64_t q, w32p;    // modulus; Shoup companion of 2^32 (q > 2^56)
+  int n, Y, JB, F, c_i, fstride, c_o, OB, taps, h, nst, stage_bytes, win_bytes, ring_bytes, tiles, items;
   int tap_off[kMaxTaps];  // step_t + h
 };
 
@@ -178,6 +183,112 @@ __device__ __forceinline__ long long mad_wide(int32_t a, int32_t b, long long c)
   return d;
 }
 
+__device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t& p0,
+                                             uint32_t& p1, uint32_t& p2, uint32_t& p3) {
+  const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a0, a1, 0x7362);
+  const uint32_t t2 = __byte_perm(a2, a3, 0x5140), t3 = __byte_perm(a2, a3, 0x7362);
+  p0 = __byte_perm(t0, t2, 0x5410);
+  p1 = __byte_perm(t0, t2, 0x7632);
+  p2 = __byte_perm(t1, t3, 0x5410);
+  p3 = __byte_perm(t1, t3, 0x7632);
+}
+
+// Phase 1 — relayout. X[p][f][jb][y][kh][d][16]: digit d of channel
+// j = jb*32 + kh*16 + jj at extension slot (n - h + y + shift_j) of source
+// ciphertext src_j + f*fstride (the negacyclic extension [q-a | a | q-a] of
+// conv.py:251; the alignment DRot of conv.py:342 is the slot shift).
+// One warp converts one item = 32 positions x 32 channels: lane = position,
+// 32 independent coalesced 8-byte loads (one 256-byte channel row each; the
+// common all-interior case skips the sign logic), 16 in-register 4x4 byte
+// transposes into the lane's 256-byte record, staged through the warp's 8 KB
+// of shared memory (XOR-swizzled 16-byte chunks) so X is written with fully
+// coalesced 512-byte warp stores.
+__device__ __forceinline__ void relayout_item(const TcArgs& a, int unit, int lane, uint8_t* stg) {
+  const int n = a.n, nyb = (a.Y + 31) / 32;
+  const int kh = unit & 1, item = unit >> 1;  // a unit is one 16-channel K half of an item
+  const int y0 = (item % nyb) * 32, jb = (item / nyb) % a.JB;
+  const int pf = item / (nyb * a.JB), p = pf / a.F, f = pf - p * a.F;
+  const int y = y0 + lane;
+  // lane c (< 16) resolves channel jb*32 + kh*16 + c once: its row pointer and
+  // the extension slot of position y0; the loop broadcasts them
+  const int jm = jb * 32 + kh * 16 + (lane & 15);
+  const int2 cm = jm < a.c_i ? __ldg(&a.chan[jm]) : make_int2(0, 0);
+  const uint64_t* rowm = a.in + ((size_t)(cm.x + f * a.fstride) * 2 + p) * n;
+  const int e0m = n - a.h + y0 + cm.y;  // in [0, 3n)
+  const int live = max(0, min(16, a.c_i - jb * 32 - kh * 16));
+  const int yoff = min(lane, a.Y - 1 - y0);  // clamped: every load is in bounds
+  // All 16 loads are unconditional so they issue back to back; validity and
+  // the negacyclic sign are applied afterwards (and skipped when uniform).
+  uint64_t x[16];
+  uint32_t neg = 0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const uint64_t* row = reinterpret_cast<const uint64_t*>(
+        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowm), c));
+    int e = __shfl_sync(0xffffffffu, e0m, c) + yoff;
+    const bool lo = e < n, hi = e >= 2 * n;
+    e -= lo ? 0 : (hi ? 2 * n : n);
+    x[c] = __ldg(&row[e]);
+    neg |= (uint32_t)(lo || hi) << c;
+  }
+  const uint32_t keep = y < a.Y ? (1u << live) - 1u : 0u;
+  neg &= keep;
+  if (!__all_sync(0xffffffffu, keep == 0xffffu)) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) x[c] = ((keep >> c) & 1) ? x[c] : 0;
+  }
+  if (__any_sync(0xffffffffu, neg != 0)) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (((neg >> c) & 1) && x[c]) x[c] = a.q - x[c];
+  }
+  // 8 in-register 4x4 byte transposes -> the lane's 128-byte half record
+  uint32_t w[8][4];
+#pragma unroll
+  for (int g4 = 0; g4 < 4; ++g4) {
+    const int c = g4 * 4;
+    transpose4x4((uint32_t)x[c], (uint32_t)x[c + 1], (uint32_t)x[c + 2], (uint32_t)x[c + 3], w[0][g4], w[1][g4],
+                 w[2][g4], w[3][g4]);
+    transpose4x4((uint32_t)(x[c] >> 32), (uint32_t)(x[c + 1] >> 32), (uint32_t)(x[c + 2] >> 32),
+                 (uint32_t)(x[c + 3] >> 32), w[4][g4], w[5][g4], w[6][g4], w[7][g4]);
+  }
+  uint4* mine = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+  for (int d = 0; d < 8; ++d) mine[d ^ (lane & 7)] = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+  __syncwarp();
+  // copy-out: 8 lanes per position half (128 contiguous bytes of X)
+  const int rows = min(32, a.Y - y0);
+  uint4* dst = reinterpret_cast<uint4*>(a.X + (((size_t)pf * a.JB + jb) * a.Y + y0) * 256 + kh * 128);
+  const uint4* st4 = reinterpret_cast<const uint4*>(stg);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int idx = i * 32 + lane, pos = idx >> 3, ch = idx & 7;
+    if (pos < rows) dst[pos * 16 + ch] = st4[pos * 8 + (ch ^ (pos & 7))];
+  }
+  __syncwarp();
+}
+
+// Grid-wide barrier of the (cooperatively launched, co-resident) persistent
+// grid: one 64-bit arrival counter that only grows (by gridDim.x per launch,
+// so it survives CUDA-graph replays without a reset); each CTA arrives once
+// and polls with acquire loads until the counter reaches the end of its epoch.
+// Bounded spin: a protocol bug traps instead of hanging.
+__device__ __forceinline__ void grid_barrier(unsigned long long* sync) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // release this CTA's phase-1 stores
+    const unsigned long long g = gridDim.x;
+    const unsigned long long target = (atomicAdd(sync, 1ull) / g + 1) * g;
+    for (uint32_t i = 0;; ++i) {
+      unsigned long long v;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(sync) : "memory");
+      if (v >= target) break;
+      if (i > (1u << 28)) __trap();
+    }
+  }
+  __syncthreads();
+}
+
 // NPOS: positions per tile (MMA N = 8·NPOS TMEM columns per accumulator).
 template <int NPOS>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
@@ -189,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NST = a.nst, JB = a.JB, taps = a.taps, n = a.n;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * a.stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.ring_bytes);
   // [0,NST) full, [NST,2NST) empty, 2NST+{0,1} tmem_full, 2NST+{2,3} tmem_empty
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
   const uint32_t bar0 = smem_u32(bars);
@@ -219,6 +330,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  // ---------------------------------------------------------- phase 1: relayout
+  if (tid == 0) TC_TRACE(2, 0);
+  for (int unit = blockIdx.x + gridDim.x * warp; unit < 2 * a.items; unit += gridDim.x * kWarps)
+    relayout_item(a, unit, lane, smem + warp * 4096);
+  if (lane == 0) TC_TRACE(3, warp);
+  asm volatile("fence.proxy.async.shared::cta;");  // staging writes before the bulk copies reuse the ring
+  grid_barrier(a.sync);
+  if (tid == 0) TC_TRACE(7, 0);
+  asm volatile("fence.proxy.async.global;");  // X (generic-proxy stores) -> cp.async.bulk reads
+  // ---------------------------------------------------------- phase 2: GEMM
   const uint32_t wstage = (uint32_t)taps * kWTap;
   const size_t plane_stride = (size_t)a.Y * 256;
   const uint32_t win_load = (uint32_t)((NPOS + 2 * a.h) * 256);
@@ -333,79 +454,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TM_COLS));
 }
 
-// ------------------------------------------------------------- relayout
-// X[p][f][jb][y][kh][d][16]: digit d of channel j = jb*32 + kh*16 + jj at
-// extension slot (n - h + y + shift_j) of source ciphertext src_j + f*fstride.
-// A CTA (128 threads) converts kPrepY window positions x 32 channels in three
-// phases (many small CTAs per SM hide the load latency):
-//  1. coalesced 8-byte loads (lane = position, warp = 8 channels) into a
-//     shared [position][channel] tile, negacyclic sign applied on the fly;
-//  2. thread (position, K half, low/high word) byte-transposes 16 coefficients
-//     into 4 plane words x 4 (4x4 PRMT transposes) and stages 64 B in shared
-//     memory (16-byte chunks XOR-swizzled by position: conflict-free);
-//  3. the CTA streams the staged 8 KB to X with fully coalesced 16 B stores.
-constexpr int kPrepY = 32;
-constexpr int kPrepThreads = 128;
-
-__device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t& p0,
-                                             uint32_t& p1, uint32_t& p2, uint32_t& p3) {
-  const uint32_t t0 = __byte_perm(a0, a1, 0x5140), t1 = __byte_perm(a0, a1, 0x7362);
-  const uint32_t t2 = __byte_perm(a2, a3, 0x5140), t3 = __byte_perm(a2, a3, 0x7362);
-  p0 = __byte_perm(t0, t2, 0x5410);
-  p1 = __byte_perm(t0, t2, 0x7632);
-  p2 = __byte_perm(t1, t3, 0x5410);
-  p3 = __byte_perm(t1, t3, 0x7632);
-}
-
-__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const uint64_t* __restrict__ in,
-                                                            uint8_t* __restrict__ X, const int2* __restrict__ chan,
-                                                            int n, int Y, int F, int c_i, int h, int fstride,
-                                                            uint64_t q) {
-  __shared__ __align__(16) uint64_t raw[kPrepY][33];  // [position][channel] (+1 pad); reused for staging
-  const int y0 = blockIdx.x * kPrepY, jb = blockIdx.y, JB = gridDim.y;
-  const int pf = blockIdx.z, p = pf / F, f = pf - p * F;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // 1. load: warp w handles channels 8w..8w+7
-  const int y = y0 + lane;
-#pragma unroll
-  for (int cc = 0; cc < 8; ++cc) {
-    const int jl = warp * 8 + cc, j = jb * 32 + jl;
-    uint64_t x = 0;
-    if (j < c_i && y < Y) {
-      const int2 cs = __ldg(&chan[j]);
-      int e = n - h + y + cs.y;  // in [0, 3n)
-      const bool lo = e < n, hi = e >= 2 * n;
-      e -= lo ? 0 : (hi ? 2 * n : n);
-      x = __ldg(&in[((size_t)(cs.x + f * fstride) * 2 + p) * n + e]);
-      x = ((lo || hi) && x) ? q - x : x;
-    }
-    raw[lane][jl] = x;
-  }
-  __syncthreads();
-  // 2. pack: thread -> (position yl, K half kh, word half wh): planes 4wh..4wh+3
-  const int yl = threadIdx.x >> 2, kh = (threadIdx.x >> 1) & 1, wh = threadIdx.x & 1;
-  uint32_t w[4][4];
-#pragma unroll
-  for (int g4 = 0; g4 < 4; ++g4) {
-    const uint32_t* r = reinterpret_cast<const uint32_t*>(&raw[yl][kh * 16 + g4 * 4]) + wh;
-    transpose4x4(r[0], r[2], r[4], r[6], w[0][g4], w[1][g4], w[2][g4], w[3][g4]);
-  }
-  __syncthreads();
-  uint4* stage = reinterpret_cast<uint4*>(&raw[0][0]);  // [position][16 chunks of 16 B], chunk ^= yl & 7
-#pragma unroll
-  for (int dd = 0; dd < 4; ++dd)
-    stage[yl * 16 + kh * 8 + ((4 * wh + dd) ^ (yl & 7))] = make_uint4(w[dd][0], w[dd][1], w[dd][2], w[dd][3]);
-  __syncthreads();
-  // 3. coalesced copy-out of the CTA's contiguous [kPrepY][256 B] slab
-  const int rows = min(kPrepY, Y - y0);
-  uint4* dst = reinterpret_cast<uint4*>(X + (((size_t)pf * JB + jb) * Y + y0) * 256);
-#pragma unroll
-  for (int i = 0; i < kPrepY * 16 / kPrepThreads; ++i) {
-    const int idx = threadIdx.x + kPrepThreads * i, pos = idx >> 4, ch = idx & 15;
-    if (pos < rows) dst[idx] = stage[pos * 16 + (ch & 8) + ((ch & 7) ^ (pos & 7))];
-  }
-}
-
 template <int NPOS>
 static int launch(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
   if (a.n % NPOS) return fail(FHE_ERR_VALUE, "n must be a multiple of %d for the tc path", NPOS);
@@ -416,10 +464,11 @@ static int launch(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
   }
   a.win_bytes = ((NPOS + 2 * a.h) * 256 + 1023) / 1024 * 1024;
   a.stage_bytes = a.win_bytes + a.taps * kWTap;
-  a.nst = (214 * 1024) / a.stage_bytes;
+  a.nst = (204 * 1024) / a.stage_bytes;  // leaves room for two relayout CTAs per SM
   if (a.nst > kMaxStages) a.nst = kMaxStages;
   if (a.nst < 2) return fail(FHE_ERR_VALUE, "halo too large for the tc path");
-  const size_t smem = (size_t)a.nst * a.stage_bytes + 8 * (2 * kMaxStages + 4) + 16;
+  a.ring_bytes = std::max(a.nst * a.stage_bytes, kWarps * 4096);  // phase-1 staging reuses the ring
+  const size_t smem = (size_t)a.ring_bytes + 8 * (2 * kMaxStages + 4) + 16;
   a.tiles = (a.n / NPOS) * a.OB * 2 * a.F;
   static bool attr = false;
   if (!attr) {
@@ -432,8 +481,19 @@ static int launch(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
     FHE_CUDA(cudaGetDevice(&dev));
     FHE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  // persistent and cooperative: every CTA must be resident for the grid barrier
   const int grid = a.tiles < sms ? a.tiles : sms;
-  conv_tc_kernel<NPOS><<<grid, kThreads, smem, st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr_coop;
+  attr_coop.id = cudaLaunchAttributeCooperative;
+  attr_coop.val.cooperative = 1;
+  cfg.attrs = &attr_coop;
+  cfg.numAttrs = 1;
+  FHE_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<NPOS>, a));
   FHE_CHECK_LAUNCH("conv_tc_kernel");
   return FHE_OK;
 }
@@ -508,31 +568,25 @@ int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stre
   return FHE_OK;
 }
 
-int fhe_conv_tc_prep(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride, const int32_t* chan,
-                     int h, uint8_t* X, void* stream) {
-  if (n < 64 || (n & (n - 1)) || c_i < 1 || frags < 1 || h < 0 || h >= n || !in || !X || !chan)
-    return fail(FHE_ERR_VALUE, "bad tc prep arguments");
-  const int JB = (c_i + 31) / 32, Y = n + 2 * h;
-  if (JB > 65535 || 2 * frags > 65535) return fail(FHE_ERR_VALUE, "tc prep grid too large");
-  dim3 grid((unsigned)((Y + tc::kPrepY - 1) / tc::kPrepY), JB, 2 * frags);
-  tc::prep_kernel<<<grid, tc::kPrepThreads, 0, (cudaStream_t)stream>>>(in, X, reinterpret_cast<const int2*>(chan), n, Y, frags,
-                                                          c_i, h, fstride, q);
-  FHE_CHECK_LAUNCH("tc prep_kernel");
-  return FHE_OK;
-}
-
-int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h, const int8_t* Wpacked, int c_o,
-                int taps, int pos_tile, const int32_t* tap_steps_host, const uint64_t* bias_delta,
-                const uint8_t* bias_mask, uint64_t* out, void* stream) {
+int fhe_conv_tc(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride, const int32_t* chan, int h,
+                uint8_t* X, const int8_t* Wpacked, int c_o, int taps, int pos_tile, const int32_t* tap_steps_host,
+                const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out, uint64_t* sync,
+                void* stream) {
   if (q < (1ull << 56) || q >= (1ull << 62)) return fail(FHE_ERR_VALUE, "tc path needs 2^56 <= q < 2^62");
   if (n < 64 || (n & (n - 1)) || c_i < 1 || frags < 1 || c_o < 1 || taps < 1 || taps > tc::kMaxTaps || h < 0 ||
-      h >= n)
+      2 * h >= n)
     return fail(FHE_ERR_VALUE, "bad tc conv arguments");
-  if (!X || !Wpacked || !out || !tap_steps_host) return fail(FHE_ERR_VALUE, "null tc operand");
+  if (!in || !chan || !X || !Wpacked || !out || !tap_steps_host || !sync)
+    return fail(FHE_ERR_VALUE, "null tc operand");
   if (bias_delta && !bias_mask) return fail(FHE_ERR_VALUE, "bias needs a mask");
   if (127ll * 255 * ((c_i + 31) / 32 * 32) * taps >= (1ll << 31))
     return fail(FHE_ERR_VALUE, "tc path: plane sums would exceed s32");
   tc::TcArgs a;
+  a.in = in;
+  a.chan = reinterpret_cast<const int2*>(chan);
+  a.sync = reinterpret_cast<unsigned long long*>(sync);
+  a.c_i = c_i;
+  a.fstride = fstride;
   a.X = X;
   a.W = reinterpret_cast<const uint8_t*>(Wpacked);
   a.bias = bias_delta;
@@ -548,6 +602,11 @@ int fhe_conv_tc(uint64_t q, int n, const uint8_t* X, int c_i, int frags, int h, 
   a.OB = (c_o + tc::kOcTile - 1) / tc::kOcTile;
   a.taps = taps;
   a.h = h;
+  {
+    const long long items = (long long)((a.Y + 31) / 32) * a.JB * 2 * frags;
+    if (items > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc conv too large");
+    a.items = (int)items;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   if (pos_tile == 16) return tc::launch<16>(a, tap_steps_host, st);
   if (pos_tile == 32) return tc::launch<32>(a, tap_steps_host, st);

@@ -77,6 +77,10 @@ def scratch(name: str, nbytes: int) -> int:
     key = (torch.cuda.current_device(), name)
     t = _scratch.get(key)
     if t is None or t.numel() < nbytes:
+        if t is not None:
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError(f"scratch buffer {name!r} must grow during graph capture: run once eagerly first")
+            torch.cuda.synchronize()  # the old buffer may still be in use on any stream
         t = _scratch[key] = torch.empty(int(nbytes), dtype=torch.uint8, device=require_cuda())
     return t.data_ptr()
 

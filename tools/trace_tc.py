@@ -14,7 +14,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_2401_16732_b200 import _native, conv, params, stacks  # noqa: E402
 
-KINDS = ["mma_full_ok", "mma_commit", "epi_ld_issue", "epi_ld_done", "load_issue", "epi_full_ok", "epi_done", "epi_chunk_done"]
+KINDS = ["mma_full_ok", "mma_commit", "relayout_start", "relayout_warp_done", "load_issue", "epi_full_ok", "epi_done", "grid_barrier_done"]
 
 
 def main():

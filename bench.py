@@ -128,6 +128,24 @@ def build_stack(workload: str, seed: int = 4):
     return P, layers
 
 
+def world_max(x: float, world: int, dev) -> float:
+    """Max over ranks: the slowest rank's device time defines the job's time."""
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(layers_per_replica: int, steps: int, t_max_ms: float, world: int) -> float:
+    """Whole-job conv layers/s: every rank runs its own replica of the stack
+    (weak scaling, no data-path collective), timed by the slowest rank."""
+    return world * layers_per_replica * steps / (t_max_ms * 1e-3)
+
+
 def flush_l2(buf):
     buf.add_(1)  # 256 MiB write, > 126 MB L2 (outside the timed events)
 
@@ -401,13 +419,9 @@ def main():
     launches = launches_per_step * args.steps
     per_step = [a.elapsed_time(b) for a, b in step_ms]
     total_ms = sum(per_step)
-    t_max = total_ms
-    if world > 1:
-        tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = world_max(total_ms, world, "cuda")
     n_layers = len(layers)
-    value = world * n_layers * args.steps / (t_max * 1e-3)
+    value = job_value(n_layers, args.steps, t_max, world)
     ms_per_step = t_max / args.steps
 
     result = None

@@ -521,8 +521,46 @@ def e2e_arm(P, layers, steps, n_layers):
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
     avg = sum(times) / len(times)
+    # the PCIe roofline of this e2e step: pinned copy bandwidth of the same byte
+    # counts, each direction alone (the step overlaps the two directions)
+    dev_in = [torch.empty(pt.shape, dtype=torch.int64, device="cuda") for pt in pinned]
+    outs_dev = [L["out"] for L in layers]
+    host_out = [torch.empty(o.shape, dtype=torch.int64, pin_memory=True) for o in outs_dev]
+
+    def copy_ms(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 3
+
+    h2d_ms = copy_ms(lambda: [d.copy_(h, non_blocking=True) for d, h in zip(dev_in, pinned)])
+    d2h_ms = copy_ms(lambda: [h.copy_(d, non_blocking=True) for h, d in zip(host_out, outs_dev)])
+    s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        s_up.wait_stream(torch.cuda.current_stream())
+        s_down.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_up):
+            [d.copy_(h, non_blocking=True) for d, h in zip(dev_in, pinned)]
+        with torch.cuda.stream(s_down):
+            [h.copy_(d, non_blocking=True) for h, d in zip(host_out, outs_dev)]
+        torch.cuda.current_stream().wait_stream(s_up)
+        torch.cuda.current_stream().wait_stream(s_down)
+
+    duplex_ms = copy_ms(both)
+    bound_ms = max(h2d_ms, d2h_ms)
     return {"value": round(n_layers / avg, 3), "unit": "conv layers/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(avg * 1e3, 3),
+            "pcie": {"h2d_gbs": round(h2d / h2d_ms / 1e6, 1), "d2h_gbs": round(d2h / d2h_ms / 1e6, 1),
+                     "duplex_ms": round(duplex_ms, 3),
+                     "bound_ms": round(bound_ms, 3), "frac": round(bound_ms / (avg * 1e3), 3),
+                     "note": "bound = slower direction alone at measured pinned-copy bandwidth; duplex_ms = "
+                             "both directions' copies concurrently (no compute)"},
             "api": "paper_2401_16732_b200.conv.conv_proposed_stream (pinned host ciphertexts in, "
                    "pinned host ciphertexts out; upload/K1/download overlapped)"}
 

@@ -486,11 +486,12 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     comp = torch.cuda.current_stream()
     up, down = _streams()
     up.wait_stream(comp)
-    items, meta = [], []
-    for x, layer in jobs:  # validate everything before enqueueing anything
-        plan = _proposed_plan(x, layer, params)
-        meta.append((x, layer, plan))
-    for x, layer, plan in meta:
+    meta = [(x, layer, _proposed_plan(x, layer, params)) for x, layer in jobs]  # validate before enqueueing
+    need = max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0)
+    if need:
+        device.scratch("conv_tc_x", need)
+    outs = []
+    for x, layer, plan in meta:  # one pass: job i's download is enqueued before job i+1's upload
         ready = None
         if isinstance(x.cts, bfv.CtStack):
             inp, ready = x.cts.rows.upload_on(up)
@@ -498,10 +499,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
             inp = bfv.cts_rows(x.cts).reshape(-1, params.n)
         inp = inp.reshape(-1, 2, params.n)
         out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=inp.device)
-        items.append((plan, inp, ready, out))
-    done = issue_k1(items)
-    outs = []
-    for (x, layer, plan), (_, inp, _, out), ev in zip(meta, items, done):
+        (ev,) = issue_k1([(plan, inp, ready, out)])
         inp.record_stream(comp)
         down.wait_event(ev)
         rows = device.DeviceRows.download_on(out, down)

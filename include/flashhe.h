@@ -180,27 +180,41 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
                    const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
                    void* stream);
 /* K1-TC: the same contraction on tcgen05.mma.kind::i8 (u8 digit planes x s8
- * weights -> s32, 8 planes recombined exactly mod q): in [n_in][2][n] ->
- * out [c_o*frags][2][n], canonical mod q, bias fused. One cooperative,
- * persistent launch (one CTA per SM) in two phases separated by a grid
- * barrier: (1) relayout of the input into the digit-plane operand X,
- * uint8 [2][frags][ceil(c_i/32)][n + 2h][256 B] (UMMA core-matrix order);
- * (2) warp-specialised tcgen05 GEMM, tile = 128 output channels x pos_tile
- * (16 or 32) positions, 32 input channels per pipeline stage.
- * chan: DEVICE int32 pairs [c_i][2] = (source ct, slot shift) of channel j
- *   (the channel packing of conv.py:113-130); fragment f reads source + f*fstride.
- * X: DEVICE scratch of the size above.
- * Wpacked: int8 [ceil(c_o/128)][ceil(c_i/32)][taps][16][256 B] (UMMA
- *   core-matrix order: 8 output channels x 16 input channels per 128 B),
- *   |w| <= 127, 127*255*ceil32(c_i)*taps < 2^31; requires 2^56 <= q < 2^62.
- * tap_steps_host: HOST int32 [taps] DRot steps, each in [-h, h].
- * sync: DEVICE uint64, zeroed once before first use (grid-barrier arrival
- *   counter; do not share between launches that may run concurrently). */
-int fhe_conv_tc(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride,
-                const int32_t* chan, int h, uint8_t* X, const int8_t* Wpacked, int c_o,
-                int taps, int pos_tile, const int32_t* tap_steps_host,
-                const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out,
-                uint64_t* sync, void* stream);
+ * weights -> s32, 8 planes recombined exactly mod q), canonical mod q, bias
+ * fused, for a STACK of independent layers in one cooperative persistent
+ * launch (one CTA per SM). Per layer: (1) relayout of the input into the
+ * digit-plane operand X, uint8 [2][frags][ceil(c_i/32)][n + 2h][256 B] (UMMA
+ * core-matrix order), by all warps from a shared work counter; one grid
+ * barrier; (2) warp-specialised tcgen05 GEMM, tile = 128 output channels x
+ * pos_tile (16 or 32) positions, 32 input channels per pipeline stage. A warp
+ * starts the next layer's relayout as soon as its part of this layer is done.
+ * One layer = conv.conv_proposed; several = conv.issue_k1 / the serving path. */
+typedef struct fhe_conv_tc_layer {
+  const uint64_t* in;     /* DEVICE [n_in][2][n] input ciphertexts */
+  int c_i, frags, fstride;
+  const int32_t* chan;    /* DEVICE int32 pairs [c_i][2] = (source ct, slot shift) of
+                             channel j (the packing of conv.py:113-130); fragment f
+                             reads source + f*fstride */
+  int h;                  /* halo = max |tap step| */
+  const int8_t* w;        /* DEVICE int8 [ceil(c_o/128)][ceil(c_i/32)][taps][16][256 B]
+                             (8 output x 16 input channels per 128 B), |w| <= 127,
+                             127*255*ceil32(c_i)*taps < 2^31 */
+  int c_o, taps, pos_tile;
+  const int32_t* tap_steps; /* HOST int32 [taps] DRot steps, each in [-h, h] */
+  const uint64_t* bias_delta; /* DEVICE [c_o] or NULL (conv._bias_plaintext) */
+  const uint8_t* bias_mask;   /* DEVICE [frags][n] slots that receive the bias */
+  uint64_t* out;          /* DEVICE [c_o*frags][2][n] */
+} fhe_conv_tc_layer;
+/* layers: HOST array of nl (<= 24) layers sharing (q, n), 2^56 <= q < 2^62.
+ * X0, X1: DEVICE scratch, each >= the largest layer's X (X1 used when nl > 1;
+ *   layers alternate between them so a layer's relayout can overlap the
+ *   previous layer's GEMM).
+ * sync: DEVICE uint64[2 + 24], zeroed once before first use: launch, barrier
+ *   and per-layer work counters. They only grow (graph-replay safe); reuse one
+ *   sync buffer only for stacks with the same number of layers and never for
+ *   launches that may run concurrently. */
+int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl,
+                      uint8_t* X0, uint8_t* X1, uint64_t* sync, void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

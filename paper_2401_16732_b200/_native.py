@@ -70,8 +70,7 @@ SIGNATURES = {
         [_u64, _int, _vp, _int, _vp, _int, _int, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp],
     ),
     "fhe_conv_check_budget": (_int, [_vp, _int, _int]),
-    "fhe_conv_tc": (_int, [_u64, _int, _vp, _int, _int, _int, _vp, _int, _vp, _vp, _int, _int, _int, _vp, _vp, _vp,
-                           _vp, _vp, _vp]),
+    "fhe_conv_tc_stack": (_int, [_u64, _int, _vp, _int, _vp, _vp, _vp, _vp]),
     "fhe_to_montgomery": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_keyswitch_apply": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _int, _u64, _vp, _vp]),
     "fhe_act_client_square": (_int, [_u64, _int, _i64, _vp, _vp, _vp]),
@@ -123,6 +122,16 @@ def call(name: str, *args) -> None:
     rc = fn(name)(*args)
     if rc:
         check(rc)
+
+
+class ConvTcLayer(ctypes.Structure):
+    """struct fhe_conv_tc_layer (include/flashhe.h)."""
+
+    _fields_ = [
+        ("in_", _vp), ("c_i", _int), ("frags", _int), ("fstride", _int), ("chan", _vp), ("h", _int),
+        ("w", _vp), ("c_o", _int), ("taps", _int), ("pos_tile", _int), ("tap_steps", _vp),
+        ("bias_delta", _vp), ("bias_mask", _vp), ("out", _vp),
+    ]
 
 
 def u64_array(values) -> ctypes.Array:

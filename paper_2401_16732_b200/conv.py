@@ -342,7 +342,7 @@ class ConvTcPlan:
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
         self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
         self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
-        self.sync = torch.zeros(1, dtype=torch.int64, device=dev)  # grid-barrier counter of this plan's launches
+        self.sync = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=dev)  # counters of this plan's own launches
         self.bias, self.mask = bias, mask
 
     @property
@@ -350,20 +350,49 @@ class ConvTcPlan:
         """Size of the digit-plane operand X: [2][frags][JB][n + 2h][256 B]."""
         return 2 * self.frags * (-(-self.c_i // 32)) * (self.n + 2 * self.h) * 256
 
+    def layer(self, inp: torch.Tensor, out: torch.Tensor) -> "_native.ConvTcLayer":
+        """This layer's entry of a fhe_conv_tc_stack launch."""
+        return _native.ConvTcLayer(
+            inp.data_ptr(), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
+            self.c_o, self.taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
+            device.ptr(self.mask), out.data_ptr())
+
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
-        """One cooperative persistent launch (relayout phase, grid barrier,
-        tcgen05 GEMM phase); `mark()` (e.g. a CUDA event record) runs right
-        before it when given."""
-        X = device.scratch("conv_tc_x", self.x_bytes)
+        """One cooperative persistent launch of this layer alone (relayout,
+        grid barrier, tcgen05 GEMM); `mark()` (e.g. a CUDA event record) runs
+        right before it when given."""
         if mark is not None:
             mark()
-        rc = _native.fn("fhe_conv_tc")(self.q, self.n, inp.data_ptr(), self.c_i, self.frags, self.fstride,
-                                       self.chan.data_ptr(), self.h, X, self.w.data_ptr(), self.c_o, self.taps,
-                                       self.pos_tile, self.steps, device.ptr(self.bias), device.ptr(self.mask),
-                                       out.data_ptr(), self.sync.data_ptr(), device.stream())
-        if rc:
-            _native.check(rc)
+        run_tc_stack([(self, inp, out)], self.sync)
         return out
+
+
+SYNC_WORDS = 2 + 24  # fhe_conv_tc_stack: launch, barrier and per-layer work counters
+MAX_STACK = 24
+_stack_sync: dict[tuple, torch.Tensor] = {}
+
+
+def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
+    """One fhe_conv_tc_stack launch for [(ConvTcPlan, inp, out)] (≤ 24 layers
+    sharing q and n) on the current stream. `sync` defaults to a counter
+    buffer cached per layer sequence (the kernel's counters only grow, so a
+    buffer is tied to one stack length and must not serve concurrent launches)."""
+    tc0 = jobs[0][0]
+    if len(jobs) > MAX_STACK:
+        raise ValueError(f"at most {MAX_STACK} layers per tensor-core launch")
+    if sync is None:
+        key = (torch.cuda.current_device(),) + tuple(id(tc) for tc, *_ in jobs)
+        sync = _stack_sync.get(key)
+        if sync is None:
+            sync = _stack_sync[key] = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=device.require_cuda())
+    need = max(tc.x_bytes for tc, *_ in jobs)
+    X0 = device.scratch("conv_tc_x0", need)
+    X1 = device.scratch("conv_tc_x1", need) if len(jobs) > 1 else 0
+    arr = (_native.ConvTcLayer * len(jobs))(*[tc.layer(inp, out) for tc, inp, out in jobs])
+    rc = _native.fn("fhe_conv_tc_stack")(tc0.q, tc0.n, arr, len(jobs), X0, X1 or None, sync.data_ptr(),
+                                         device.stream())
+    if rc:
+        _native.check(rc)
 
 
 _side_streams: dict[int, tuple] = {}
@@ -380,29 +409,41 @@ def _streams():
 
 def issue_k1(items, on_gemm=None) -> list:
     """Enqueue K1 for independent jobs [(plan, inp, ready_event | None, out)]
-    on the current stream (each job one launch; `ready` is waited on first).
-    `on_gemm(i, "start" | "end")` is called around every tensor-core launch
-    (e.g. to record timing events). Returns one completion event per job,
+    on the current stream. Consecutive tensor-core jobs (up to 24) share ONE
+    fhe_conv_tc_stack launch — each layer's relayout overlaps the previous
+    layer's GEMM tail and no per-layer launch gap remains; other jobs run one
+    launch each. `on_gemm(i, "start" | "end")` is called around every
+    tensor-core launch (i = its first job; e.g. to record timing events).
+    Returns one completion event per job (jobs of one launch share it),
     recorded on the current stream. CUDA-graph capturable."""
     comp = torch.cuda.current_stream()
     need = max((plan.tc.x_bytes for plan, *_ in items if plan.path == "tc"), default=0)
-    if need:  # size the operand buffer before anything is enqueued
-        device.scratch("conv_tc_x", need)
-    done = []
-    for i, (plan, inp, ready, out) in enumerate(items):
-        if ready is not None:
-            comp.wait_event(ready)
-        if plan.path == "tc":
+    if need:  # size the operand buffers before anything is enqueued
+        device.scratch("conv_tc_x0", need)
+        device.scratch("conv_tc_x1", need)
+    done = [None] * len(items)
+    i = 0
+    while i < len(items):
+        j = i + 1
+        if items[i][0].path == "tc":
+            while j < len(items) and j - i < MAX_STACK and items[j][0].path == "tc":
+                j += 1
+        for _, _, ready, _ in items[i:j]:
+            if ready is not None:
+                comp.wait_event(ready)
+        if items[i][0].path == "tc":
             if on_gemm:
                 on_gemm(i, "start")
-            plan.tc.run(inp, out)
+            run_tc_stack([(plan.tc, inp, out) for plan, inp, _, out in items[i:j]])
             if on_gemm:
                 on_gemm(i, "end")
         else:
+            plan, inp, _, out = items[i]
             plan.run(inp, out)
         ev = torch.cuda.Event()
         ev.record(comp)
-        done.append(ev)
+        done[i:j] = [ev] * (j - i)
+        i = j
     return done
 
 
@@ -489,7 +530,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     meta = [(x, layer, _proposed_plan(x, layer, params)) for x, layer in jobs]  # validate before enqueueing
     need = max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0)
     if need:
-        device.scratch("conv_tc_x", need)
+        device.scratch("conv_tc_x0", need)
     outs = []
     for x, layer, plan in meta:  # one pass: job i's download is enqueued before job i+1's upload
         ready = None

@@ -11,30 +11,32 @@
 // and P_d is one tcgen05.mma.kind::i8 (s8 x u8 -> s32) accumulation.
 //
 // GEMM shape: M = 128 output channels (A = packed weights of one tap),
-// N = 8·NPOS rows (position, plane) (B = digit-plane window), K = 32 input
+// N = 8·npos rows (position, plane) (B = digit-plane window), K = 32 input
 // channels per stage. The 8 planes of a position are the 8 rows of one UMMA
 // core matrix (K-major, no swizzle: 8 rows x 16 B, LBO = 128 B between the two
 // 16-channel K halves, SBO = 256 B between positions), so a tap's DRot shift
 // moves the B operand by whole positions: one shared-memory window of
-// positions [s0-h, s0+NPOS+h) serves all f_w² taps via descriptor start
+// positions [s0-h, s0+npos+h) serves all f_w² taps via descriptor start
 // offsets — no im2col. The accumulator puts one output channel per TMEM lane
 // and the 8 planes of a position in 8 adjacent columns, so the epilogue
 // recombines V = Σ_d 256^d P_d inside each thread (no cross-lane traffic).
 //
-// Two launches per layer:
-//  * prep_kernel: ciphertexts -> digit-plane operand X in that core-matrix
-//    order (coalesced loads, a shared-memory byte transpose, 1 KB-contiguous
-//    warp stores; X stays L2-resident for the GEMM).
-//  * conv_tc_kernel: persistent (one CTA per SM), warp-specialised:
-//      warp 0     MMA issue (one thread: tcgen05.mma, tcgen05.commit)
-//      warp 1     stage loads (one thread: two cp.async.bulk per stage,
-//                 window + packed weights, mbarrier complete_tx)
-//      warps 2-9  epilogue: tcgen05.ld of the s32 plane sums, in-thread
-//                 recombination and one canonical reduction mod q per
-//                 coefficient (+ fused bias), 32-byte row stores.
-//    NST-deep stage ring (full/empty mbarriers) and two TMEM accumulator
-//    buffers (tmem_full/tmem_empty): the epilogue of tile i overlaps the
-//    MMAs of tile i+1.
+// One cooperative persistent launch (one CTA per SM) runs a whole STACK of
+// independent conv layers (one layer for conv_proposed; a network's layers or
+// many requests for the serving path). Per layer:
+//  phase 1  relayout: every warp grabs (32 positions x 16 channels) units from
+//           a per-layer work counter and writes the digit-plane operand X
+//           (two X buffers alternate between layers);
+//  barrier  one grid-wide arrival (the X of this layer is complete);
+//  phase 2  warp-specialised GEMM over the layer's tiles:
+//             warp 0     MMA issue (one thread: tcgen05.mma, tcgen05.commit)
+//             warp 1     stage loads (one thread: two cp.async.bulk per stage)
+//             warps 2-9  epilogue: tcgen05.ld, in-thread recombination, one
+//                        canonical reduction mod q (+ fused bias), row stores
+//           with an NST-deep stage ring and two TMEM accumulator buffers.
+// A warp moves on to the next layer's relayout as soon as its own role in
+// this layer is done, so relayout work fills the SMs that finish early (the
+// GEMM's wave-quantisation tail) and no per-layer launch gap remains.
 #include <algorithm>
 
 #include "common.cuh"
@@ -47,11 +49,15 @@ constexpr int kWarps = 2 + kEpiWarps;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kMaxTaps = 64;
 constexpr int kMaxStages = 6;
+constexpr int kMaxLayers = 24;
 constexpr int kEpilogue = 32 * kEpiWarps;
-constexpr int kOcTile = 128;                  // output channels per tile (MMA M)
-constexpr int kWTap = kOcTile * 32;           // packed weight bytes per (tap, 32 channels)
+constexpr int kOcTile = 128;         // output channels per tile (MMA M)
+constexpr int kWTap = kOcTile * 32;  // packed weight bytes per (tap, 32 channels)
+constexpr int kStg = 4096;           // phase-1 staging bytes per warp
+constexpr int kRingBudget = 184 * 1024;
+constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
 
-struct TcArgs {
+struct LayerDesc {
   const uint64_t* in;  // input ciphertext rows [n_in][2][n]
   const int2* chan;    // [c_i] (source ciphertext, slot shift) of each channel
   uint8_t* X;          // [2][F][JB][Y][256] digit planes (written by phase 1)
@@ -59,10 +65,15 @@ struct TcArgs {
   const uint64_t* bias;
   const uint8_t* bmask;
   uint64_t* out;
-  unsigned long long* sync;  // zero-initialised once: grid-barrier arrival counter
-  uint64_t q, w32p;    // modulus; Shoup companion of 2^32 (q > 2^56)
-  int n, Y, JB, F, c_i, fstride, c_o, OB, taps, h, nst, stage_bytes, win_bytes, ring_bytes, tiles, items;
-  int tap_off[kMaxTaps];  // step_t + h
+  int Y, JB, F, c_i, fstride, c_o, OB, taps, h, npos, nst, stage_bytes, win_bytes, tiles, units;
+  int16_t tap_off[kMaxTaps];  // step_t + h
+};
+
+struct StackArgs {
+  LayerDesc L[kMaxLayers];
+  unsigned long long* sync;  // [0] launches, [1] barrier arrivals, [2 + l] unit counters
+  uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
+  int n, nl;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -112,13 +123,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
          (1ull << 46);
 }
 
+// instruction descriptor: D s32, A s8 (weights), B u8 (digit planes), M = 128
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
 // D[128 x N] (+)= A[128 x 32] (s8 weights) · B[N x 32]^T (u8 digit planes)
-template <int N>
-__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
-  constexpr uint32_t idesc = (2u << 4)              // D: s32
-                             | (1u << 7)            // A: s8
-                             | (0u << 10)           // B: u8
-                             | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -142,10 +154,6 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])  \
       : "r"(taddr))
 
-struct Tile {
-  int ob, p, f, s0;
-};
-
 // Optional timeline instrumentation (fhe_debug_trace): CTA 0 records
 // clock64() at pipeline events, [kind][index] with 4096 slots per kind.
 __device__ unsigned long long* g_trace = nullptr;
@@ -154,18 +162,21 @@ __device__ unsigned long long* g_trace = nullptr;
     if (g_trace && blockIdx.x == 0 && (idx) < 4096) g_trace[(kind) * 4096 + (idx)] = clock64(); \
   } while (0)
 
+struct Tile {
+  int ob, p, f, s0;
+};
+
 // tile t -> (output-channel block fastest, so CTAs running together share the
 // same window in L2; then position block, fragment, poly)
-template <int NPOS>
-__device__ __forceinline__ Tile tile_of(int t, const TcArgs& a) {
+__device__ __forceinline__ Tile tile_of(int t, const LayerDesc& d, int n) {
   Tile r;
-  r.ob = t % a.OB;
-  t /= a.OB;
-  const int nsb = a.n / NPOS;
-  r.s0 = (t % nsb) * NPOS;
+  r.ob = t % d.OB;
+  t /= d.OB;
+  const int nsb = n / d.npos;
+  r.s0 = (t % nsb) * d.npos;
   t /= nsb;
-  r.f = t % a.F;
-  r.p = t / a.F;
+  r.f = t % d.F;
+  r.p = t / d.F;
   return r;
 }
 
@@ -197,28 +208,27 @@ __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t 
 // j = jb*32 + kh*16 + jj at extension slot (n - h + y + shift_j) of source
 // ciphertext src_j + f*fstride (the negacyclic extension [q-a | a | q-a] of
 // conv.py:251; the alignment DRot of conv.py:342 is the slot shift).
-// One warp converts one item = 32 positions x 32 channels: lane = position,
-// 32 independent coalesced 8-byte loads (one 256-byte channel row each; the
-// common all-interior case skips the sign logic), 16 in-register 4x4 byte
-// transposes into the lane's 256-byte record, staged through the warp's 8 KB
-// of shared memory (XOR-swizzled 16-byte chunks) so X is written with fully
-// coalesced 512-byte warp stores.
-__device__ __forceinline__ void relayout_item(const TcArgs& a, int unit, int lane, uint8_t* stg) {
-  const int n = a.n, nyb = (a.Y + 31) / 32;
+// One warp converts one unit = 32 positions x 16 channels: lane = position,
+// 16 unconditional (clamped, in-bounds) coalesced 8-byte loads issued back to
+// back, validity and the negacyclic sign applied afterwards from per-lane
+// masks, 8 in-register 4x4 byte transposes into the lane's 128-byte half
+// record, staged through the warp's shared memory (XOR-swizzled 16-byte
+// chunks) so X is written with full 128-byte lines.
+__device__ __forceinline__ void relayout_unit(const LayerDesc& d, int n, uint64_t q, int unit, int lane,
+                                              uint8_t* stg) {
+  const int nyb = (d.Y + 31) / 32;
   const int kh = unit & 1, item = unit >> 1;  // a unit is one 16-channel K half of an item
-  const int y0 = (item % nyb) * 32, jb = (item / nyb) % a.JB;
-  const int pf = item / (nyb * a.JB), p = pf / a.F, f = pf - p * a.F;
+  const int y0 = (item % nyb) * 32, jb = (item / nyb) % d.JB;
+  const int pf = item / (nyb * d.JB), p = pf / d.F, f = pf - p * d.F;
   const int y = y0 + lane;
   // lane c (< 16) resolves channel jb*32 + kh*16 + c once: its row pointer and
   // the extension slot of position y0; the loop broadcasts them
   const int jm = jb * 32 + kh * 16 + (lane & 15);
-  const int2 cm = jm < a.c_i ? __ldg(&a.chan[jm]) : make_int2(0, 0);
-  const uint64_t* rowm = a.in + ((size_t)(cm.x + f * a.fstride) * 2 + p) * n;
-  const int e0m = n - a.h + y0 + cm.y;  // in [0, 3n)
-  const int live = max(0, min(16, a.c_i - jb * 32 - kh * 16));
-  const int yoff = min(lane, a.Y - 1 - y0);  // clamped: every load is in bounds
-  // All 16 loads are unconditional so they issue back to back; validity and
-  // the negacyclic sign are applied afterwards (and skipped when uniform).
+  const int2 cm = jm < d.c_i ? __ldg(&d.chan[jm]) : make_int2(0, 0);
+  const uint64_t* rowm = d.in + ((size_t)(cm.x + f * d.fstride) * 2 + p) * n;
+  const int e0m = n - d.h + y0 + cm.y;  // in [0, 3n)
+  const int live = max(0, min(16, d.c_i - jb * 32 - kh * 16));
+  const int yoff = min(lane, d.Y - 1 - y0);  // clamped: every load is in bounds
   uint64_t x[16];
   uint32_t neg = 0;
 #pragma unroll
@@ -231,7 +241,7 @@ __device__ __forceinline__ void relayout_item(const TcArgs& a, int unit, int lan
     x[c] = __ldg(&row[e]);
     neg |= (uint32_t)(lo || hi) << c;
   }
-  const uint32_t keep = y < a.Y ? (1u << live) - 1u : 0u;
+  const uint32_t keep = y < d.Y ? (1u << live) - 1u : 0u;
   neg &= keep;
   if (!__all_sync(0xffffffffu, keep == 0xffffu)) {
 #pragma unroll
@@ -240,9 +250,8 @@ __device__ __forceinline__ void relayout_item(const TcArgs& a, int unit, int lan
   if (__any_sync(0xffffffffu, neg != 0)) {
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (((neg >> c) & 1) && x[c]) x[c] = a.q - x[c];
+      if (((neg >> c) & 1) && x[c]) x[c] = q - x[c];
   }
-  // 8 in-register 4x4 byte transposes -> the lane's 128-byte half record
   uint32_t w[8][4];
 #pragma unroll
   for (int g4 = 0; g4 < 4; ++g4) {
@@ -254,11 +263,11 @@ __device__ __forceinline__ void relayout_item(const TcArgs& a, int unit, int lan
   }
   uint4* mine = reinterpret_cast<uint4*>(stg + lane * 128);
 #pragma unroll
-  for (int d = 0; d < 8; ++d) mine[d ^ (lane & 7)] = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+  for (int dd = 0; dd < 8; ++dd) mine[dd ^ (lane & 7)] = make_uint4(w[dd][0], w[dd][1], w[dd][2], w[dd][3]);
   __syncwarp();
   // copy-out: 8 lanes per position half (128 contiguous bytes of X)
-  const int rows = min(32, a.Y - y0);
-  uint4* dst = reinterpret_cast<uint4*>(a.X + (((size_t)pf * a.JB + jb) * a.Y + y0) * 256 + kh * 128);
+  const int rows = min(32, d.Y - y0);
+  uint4* dst = reinterpret_cast<uint4*>(d.X + (((size_t)pf * d.JB + jb) * d.Y + y0) * 256 + kh * 128);
   const uint4* st4 = reinterpret_cast<const uint4*>(stg);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -268,20 +277,21 @@ __device__ __forceinline__ void relayout_item(const TcArgs& a, int unit, int lan
   __syncwarp();
 }
 
-// Grid-wide barrier of the (cooperatively launched, co-resident) persistent
-// grid: one 64-bit arrival counter that only grows (by gridDim.x per launch,
-// so it survives CUDA-graph replays without a reset); each CTA arrives once
-// and polls with acquire loads until the counter reaches the end of its epoch.
-// Bounded spin: a protocol bug traps instead of hanging.
-__device__ __forceinline__ void grid_barrier(unsigned long long* sync) {
+// Monotonic launch-scoped counters (never reset, so CUDA-graph replays are
+// safe). The launch epoch e = arrivals / gridDim.x; grid barrier l of launch e
+// completes when the arrival counter reaches ((e-1)·nl + l + 1)·gridDim.x;
+// layer l's unit counter starts launch e at (e-1)·(units + warps in grid)
+// because every warp overshoots it exactly once. The grid is cooperative, so
+// every CTA is resident and the waits cannot deadlock; spins are bounded (a
+// protocol bug traps instead of hanging).
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned long long target) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();  // release this CTA's phase-1 stores
-    const unsigned long long g = gridDim.x;
-    const unsigned long long target = (atomicAdd(sync, 1ull) / g + 1) * g;
+    atomicAdd(ctr, 1ull);
     for (uint32_t i = 0;; ++i) {
       unsigned long long v;
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(sync) : "memory");
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
       if (v >= target) break;
       if (i > (1u << 28)) __trap();
     }
@@ -289,33 +299,34 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* sync) {
   __syncthreads();
 }
 
-// NPOS: positions per tile (MMA N = 8·NPOS TMEM columns per accumulator).
-template <int NPOS>
-__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid_constant__ StackArgs A) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int MN = 8 * NPOS;         // MMA N = TMEM columns per accumulator
-  constexpr int TM_COLS = 2 * MN;      // double buffered
-  static_assert(TM_COLS == 256 || TM_COLS == 512, "tmem");
-
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NST = a.nst, JB = a.JB, taps = a.taps, n = a.n;
-
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.ring_bytes);
-  // [0,NST) full, [NST,2NST) empty, 2NST+{0,1} tmem_full, 2NST+{2,3} tmem_empty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
+  const int n = A.n, nl = A.nl, G = gridDim.x;
+  const uint64_t q = A.q;
+  int ring_bytes = 0;
+  for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].nst * A.L[l].stage_bytes);
+  uint8_t* stg = smem + ring_bytes + warp * kStg;  // this warp's phase-1 staging (outside the ring)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes + kWarps * kStg);
+  // [0,6) full, [6,12) empty, 12+{0,1} tmem_full, 12+{2,3} tmem_empty
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
-  auto empty_bar = [&](int s) { return bar0 + 8 * (NST + s); };
-  auto tfull_bar = [&](int b) { return bar0 + 8 * (2 * NST + b); };
-  auto tempty_bar = [&](int b) { return bar0 + 8 * (2 * NST + 2 + b); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (kMaxStages + s); };
+  auto tfull_bar = [&](int b) { return bar0 + 8 * (2 * kMaxStages + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8 * (2 * kMaxStages + 2 + b); };
 
+  if (tid == 0) {
+    const unsigned long long arr = atomicAdd(A.sync, 1ull);
+    slot[1] = (unsigned)(arr / (unsigned long long)G);  // epoch - 1
+  }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(TM_COLS));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                 "n"(2 * kAccCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(s)));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty_bar(s)));
     }
@@ -329,173 +340,158 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const TcArgs a) {
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
-  // ---------------------------------------------------------- phase 1: relayout
-  if (tid == 0) TC_TRACE(2, 0);
-  for (int unit = blockIdx.x + gridDim.x * warp; unit < 2 * a.items; unit += gridDim.x * kWarps)
-    relayout_item(a, unit, lane, smem + warp * 4096);
-  if (lane == 0) TC_TRACE(3, warp);
-  asm volatile("fence.proxy.async.shared::cta;");  // staging writes before the bulk copies reuse the ring
-  grid_barrier(a.sync);
-  if (tid == 0) TC_TRACE(7, 0);
-  asm volatile("fence.proxy.async.global;");  // X (generic-proxy stores) -> cp.async.bulk reads
-  // ---------------------------------------------------------- phase 2: GEMM
-  const uint32_t wstage = (uint32_t)taps * kWTap;
-  const size_t plane_stride = (size_t)a.Y * 256;
-  const uint32_t win_load = (uint32_t)((NPOS + 2 * a.h) * 256);
+  const uint32_t tmem = slot[0];
+  const unsigned long long e1 = slot[1];  // epoch - 1
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ MMA issue
-    if (lane == 0) {
-      int it = 0, tl = 0;
-      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++tl) {
-        const int buf = tl & 1;
-        mbar_wait(tempty_bar(buf), ((tl >> 1) & 1) ^ 1);  // epilogue released this buffer
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t acc = tmem + buf * MN;
-        for (int jb = 0; jb < JB; ++jb, ++it) {
-          const int s = it % NST;
-          mbar_wait(full_bar(s), (it / NST) & 1);
-          TC_TRACE(0, it);
+  // per-role pipeline state that persists across layers
+  int s_ld = 0, s_mma = 0;          // stage cursors (loader / MMA)
+  uint32_t par_ld = 0, par_mma = 0;  // per-stage phase parities: fills done / consumes done
+  uint32_t used = 0;                 // stages filled at least once (loader)
+  int prev_stage_bytes = -1, prev_stage_bytes_mma = -1;
+  int tl = 0;                        // tile counter (TMEM buffer parity) for MMA and epilogue
+  const int quad = warp & 3, sub = (warp - 2) >> 2;
+  const int k8 = opaque(1 << 8), k16 = opaque(1 << 16), k24 = opaque(1 << 24);
+
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc& d = A.L[l];
+    // ------------------------------------------------------ phase 1: relayout
+    if (tid == 0) TC_TRACE(2, l);
+    {
+      const unsigned long long base = e1 * (unsigned long long)(d.units + G * kWarps);
+      for (;;) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(A.sync + 2 + l, 1ull) - base;
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= (unsigned long long)d.units) break;
+        relayout_unit(d, n, q, (int)u, lane, stg);
+      }
+    }
+    if (lane == 0) TC_TRACE(3, l * 16 + warp);
+    grid_barrier(A.sync + 1, (e1 * nl + l + 1) * (unsigned long long)G);
+    if (tid == 0) TC_TRACE(7, l);
+    // ------------------------------------------------------ phase 2: GEMM
+    const int npos = d.npos, JB = d.JB, taps = d.taps;
+    const uint32_t wstage = (uint32_t)taps * kWTap;
+    if (warp == 0) {
+      // MMA issue
+      if (lane == 0) {
+        if (d.stage_bytes != prev_stage_bytes_mma) s_mma = 0;  // the loader drained and re-partitioned the ring
+        prev_stage_bytes_mma = d.stage_bytes;
+        const uint32_t idesc = idesc_i8(8 * npos);
+        for (int t = blockIdx.x; t < d.tiles; t += G, ++tl) {
+          const int buf = tl & 1;
+          mbar_wait(tempty_bar(buf), ((tl >> 1) & 1) ^ 1);  // epilogue released this buffer
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t sx = smem_u32(smem + s * a.stage_bytes);
-          const uint32_t sw = sx + a.win_bytes;
-          for (int tp = 0; tp < taps; ++tp)
-            mma_i8<MN>(acc, umma_desc(sw + tp * kWTap), umma_desc(sx + (uint32_t)a.tap_off[tp] * 256),
-                       (jb | tp) != 0);
-          mma_commit(empty_bar(s));  // stage free once these MMAs retire
-          TC_TRACE(1, it);
-        }
-        mma_commit(tfull_bar(buf));  // accumulator complete
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ stage loads
-    if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-        const Tile T = tile_of<NPOS>(t, a);
-        const uint8_t* xbase = a.X + ((size_t)(T.p * a.F + T.f) * JB) * plane_stride + (size_t)T.s0 * 256;
-        const uint8_t* wbase = a.W + (size_t)T.ob * JB * wstage;
-        for (int jb = 0; jb < JB; ++jb, ++it) {
-          const int s = it % NST;
-          mbar_wait_sleep(empty_bar(s), ((it / NST) & 1) ^ 1, 32);
-          const uint32_t sx = smem_u32(smem + s * a.stage_bytes);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
-                       "r"(win_load + wstage)
-                       : "memory");
-          TC_TRACE(4, it);
-          bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
-          bulk_load(sx + a.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
+          const uint32_t acc = tmem + buf * kAccCols;
+          for (int jb = 0; jb < JB; ++jb) {
+            const int s = s_mma;
+            mbar_wait(full_bar(s), (par_mma >> s) & 1);
+            par_mma ^= 1u << s;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
+            const uint32_t sw = sx + d.win_bytes;
+            for (int tp = 0; tp < taps; ++tp)
+              mma_i8(acc, umma_desc(sw + tp * kWTap), umma_desc(sx + (uint32_t)d.tap_off[tp] * 256), idesc,
+                     (jb | tp) != 0);
+            mma_commit(empty_bar(s));  // stage free once these MMAs retire
+            s_mma = s + 1 == d.nst ? 0 : s + 1;
+          }
+          mma_commit(tfull_bar(buf));  // accumulator complete
         }
       }
-    }
-  } else {
-    // ---------------------------------------------------------------- epilogue
-    // lane = output channel within the quadrant; a 32-column TMEM chunk holds
-    // 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and hi = q + Σ_{d>=4}
-    // 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31, q > 2^56); V = lo + 2^32 hi.
-    const int quad = warp & 3;        // TMEM lane quadrant (hardware: warp id % 4)
-    const int sub = (warp - 2) >> 2;  // which warp of the quadrant
-    const uint64_t q = a.q;
-    const int k8 = opaque(1 << 8), k16 = opaque(1 << 16), k24 = opaque(1 << 24);
-    int tl = 0;
-    for (int t = blockIdx.x; t < a.tiles; t += gridDim.x, ++tl) {
-      const Tile T = tile_of<NPOS>(t, a);
-      const int buf = tl & 1;
-      const int o = T.ob * kOcTile + quad * 32 + lane;
-      const bool active = T.ob * kOcTile + quad * 32 < a.c_o;  // warp-uniform
-      mbar_wait_sleep(tfull_bar(buf), (tl >> 1) & 1, 64);
-      if (lane == 0 && warp == 2) TC_TRACE(5, tl);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      if (active) {
-        const uint64_t bd = (T.p == 0 && a.bias && o < a.c_o) ? a.bias[o] : 0;
-        const uint32_t acc = tmem + buf * MN + ((uint32_t)(quad * 32) << 16);
-        uint64_t* orow = a.out + ((size_t)(o * a.F + T.f) * 2 + T.p) * n + T.s0;
+      __syncwarp();
+    } else if (warp == 1) {
+      // stage loads
+      if (lane == 0) {
+        if (d.stage_bytes != prev_stage_bytes) {
+          // new ring partition: every stage of the old one must be consumed first
+          for (int s = 0; s < kMaxStages; ++s)
+            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par_ld >> s) & 1) ^ 1, 32);
+          s_ld = 0;
+          prev_stage_bytes = d.stage_bytes;
+        }
+        asm volatile("fence.proxy.async.global;");  // generic-proxy X stores -> cp.async.bulk reads
+        const size_t plane_stride = (size_t)d.Y * 256;
+        const uint32_t win_load = (uint32_t)((npos + 2 * d.h) * 256);
+        for (int t = blockIdx.x; t < d.tiles; t += G) {
+          const Tile T = tile_of(t, d, n);
+          const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * JB) * plane_stride + (size_t)T.s0 * 256;
+          const uint8_t* wbase = d.W + (size_t)T.ob * JB * wstage;
+          for (int jb = 0; jb < JB; ++jb) {
+            const int s = s_ld;
+            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par_ld >> s) & 1) ^ 1, 32);
+            used |= 1u << s;
+            par_ld ^= 1u << s;
+            const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
+                         "r"(win_load + wstage)
+                         : "memory");
+            bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+            bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
+            s_ld = s + 1 == d.nst ? 0 : s + 1;
+          }
+        }
+      }
+      __syncwarp();
+    } else {
+      // epilogue: lane = output channel within the quadrant; a 32-column TMEM
+      // chunk holds 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and
+      // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,
+      // q > 2^56); V = lo + 2^32 hi.
+      for (int t = blockIdx.x; t < d.tiles; t += G, ++tl) {
+        const Tile T = tile_of(t, d, n);
+        const int buf = tl & 1;
+        const int o = T.ob * kOcTile + quad * 32 + lane;
+        const bool active = T.ob * kOcTile + quad * 32 < d.c_o;  // warp-uniform
+        mbar_wait_sleep(tfull_bar(buf), (tl >> 1) & 1, 64);
+        if (lane == 0 && warp == 2) TC_TRACE(5, tl);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (active) {
+          const uint64_t bd = (T.p == 0 && d.bias && o < d.c_o) ? d.bias[o] : 0;
+          const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
+          uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + T.s0;
 #pragma unroll 1
-        for (int k = sub; k < NPOS / 4; k += kEpiWarps / 4) {
-          uint32_t v[32];
-          TMEM_LD32(acc + k * 32, v);
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-          uint64_t r[4];
+          for (int k = sub; k < npos / 4; k += kEpiWarps / 4) {
+            uint32_t v[32];
+            TMEM_LD32(acc + k * 32, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            uint64_t r[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int32_t* P = reinterpret_cast<const int32_t*>(v + 8 * j);
-            const long long lo =
-                mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, (long long)q + P[0])));
-            const long long hi =
-                mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, (long long)q + P[4])));
-            // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
-            const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(a.w32p, (uint64_t)hi) * q;
-            uint64_t val = (uint64_t)lo + uh;  // < 4q
-            val = val >= 2 * q ? val - 2 * q : val;
-            r[j] = val >= q ? val - q : val;
-          }
-          if (bd) {
-            const uint32_t mk = *reinterpret_cast<const uint32_t*>(a.bmask + (size_t)T.f * n + T.s0 + 4 * k);
+            for (int j = 0; j < 4; ++j) {
+              const int32_t* P = reinterpret_cast<const int32_t*>(v + 8 * j);
+              const long long lo =
+                  mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, (long long)q + P[0])));
+              const long long hi =
+                  mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, (long long)q + P[4])));
+              // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
+              const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(A.w32p, (uint64_t)hi) * q;
+              uint64_t val = (uint64_t)lo + uh;  // < 4q
+              val = val >= 2 * q ? val - 2 * q : val;
+              r[j] = val >= q ? val - q : val;
+            }
+            if (bd) {
+              const uint32_t mk = *reinterpret_cast<const uint32_t*>(d.bmask + (size_t)T.f * n + T.s0 + 4 * k);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
-          }
-          if (o < a.c_o) {
-            ulonglong2* dst = reinterpret_cast<ulonglong2*>(orow + 4 * k);
-            dst[0] = make_ulonglong2(r[0], r[1]);
-            dst[1] = make_ulonglong2(r[2], r[3]);
+              for (int j = 0; j < 4; ++j)
+                if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
+            }
+            if (o < d.c_o) {
+              ulonglong2* dst = reinterpret_cast<ulonglong2*>(orow + 4 * k);
+              dst[0] = make_ulonglong2(r[0], r[1]);
+              dst[1] = make_ulonglong2(r[2], r[3]);
+            }
           }
         }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(tempty_bar(buf));
+        if (lane == 0 && warp == 2) TC_TRACE(6, tl);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(tempty_bar(buf));
-      if (lane == 0 && warp == 2) TC_TRACE(6, tl);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TM_COLS));
-}
-
-template <int NPOS>
-static int launch(TcArgs& a, const int32_t* tap_steps_host, cudaStream_t st) {
-  if (a.n % NPOS) return fail(FHE_ERR_VALUE, "n must be a multiple of %d for the tc path", NPOS);
-  for (int t = 0; t < a.taps; ++t) {
-    const int off = tap_steps_host[t] + a.h;
-    if (off < 0 || off > 2 * a.h) return fail(FHE_ERR_VALUE, "tap step outside the halo");
-    a.tap_off[t] = off;
-  }
-  a.win_bytes = ((NPOS + 2 * a.h) * 256 + 1023) / 1024 * 1024;
-  a.stage_bytes = a.win_bytes + a.taps * kWTap;
-  a.nst = (204 * 1024) / a.stage_bytes;  // leaves room for two relayout CTAs per SM
-  if (a.nst > kMaxStages) a.nst = kMaxStages;
-  if (a.nst < 2) return fail(FHE_ERR_VALUE, "halo too large for the tc path");
-  a.ring_bytes = std::max(a.nst * a.stage_bytes, kWarps * 4096);  // phase-1 staging reuses the ring
-  const size_t smem = (size_t)a.ring_bytes + 8 * (2 * kMaxStages + 4) + 16;
-  a.tiles = (a.n / NPOS) * a.OB * 2 * a.F;
-  static bool attr = false;
-  if (!attr) {
-    FHE_CUDA(cudaFuncSetAttribute(conv_tc_kernel<NPOS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    FHE_CUDA(cudaGetDevice(&dev));
-    FHE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  // persistent and cooperative: every CTA must be resident for the grid barrier
-  const int grid = a.tiles < sms ? a.tiles : sms;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr_coop;
-  attr_coop.id = cudaLaunchAttributeCooperative;
-  attr_coop.val.cooperative = 1;
-  cfg.attrs = &attr_coop;
-  cfg.numAttrs = 1;
-  FHE_CUDA(cudaLaunchKernelEx(&cfg, conv_tc_kernel<NPOS>, a));
-  FHE_CHECK_LAUNCH("conv_tc_kernel");
-  return FHE_OK;
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kAccCols));
 }
 
 // Dense int8 tcgen05 roofline probe: back-to-back M=128 N K=32 MMAs on
@@ -521,9 +517,10 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, uint32_t* si
   const uint32_t tmem = *slot;
   if (threadIdx.x == 0) {
     const uint64_t ad = umma_desc(smem_u32(smem)), bd = umma_desc(smem_u32(smem + 4096));
+    constexpr uint32_t idesc = idesc_i8(N);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) mma_i8<N>(tmem + (k & 1) * 256, ad, bd, 1);
+      for (int k = 0; k < 8; ++k) mma_i8(tmem + (k & 1) * 256, ad, bd, idesc, 1);
     }
     mma_commit(smem_u32(bar));
   }
@@ -568,49 +565,89 @@ int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stre
   return FHE_OK;
 }
 
-int fhe_conv_tc(uint64_t q, int n, const uint64_t* in, int c_i, int frags, int fstride, const int32_t* chan, int h,
-                uint8_t* X, const int8_t* Wpacked, int c_o, int taps, int pos_tile, const int32_t* tap_steps_host,
-                const uint64_t* bias_delta, const uint8_t* bias_mask, uint64_t* out, uint64_t* sync,
-                void* stream) {
+int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl, uint8_t* X0, uint8_t* X1,
+                      uint64_t* sync, void* stream) {
   if (q < (1ull << 56) || q >= (1ull << 62)) return fail(FHE_ERR_VALUE, "tc path needs 2^56 <= q < 2^62");
-  if (n < 64 || (n & (n - 1)) || c_i < 1 || frags < 1 || c_o < 1 || taps < 1 || taps > tc::kMaxTaps || h < 0 ||
-      2 * h >= n)
-    return fail(FHE_ERR_VALUE, "bad tc conv arguments");
-  if (!in || !chan || !X || !Wpacked || !out || !tap_steps_host || !sync)
-    return fail(FHE_ERR_VALUE, "null tc operand");
-  if (bias_delta && !bias_mask) return fail(FHE_ERR_VALUE, "bias needs a mask");
-  if (127ll * 255 * ((c_i + 31) / 32 * 32) * taps >= (1ll << 31))
-    return fail(FHE_ERR_VALUE, "tc path: plane sums would exceed s32");
-  tc::TcArgs a;
-  a.in = in;
-  a.chan = reinterpret_cast<const int2*>(chan);
-  a.sync = reinterpret_cast<unsigned long long*>(sync);
-  a.c_i = c_i;
-  a.fstride = fstride;
-  a.X = X;
-  a.W = reinterpret_cast<const uint8_t*>(Wpacked);
-  a.bias = bias_delta;
-  a.bmask = bias_mask;
-  a.out = out;
-  a.q = q;
-  a.w32p = h_shoup(1ull << 32, q);
-  a.n = n;
-  a.Y = n + 2 * h;
-  a.JB = (c_i + 31) / 32;
-  a.F = frags;
-  a.c_o = c_o;
-  a.OB = (c_o + tc::kOcTile - 1) / tc::kOcTile;
-  a.taps = taps;
-  a.h = h;
-  {
-    const long long items = (long long)((a.Y + 31) / 32) * a.JB * 2 * frags;
-    if (items > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc conv too large");
-    a.items = (int)items;
+  if (n < 64 || (n & (n - 1))) return fail(FHE_ERR_VALUE, "tc path needs a power-of-two n >= 64");
+  if (nl < 1 || nl > tc::kMaxLayers) return fail(FHE_ERR_VALUE, "tc stack: 1..%d layers", tc::kMaxLayers);
+  if (!layers || !X0 || !sync || (nl > 1 && !X1)) return fail(FHE_ERR_VALUE, "null tc stack operand");
+  static tc::StackArgs A;  // large: kept off the stack; launches are issued from one host thread at a time
+  A.q = q;
+  A.w32p = h_shoup(1ull << 32, q);
+  A.n = n;
+  A.nl = nl;
+  A.sync = reinterpret_cast<unsigned long long*>(sync);
+  int max_tiles = 0, ring = 0;
+  for (int l = 0; l < nl; ++l) {
+    const fhe_conv_tc_layer& s = layers[l];
+    tc::LayerDesc& d = A.L[l];
+    if (s.c_i < 1 || s.frags < 1 || s.c_o < 1 || s.taps < 1 || s.taps > tc::kMaxTaps || s.h < 0 || 2 * s.h >= n)
+      return fail(FHE_ERR_VALUE, "tc layer %d: bad shape", l);
+    if (!s.in || !s.chan || !s.w || !s.out || !s.tap_steps) return fail(FHE_ERR_VALUE, "tc layer %d: null operand", l);
+    if (s.bias_delta && !s.bias_mask) return fail(FHE_ERR_VALUE, "tc layer %d: bias needs a mask", l);
+    if (s.pos_tile != 16 && s.pos_tile != 32) return fail(FHE_ERR_VALUE, "tc layer %d: pos_tile must be 16 or 32", l);
+    if (127ll * 255 * ((s.c_i + 31) / 32 * 32) * s.taps >= (1ll << 31))
+      return fail(FHE_ERR_VALUE, "tc layer %d: plane sums would exceed s32", l);
+    d.in = s.in;
+    d.chan = reinterpret_cast<const int2*>(s.chan);
+    d.X = (l & 1) ? X1 : X0;
+    d.W = reinterpret_cast<const uint8_t*>(s.w);
+    d.bias = s.bias_delta;
+    d.bmask = s.bias_mask;
+    d.out = s.out;
+    d.Y = n + 2 * s.h;
+    d.JB = (s.c_i + 31) / 32;
+    d.F = s.frags;
+    d.c_i = s.c_i;
+    d.fstride = s.fstride;
+    d.c_o = s.c_o;
+    d.OB = (s.c_o + tc::kOcTile - 1) / tc::kOcTile;
+    d.taps = s.taps;
+    d.h = s.h;
+    d.npos = s.pos_tile;
+    for (int t = 0; t < s.taps; ++t) {
+      const int off = s.tap_steps[t] + s.h;
+      if (off < 0 || off > 2 * s.h) return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
+      d.tap_off[t] = (int16_t)off;
+    }
+    d.win_bytes = ((d.npos + 2 * d.h) * 256 + 1023) / 1024 * 1024;
+    d.stage_bytes = d.win_bytes + d.taps * tc::kWTap;
+    d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
+    if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
+    d.tiles = (n / d.npos) * d.OB * 2 * d.F;
+    const long long units = 2ll * ((d.Y + 31) / 32) * d.JB * 2 * d.F;
+    if (units > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc layer %d too large", l);
+    d.units = (int)units;
+    max_tiles = std::max(max_tiles, d.tiles);
+    ring = std::max(ring, d.nst * d.stage_bytes);
   }
-  cudaStream_t st = (cudaStream_t)stream;
-  if (pos_tile == 16) return tc::launch<16>(a, tap_steps_host, st);
-  if (pos_tile == 32) return tc::launch<32>(a, tap_steps_host, st);
-  return fail(FHE_ERR_VALUE, "pos_tile must be 16 or 32");
+  const size_t smem = (size_t)ring + tc::kWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
+  static bool attr = false;
+  if (!attr) {
+    FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    FHE_CUDA(cudaGetDevice(&dev));
+    FHE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  // persistent and cooperative: every CTA must be resident for the grid barriers
+  (void)max_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(tc::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr_coop;
+  attr_coop.id = cudaLaunchAttributeCooperative;
+  attr_coop.val.cooperative = 1;
+  cfg.attrs = &attr_coop;
+  cfg.numAttrs = 1;
+  FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel, A));
+  FHE_CHECK_LAUNCH("conv_tc_stack_kernel");
+  return FHE_OK;
 }
 
 }  // extern "C"

@@ -184,10 +184,10 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
  * fused, for a STACK of independent layers in one cooperative persistent
  * launch (one CTA per SM). Per layer: (1) relayout of the input into the
  * digit-plane operand X, uint8 [2][frags][ceil(c_i/32)][n + 2h][256 B] (UMMA
- * core-matrix order), by all warps from a shared work counter; one grid
- * barrier; (2) warp-specialised tcgen05 GEMM, tile = 128 output channels x
- * pos_tile (16 or 32) positions, 32 input channels per pipeline stage. A warp
- * starts the next layer's relayout as soon as its part of this layer is done.
+ * core-matrix order), by dedicated relayout warps of all CTAs from a shared
+ * work counter, up to three layers ahead of the GEMM; (2) warp-specialised tcgen05 GEMM,
+ * tile = 128 output channels x pos_tile (16 or 32) positions, 32 input
+ * channels per pipeline stage, starting once its layer's X is complete.
  * One layer = conv.conv_proposed; several = conv.issue_k1 / the serving path. */
 typedef struct fhe_conv_tc_layer {
   const uint64_t* in;     /* DEVICE [n_in][2][n] input ciphertexts */
@@ -206,15 +206,15 @@ typedef struct fhe_conv_tc_layer {
   uint64_t* out;          /* DEVICE [c_o*frags][2][n] */
 } fhe_conv_tc_layer;
 /* layers: HOST array of nl (<= 24) layers sharing (q, n), 2^56 <= q < 2^62.
- * X0, X1: DEVICE scratch, each >= the largest layer's X (X1 used when nl > 1;
- *   layers alternate between them so a layer's relayout can overlap the
- *   previous layer's GEMM).
- * sync: DEVICE uint64[2 + 24], zeroed once before first use: launch, barrier
- *   and per-layer work counters. They only grow (graph-replay safe); reuse one
+ * X: DEVICE scratch of 3 operand buffers x_stride bytes apart (x_stride >= the
+ *   largest layer's X; one buffer when nl == 1). Layer l uses buffer l % 3:
+ *   layer l+1 is relaid out while layer l's GEMM runs.
+ * sync: DEVICE uint64[3 + 24], zeroed once before first use: launch,
+ *   relayout-done, GEMM-done and per-layer work counters. They only grow (graph-replay safe); reuse one
  *   sync buffer only for stacks with the same number of layers and never for
  *   launches that may run concurrently. */
 int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl,
-                      uint8_t* X0, uint8_t* X1, uint64_t* sync, void* stream);
+                      uint8_t* X, size_t x_stride, uint64_t* sync, void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

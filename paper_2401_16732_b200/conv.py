@@ -302,10 +302,15 @@ class ConvTcPlan:
     def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int) -> int:
         """32 positions per tile, or 16 when that leaves fewer than two tiles
         per SM (small layers are epilogue-latency bound) and still fits."""
-        tiles = (n // 32) * -(-c_o // ConvTcPlan.OC_TILE) * 2 * frags
-        if tiles < 2 * ConvTcPlan.SMS or not ConvTcPlan._fits(32, h, taps):
+        import os
+
+        if not ConvTcPlan._fits(32, h, taps):
             return 16
-        return 32
+        mode = os.environ.get("FLASHHE_TC_POS", "32")
+        if mode == "auto":
+            tiles = (n // 32) * -(-c_o // ConvTcPlan.OC_TILE) * 2 * frags
+            return 16 if tiles < 2 * ConvTcPlan.SMS else 32
+        return int(mode)
 
     @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
@@ -367,7 +372,7 @@ class ConvTcPlan:
         return out
 
 
-SYNC_WORDS = 2 + 24  # fhe_conv_tc_stack: launch, barrier and per-layer work counters
+SYNC_WORDS = 3 + 24  # fhe_conv_tc_stack: launch, relayout, GEMM and per-layer work counters
 MAX_STACK = 24
 _stack_sync: dict[tuple, torch.Tensor] = {}
 
@@ -385,12 +390,10 @@ def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
         sync = _stack_sync.get(key)
         if sync is None:
             sync = _stack_sync[key] = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=device.require_cuda())
-    need = max(tc.x_bytes for tc, *_ in jobs)
-    X0 = device.scratch("conv_tc_x0", need)
-    X1 = device.scratch("conv_tc_x1", need) if len(jobs) > 1 else 0
+    need = -(-max(tc.x_bytes for tc, *_ in jobs) // 256) * 256
+    X = device.scratch("conv_tc_x", need * (3 if len(jobs) > 1 else 1))
     arr = (_native.ConvTcLayer * len(jobs))(*[tc.layer(inp, out) for tc, inp, out in jobs])
-    rc = _native.fn("fhe_conv_tc_stack")(tc0.q, tc0.n, arr, len(jobs), X0, X1 or None, sync.data_ptr(),
-                                         device.stream())
+    rc = _native.fn("fhe_conv_tc_stack")(tc0.q, tc0.n, arr, len(jobs), X, need, sync.data_ptr(), device.stream())
     if rc:
         _native.check(rc)
 
@@ -410,17 +413,15 @@ def _streams():
 def issue_k1(items, on_gemm=None) -> list:
     """Enqueue K1 for independent jobs [(plan, inp, ready_event | None, out)]
     on the current stream. Consecutive tensor-core jobs (up to 24) share ONE
-    fhe_conv_tc_stack launch — each layer's relayout overlaps the previous
-    layer's GEMM tail and no per-layer launch gap remains; other jobs run one
-    launch each. `on_gemm(i, "start" | "end")` is called around every
+    fhe_conv_tc_stack launch — layer i+1 is relaid out while layer i's GEMM
+    runs and no per-layer launch gap remains; other jobs run one launch each. `on_gemm(i, "start" | "end")` is called around every
     tensor-core launch (i = its first job; e.g. to record timing events).
     Returns one completion event per job (jobs of one launch share it),
     recorded on the current stream. CUDA-graph capturable."""
     comp = torch.cuda.current_stream()
     need = max((plan.tc.x_bytes for plan, *_ in items if plan.path == "tc"), default=0)
     if need:  # size the operand buffers before anything is enqueued
-        device.scratch("conv_tc_x0", need)
-        device.scratch("conv_tc_x1", need)
+        device.scratch("conv_tc_x", 3 * (-(-need // 256) * 256))
     done = [None] * len(items)
     i = 0
     while i < len(items):
@@ -530,7 +531,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     meta = [(x, layer, _proposed_plan(x, layer, params)) for x, layer in jobs]  # validate before enqueueing
     need = max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0)
     if need:
-        device.scratch("conv_tc_x0", need)
+        device.scratch("conv_tc_x", -(-need // 256) * 256)
     outs = []
     for x, layer, plan in meta:  # one pass: job i's download is enqueued before job i+1's upload
         ready = None

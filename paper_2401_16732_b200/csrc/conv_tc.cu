@@ -45,7 +45,8 @@ namespace fhe {
 namespace tc {
 
 constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant
-constexpr int kWarps = 2 + kEpiWarps;
+constexpr int kRelWarps = 6;  // dedicated relayout warps (run ahead of the GEMM)
+constexpr int kWarps = 2 + kEpiWarps + kRelWarps;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kMaxTaps = 64;
 constexpr int kMaxStages = 6;
@@ -54,8 +55,12 @@ constexpr int kEpilogue = 32 * kEpiWarps;
 constexpr int kOcTile = 128;         // output channels per tile (MMA M)
 constexpr int kWTap = kOcTile * 32;  // packed weight bytes per (tap, 32 channels)
 constexpr int kStg = 4096;           // phase-1 staging bytes per warp
-constexpr int kRingBudget = 184 * 1024;
+constexpr int kRingBudget = 168 * 1024;
 constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
+#ifndef FHE_UNITS_PER_GRAB
+#define FHE_UNITS_PER_GRAB 1
+#endif
+constexpr int kUnitsPerGrab = FHE_UNITS_PER_GRAB;  // relayout units taken per work-counter grab
 
 struct LayerDesc {
   const uint64_t* in;  // input ciphertext rows [n_in][2][n]
@@ -71,7 +76,7 @@ struct LayerDesc {
 
 struct StackArgs {
   LayerDesc L[kMaxLayers];
-  unsigned long long* sync;  // [0] launches, [1] barrier arrivals, [2 + l] unit counters
+  unsigned long long* sync;  // [0] launches, [1] relayout done, [2] GEMM done, [3 + l] unit counters
   uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
   int n, nl;
 };
@@ -214,13 +219,19 @@ __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t 
 // masks, 8 in-register 4x4 byte transposes into the lane's 128-byte half
 // record, staged through the warp's shared memory (XOR-swizzled 16-byte
 // chunks) so X is written with full 128-byte lines.
-__device__ __forceinline__ void relayout_unit(const LayerDesc& d, int n, uint64_t q, int unit, int lane,
-                                              uint8_t* stg) {
+struct UnitLoad {
+  uint64_t x[16];
+  uint32_t neg, keep;
+  int y0, jb, pf, kh;
+};
+
+// load half: all 16 loads issued back to back
+__device__ __forceinline__ void relayout_load(const LayerDesc& d, int n, int unit, int lane, UnitLoad& U) {
   const int nyb = (d.Y + 31) / 32;
   const int kh = unit & 1, item = unit >> 1;  // a unit is one 16-channel K half of an item
   const int y0 = (item % nyb) * 32, jb = (item / nyb) % d.JB;
   const int pf = item / (nyb * d.JB), p = pf / d.F, f = pf - p * d.F;
-  const int y = y0 + lane;
+  U.y0 = y0, U.jb = jb, U.pf = pf, U.kh = kh;
   // lane c (< 16) resolves channel jb*32 + kh*16 + c once: its row pointer and
   // the extension slot of position y0; the loop broadcasts them
   const int jm = jb * 32 + kh * 16 + (lane & 15);
@@ -229,7 +240,6 @@ __device__ __forceinline__ void relayout_unit(const LayerDesc& d, int n, uint64_
   const int e0m = n - d.h + y0 + cm.y;  // in [0, 3n)
   const int live = max(0, min(16, d.c_i - jb * 32 - kh * 16));
   const int yoff = min(lane, d.Y - 1 - y0);  // clamped: every load is in bounds
-  uint64_t x[16];
   uint32_t neg = 0;
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
@@ -238,36 +248,43 @@ __device__ __forceinline__ void relayout_unit(const LayerDesc& d, int n, uint64_
     int e = __shfl_sync(0xffffffffu, e0m, c) + yoff;
     const bool lo = e < n, hi = e >= 2 * n;
     e -= lo ? 0 : (hi ? 2 * n : n);
-    x[c] = __ldg(&row[e]);
+    U.x[c] = __ldg(&row[e]);
     neg |= (uint32_t)(lo || hi) << c;
   }
-  const uint32_t keep = y < d.Y ? (1u << live) - 1u : 0u;
-  neg &= keep;
-  if (!__all_sync(0xffffffffu, keep == 0xffffu)) {
+  U.keep = y0 + lane < d.Y ? (1u << live) - 1u : 0u;
+  U.neg = neg & U.keep;
+}
+
+// store half: validity / sign masks, 8 in-register 4x4 byte transposes into
+// the lane's 128-byte half record, staged (XOR-swizzled 16-byte chunks) so X
+// is written with full 128-byte lines
+__device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, int lane, UnitLoad& U,
+                                               uint8_t* stg) {
+  if (!__all_sync(0xffffffffu, U.keep == 0xffffu)) {
 #pragma unroll
-    for (int c = 0; c < 16; ++c) x[c] = ((keep >> c) & 1) ? x[c] : 0;
+    for (int c = 0; c < 16; ++c) U.x[c] = ((U.keep >> c) & 1) ? U.x[c] : 0;
   }
-  if (__any_sync(0xffffffffu, neg != 0)) {
+  if (__any_sync(0xffffffffu, U.neg != 0)) {
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (((neg >> c) & 1) && x[c]) x[c] = q - x[c];
+      if (((U.neg >> c) & 1) && U.x[c]) U.x[c] = q - U.x[c];
   }
   uint32_t w[8][4];
 #pragma unroll
   for (int g4 = 0; g4 < 4; ++g4) {
     const int c = g4 * 4;
-    transpose4x4((uint32_t)x[c], (uint32_t)x[c + 1], (uint32_t)x[c + 2], (uint32_t)x[c + 3], w[0][g4], w[1][g4],
-                 w[2][g4], w[3][g4]);
-    transpose4x4((uint32_t)(x[c] >> 32), (uint32_t)(x[c + 1] >> 32), (uint32_t)(x[c + 2] >> 32),
-                 (uint32_t)(x[c + 3] >> 32), w[4][g4], w[5][g4], w[6][g4], w[7][g4]);
+    transpose4x4((uint32_t)U.x[c], (uint32_t)U.x[c + 1], (uint32_t)U.x[c + 2], (uint32_t)U.x[c + 3], w[0][g4],
+                 w[1][g4], w[2][g4], w[3][g4]);
+    transpose4x4((uint32_t)(U.x[c] >> 32), (uint32_t)(U.x[c + 1] >> 32), (uint32_t)(U.x[c + 2] >> 32),
+                 (uint32_t)(U.x[c + 3] >> 32), w[4][g4], w[5][g4], w[6][g4], w[7][g4]);
   }
   uint4* mine = reinterpret_cast<uint4*>(stg + lane * 128);
 #pragma unroll
   for (int dd = 0; dd < 8; ++dd) mine[dd ^ (lane & 7)] = make_uint4(w[dd][0], w[dd][1], w[dd][2], w[dd][3]);
   __syncwarp();
   // copy-out: 8 lanes per position half (128 contiguous bytes of X)
-  const int rows = min(32, d.Y - y0);
-  uint4* dst = reinterpret_cast<uint4*>(d.X + (((size_t)pf * d.JB + jb) * d.Y + y0) * 256 + kh * 128);
+  const int rows = min(32, d.Y - U.y0);
+  uint4* dst = reinterpret_cast<uint4*>(d.X + (((size_t)U.pf * d.JB + U.jb) * d.Y + U.y0) * 256 + U.kh * 128);
   const uint4* st4 = reinterpret_cast<const uint4*>(stg);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -277,26 +294,53 @@ __device__ __forceinline__ void relayout_unit(const LayerDesc& d, int n, uint64_
   __syncwarp();
 }
 
-// Monotonic launch-scoped counters (never reset, so CUDA-graph replays are
-// safe). The launch epoch e = arrivals / gridDim.x; grid barrier l of launch e
-// completes when the arrival counter reaches ((e-1)·nl + l + 1)·gridDim.x;
-// layer l's unit counter starts launch e at (e-1)·(units + warps in grid)
-// because every warp overshoots it exactly once. The grid is cooperative, so
-// every CTA is resident and the waits cannot deadlock; spins are bounded (a
-// protocol bug traps instead of hanging).
-__device__ __forceinline__ void grid_barrier(unsigned long long* ctr, unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();  // release this CTA's phase-1 stores
-    atomicAdd(ctr, 1ull);
-    for (uint32_t i = 0;; ++i) {
-      unsigned long long v;
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-      if (v >= target) break;
-      if (i > (1u << 28)) __trap();
-    }
+// Cross-CTA protocol — monotonic launch-scoped counters in `sync` (never
+// reset, so CUDA-graph replays are safe); the grid is cooperative (every CTA
+// resident) and all spins are bounded (a protocol bug traps, never hangs).
+// P(l) = warps per CTA that relayout layer l: epilogue + relayout warps for
+// layer 0 (nothing else to do yet), the kRelWarps relayout warps afterwards.
+//   sync[0]      launch arrivals: epoch e = arrivals / gridDim.x + 1
+//   sync[1]      relayout completions (one per participating warp): layer
+//                l's X is ready when it reaches
+//                (e-1)·G·(P(0) + kRelWarps·(nl-1)) + G·(P(0) + kRelWarps·l)
+//   sync[2]      GEMM completions (one per CTA per layer): layer l's X has
+//                been fully consumed at (e-1)·G·nl + G·(l+1)
+//   sync[3 + l]  layer l's relayout work counter, taken g = kUnitsPerGrab
+//                units at a time: launch e starts at
+//                (e-1)·(g·ceil(units/g) + g·G·P(l)) (each participating warp
+//                overshoots it exactly once)
+// The relayout warps run up to three layers ahead of the GEMM: layer l's X
+// buffer (three rotate) is overwritten only after every CTA finished the
+// GEMM of layer l-3. The loader waits for "X ready" before layer l's first
+// stage.
+// Polls are relaxed (an acquire load would invalidate L1 on every poll); one
+// acquire fence follows a successful poll.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned long long target) {
+  for (uint32_t i = 0; ld_relaxed(p) < target; ++i) {
+    if (i > (1u << 26)) __trap();
+    __nanosleep(64);
   }
-  __syncthreads();
+  fence_acquire();
+}
+
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid_constant__ StackArgs A) {
@@ -306,8 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   const uint64_t q = A.q;
   int ring_bytes = 0;
   for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].nst * A.L[l].stage_bytes);
-  uint8_t* stg = smem + ring_bytes + warp * kStg;  // this warp's phase-1 staging (outside the ring)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes + kWarps * kStg);
+  uint8_t* stg = smem + ring_bytes + (warp - 2) * kStg;  // relayout staging of warps >= 2 (outside the ring)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes + (kEpiWarps + kRelWarps) * kStg);
   // [0,6) full, [6,12) empty, 12+{0,1} tmem_full, 12+{2,3} tmem_empty
   uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
   const uint32_t bar0 = smem_u32(bars);
@@ -316,10 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   auto tfull_bar = [&](int b) { return bar0 + 8 * (2 * kMaxStages + b); };
   auto tempty_bar = [&](int b) { return bar0 + 8 * (2 * kMaxStages + 2 + b); };
 
-  if (tid == 0) {
-    const unsigned long long arr = atomicAdd(A.sync, 1ull);
-    slot[1] = (unsigned)(arr / (unsigned long long)G);  // epoch - 1
-  }
+  if (tid == 0) slot[1] = (unsigned)(atomicAdd(A.sync, 1ull) / (unsigned long long)G);  // epoch - 1
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
                  "n"(2 * kAccCols));
@@ -342,86 +383,105 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = slot[0];
   const unsigned long long e1 = slot[1];  // epoch - 1
-
-  // per-role pipeline state that persists across layers
-  int s_ld = 0, s_mma = 0;          // stage cursors (loader / MMA)
-  uint32_t par_ld = 0, par_mma = 0;  // per-stage phase parities: fills done / consumes done
-  uint32_t used = 0;                 // stages filled at least once (loader)
-  int prev_stage_bytes = -1, prev_stage_bytes_mma = -1;
-  int tl = 0;                        // tile counter (TMEM buffer parity) for MMA and epilogue
-  const int quad = warp & 3, sub = (warp - 2) >> 2;
-  const int k8 = opaque(1 << 8), k16 = opaque(1 << 16), k24 = opaque(1 << 24);
-
-  for (int l = 0; l < nl; ++l) {
+  constexpr int P0 = kEpiWarps + kRelWarps;  // warps per CTA relaying out layer 0
+  const unsigned long long Gu = (unsigned long long)G;
+  auto ready_target = [&](int l) {
+    return e1 * Gu * (P0 + kRelWarps * (nl - 1)) + Gu * (P0 + kRelWarps * l);
+  };
+  auto gemm_target = [&](int l) { return e1 * Gu * nl + Gu * (l + 1); };
+  // relayout units of layer l until none is left, then publish this warp's completion
+  auto relayout_layer = [&](int l, int participants) {
     const LayerDesc& d = A.L[l];
-    // ------------------------------------------------------ phase 1: relayout
-    if (tid == 0) TC_TRACE(2, l);
-    {
-      const unsigned long long base = e1 * (unsigned long long)(d.units + G * kWarps);
-      for (;;) {
-        unsigned long long u = 0;
-        if (lane == 0) u = atomicAdd(A.sync + 2 + l, 1ull) - base;
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= (unsigned long long)d.units) break;
-        relayout_unit(d, n, q, (int)u, lane, stg);
+    constexpr unsigned long long kG = kUnitsPerGrab;
+    const unsigned long long per_launch = kG * ((d.units + kG - 1) / kG) + kG * Gu * participants;
+    for (;;) {
+      unsigned long long u = 0;
+      if (lane == 0) u = atomicAdd(A.sync + 3 + l, kG) - e1 * per_launch;
+      u = __shfl_sync(0xffffffffu, u, 0);
+      if (u >= (unsigned long long)d.units) break;
+      if (kUnitsPerGrab == 1) {
+        UnitLoad U0;
+        relayout_load(d, n, (int)u, lane, U0);
+        relayout_store(d, q, lane, U0, stg);
+      } else {
+        UnitLoad U0, U1;
+        const bool two = u + 1 < (unsigned long long)d.units;
+        relayout_load(d, n, (int)u, lane, U0);
+        if (two) relayout_load(d, n, (int)u + 1, lane, U1);
+        relayout_store(d, q, lane, U0, stg);
+        if (two) relayout_store(d, q, lane, U1, stg);
       }
     }
-    if (lane == 0) TC_TRACE(3, l * 16 + warp);
-    grid_barrier(A.sync + 1, (e1 * nl + l + 1) * (unsigned long long)G);
-    if (tid == 0) TC_TRACE(7, l);
-    // ------------------------------------------------------ phase 2: GEMM
-    const int npos = d.npos, JB = d.JB, taps = d.taps;
-    const uint32_t wstage = (uint32_t)taps * kWTap;
-    if (warp == 0) {
-      // MMA issue
-      if (lane == 0) {
-        if (d.stage_bytes != prev_stage_bytes_mma) s_mma = 0;  // the loader drained and re-partitioned the ring
-        prev_stage_bytes_mma = d.stage_bytes;
-        const uint32_t idesc = idesc_i8(8 * npos);
+    __threadfence();  // this warp's X stores before its completion count
+    __syncwarp();
+    if (lane == 0) atomicAdd(A.sync + 1, 1ull);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ MMA issue
+    if (lane == 0) {
+      int s_mma = 0, prev_sb = -1, tl = 0;
+      uint32_t par = 0;  // per-stage phase parity of the full barriers
+      for (int l = 0; l < nl; ++l) {
+        const LayerDesc& d = A.L[l];
+        if (d.tiles <= (int)blockIdx.x) continue;  // no tiles of this layer here (the loader skips it too)
+        if (d.stage_bytes != prev_sb) s_mma = 0;  // the loader drained and re-partitioned the ring
+        prev_sb = d.stage_bytes;
+        const uint32_t idesc = idesc_i8(8 * d.npos);
         for (int t = blockIdx.x; t < d.tiles; t += G, ++tl) {
           const int buf = tl & 1;
           mbar_wait(tempty_bar(buf), ((tl >> 1) & 1) ^ 1);  // epilogue released this buffer
           asm volatile("tcgen05.fence::after_thread_sync;");
+          TC_TRACE(0, tl);
           const uint32_t acc = tmem + buf * kAccCols;
-          for (int jb = 0; jb < JB; ++jb) {
+          for (int jb = 0; jb < d.JB; ++jb) {
             const int s = s_mma;
-            mbar_wait(full_bar(s), (par_mma >> s) & 1);
-            par_mma ^= 1u << s;
+            mbar_wait(full_bar(s), (par >> s) & 1);
+            par ^= 1u << s;
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
             const uint32_t sw = sx + d.win_bytes;
-            for (int tp = 0; tp < taps; ++tp)
+            for (int tp = 0; tp < d.taps; ++tp)
               mma_i8(acc, umma_desc(sw + tp * kWTap), umma_desc(sx + (uint32_t)d.tap_off[tp] * 256), idesc,
                      (jb | tp) != 0);
             mma_commit(empty_bar(s));  // stage free once these MMAs retire
             s_mma = s + 1 == d.nst ? 0 : s + 1;
           }
           mma_commit(tfull_bar(buf));  // accumulator complete
+          TC_TRACE(1, tl);
         }
       }
-      __syncwarp();
-    } else if (warp == 1) {
-      // stage loads
-      if (lane == 0) {
-        if (d.stage_bytes != prev_stage_bytes) {
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ stage loads
+    if (lane == 0) {
+      int s_ld = 0, prev_sb = -1;
+      uint32_t par = 0, used = 0;  // per-stage fill parity; stages filled at least once
+      for (int l = 0; l < nl; ++l) {
+        const LayerDesc& d = A.L[l];
+        if (d.tiles <= (int)blockIdx.x) continue;  // no tiles of this layer here
+        if (d.stage_bytes != prev_sb) {
           // new ring partition: every stage of the old one must be consumed first
           for (int s = 0; s < kMaxStages; ++s)
-            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par_ld >> s) & 1) ^ 1, 32);
+            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
           s_ld = 0;
-          prev_stage_bytes = d.stage_bytes;
+          prev_sb = d.stage_bytes;
         }
+        wait_count(A.sync + 1, ready_target(l));    // layer l's X is complete
+        TC_TRACE(7, l);
         asm volatile("fence.proxy.async.global;");  // generic-proxy X stores -> cp.async.bulk reads
+        const uint32_t wstage = (uint32_t)d.taps * kWTap;
         const size_t plane_stride = (size_t)d.Y * 256;
-        const uint32_t win_load = (uint32_t)((npos + 2 * d.h) * 256);
+        const uint32_t win_load = (uint32_t)((d.npos + 2 * d.h) * 256);
         for (int t = blockIdx.x; t < d.tiles; t += G) {
           const Tile T = tile_of(t, d, n);
-          const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * JB) * plane_stride + (size_t)T.s0 * 256;
-          const uint8_t* wbase = d.W + (size_t)T.ob * JB * wstage;
-          for (int jb = 0; jb < JB; ++jb) {
+          const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
+          const uint8_t* wbase = d.W + (size_t)T.ob * d.JB * wstage;
+          for (int jb = 0; jb < d.JB; ++jb) {
             const int s = s_ld;
-            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par_ld >> s) & 1) ^ 1, 32);
+            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
             used |= 1u << s;
-            par_ld ^= 1u << s;
+            par ^= 1u << s;
             const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
                          "r"(win_load + wstage)
@@ -432,12 +492,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
           }
         }
       }
-      __syncwarp();
-    } else {
-      // epilogue: lane = output channel within the quadrant; a 32-column TMEM
-      // chunk holds 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and
-      // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,
-      // q > 2^56); V = lo + 2^32 hi.
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    // ------------------------------------------------------- relayout warps
+    if (tid == 32 * (2 + kEpiWarps)) TC_TRACE(2, 0);
+    relayout_layer(0, P0);
+    for (int l = 1; l < nl; ++l) {
+      if (l >= 3) wait_count(A.sync + 2, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
+      relayout_layer(l, kRelWarps);
+      if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(3, l);
+    }
+  } else {
+    // -------------------------------------------------------------- epilogue
+    const int quad = warp & 3, sub = (warp - 2) >> 2;
+    const int k8 = opaque(1 << 8), k16 = opaque(1 << 16), k24 = opaque(1 << 24);
+    relayout_layer(0, P0);  // nothing to do yet but help with layer 0
+    int tl = 0;
+    for (int l = 0; l < nl; ++l) {
+      const LayerDesc& d = A.L[l];
       for (int t = blockIdx.x; t < d.tiles; t += G, ++tl) {
         const Tile T = tile_of(t, d, n);
         const int buf = tl & 1;
@@ -447,11 +519,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         if (lane == 0 && warp == 2) TC_TRACE(5, tl);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
+          // lane = output channel within the quadrant; a 32-column TMEM chunk
+          // holds 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and
+          // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,
+          // q > 2^56); V = lo + 2^32 hi.
           const uint64_t bd = (T.p == 0 && d.bias && o < d.c_o) ? d.bias[o] : 0;
           const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
           uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + T.s0;
 #pragma unroll 1
-          for (int k = sub; k < npos / 4; k += kEpiWarps / 4) {
+          for (int k = sub; k < d.npos / 4; k += kEpiWarps / 4) {
             uint32_t v[32];
             TMEM_LD32(acc + k * 32, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;");
@@ -486,6 +562,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         mbar_arrive(tempty_bar(buf));
         if (lane == 0 && warp == 2) TC_TRACE(6, tl);
       }
+      // this CTA consumed all of layer l's X (every tile's MMAs completed)
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue));
+      if (tid == 64) atomicAdd(A.sync + 2, 1ull);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -565,12 +644,12 @@ int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stre
   return FHE_OK;
 }
 
-int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl, uint8_t* X0, uint8_t* X1,
+int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl, uint8_t* X, size_t x_stride,
                       uint64_t* sync, void* stream) {
   if (q < (1ull << 56) || q >= (1ull << 62)) return fail(FHE_ERR_VALUE, "tc path needs 2^56 <= q < 2^62");
   if (n < 64 || (n & (n - 1))) return fail(FHE_ERR_VALUE, "tc path needs a power-of-two n >= 64");
   if (nl < 1 || nl > tc::kMaxLayers) return fail(FHE_ERR_VALUE, "tc stack: 1..%d layers", tc::kMaxLayers);
-  if (!layers || !X0 || !sync || (nl > 1 && !X1)) return fail(FHE_ERR_VALUE, "null tc stack operand");
+  if (!layers || !X || !sync) return fail(FHE_ERR_VALUE, "null tc stack operand");
   static tc::StackArgs A;  // large: kept off the stack; launches are issued from one host thread at a time
   A.q = q;
   A.w32p = h_shoup(1ull << 32, q);
@@ -590,7 +669,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
       return fail(FHE_ERR_VALUE, "tc layer %d: plane sums would exceed s32", l);
     d.in = s.in;
     d.chan = reinterpret_cast<const int2*>(s.chan);
-    d.X = (l & 1) ? X1 : X0;
+    d.X = X + (size_t)(l % 3) * x_stride;
     d.W = reinterpret_cast<const uint8_t*>(s.w);
     d.bias = s.bias_delta;
     d.bmask = s.bias_mask;
@@ -615,13 +694,15 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
     if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
     d.tiles = (n / d.npos) * d.OB * 2 * d.F;
+    if (nl > 1 && (size_t)2 * d.F * d.JB * d.Y * 256 > x_stride)
+      return fail(FHE_ERR_VALUE, "tc layer %d: X stride smaller than its operand", l);
     const long long units = 2ll * ((d.Y + 31) / 32) * d.JB * 2 * d.F;
     if (units > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc layer %d too large", l);
     d.units = (int)units;
     max_tiles = std::max(max_tiles, d.tiles);
     ring = std::max(ring, d.nst * d.stage_bytes);
   }
-  const size_t smem = (size_t)ring + tc::kWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
+  const size_t smem = (size_t)ring + (tc::kEpiWarps + tc::kRelWarps) * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
   static bool attr = false;
   if (!attr) {
     FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));

@@ -1,0 +1,52 @@
+"""Timeline of CTA 0 through the stacked K1-TC launch of a bench workload.
+
+Development probe:  python tools/trace_stack.py [--workload config4]
+Prints per layer (cycles from kernel start, CTA 0): relayout warp done with
+the layer, loader sees the layer's X ready, first MMA tile start, last MMA
+commit, last epilogue done.
+"""
+
+import argparse
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import bench  # noqa: E402
+from paper_2401_16732_b200 import _native, conv  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="config4")
+    args = ap.parse_args()
+    P, layers = bench.build_stack(args.workload)
+    items = [(L["plan"], L["dev"], None, L["out"]) for L in layers]
+    conv.issue_k1(items)
+    torch.cuda.synchronize()
+    buf = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
+    _native.call("fhe_debug_trace", buf.data_ptr())
+    conv.issue_k1(items)
+    torch.cuda.synchronize()
+    _native.call("fhe_debug_trace", None)
+    t = buf.cpu().numpy().reshape(8, 4096).astype(np.int64)
+    t0 = t[2][0]
+    rel = lambda v: int(v - t0) if v else -1  # noqa: E731
+    tl = 0
+    print(f"{'layer':10s} {'rel_done':>9s} {'x_ready':>9s} {'mma0':>9s} {'mma_end':>9s} {'epi_end':>9s} tiles(CTA0)")
+    for l, L in enumerate(layers):
+        d = L["plan"].tc
+        tiles = (P.n // d.pos_tile) * -(-d.c_o // 128) * 2 * d.frags
+        mine = len(range(0, tiles, 148))
+        first, last = tl, tl + mine - 1
+        print(f"{L['layer'].name:10s} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
+              f"{rel(t[1][last]) if mine else -1:9d} {rel(t[6][last]) if mine else -1:9d} {mine}")
+        tl += mine
+
+
+
+if __name__ == "__main__":
+    main()

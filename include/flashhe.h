@@ -191,7 +191,7 @@ int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in,
  * One layer = conv.conv_proposed; several = conv.issue_k1 / the serving path. */
 typedef struct fhe_conv_tc_layer {
   const uint64_t* in;     /* DEVICE [n_in][2][n] input ciphertexts */
-  int c_i, frags, fstride;
+  int n_in, c_i, frags, fstride;
   const int32_t* chan;    /* DEVICE int32 pairs [c_i][2] = (source ct, slot shift) of
                              channel j (the packing of conv.py:113-130); fragment f
                              reads source + f*fstride */

@@ -128,7 +128,7 @@ class ConvTcLayer(ctypes.Structure):
     """struct fhe_conv_tc_layer (include/flashhe.h)."""
 
     _fields_ = [
-        ("in_", _vp), ("c_i", _int), ("frags", _int), ("fstride", _int), ("chan", _vp), ("h", _int),
+        ("in_", _vp), ("n_in", _int), ("c_i", _int), ("frags", _int), ("fstride", _int), ("chan", _vp), ("h", _int),
         ("w", _vp), ("c_o", _int), ("taps", _int), ("pos_tile", _int), ("tap_steps", _vp),
         ("bias_delta", _vp), ("bias_mask", _vp), ("out", _vp),
     ]

@@ -358,7 +358,7 @@ class ConvTcPlan:
     def layer(self, inp: torch.Tensor, out: torch.Tensor) -> "_native.ConvTcLayer":
         """This layer's entry of a fhe_conv_tc_stack launch."""
         return _native.ConvTcLayer(
-            inp.data_ptr(), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
+            inp.data_ptr(), inp.numel() // (2 * self.n), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
             self.c_o, self.taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
             device.ptr(self.mask), out.data_ptr())
 

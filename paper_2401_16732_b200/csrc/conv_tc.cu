@@ -70,7 +70,9 @@ struct LayerDesc {
   const uint64_t* bias;
   const uint8_t* bmask;
   uint64_t* out;
+  size_t in_bytes, w_bytes;  // extents of the input and weights (L2 prefetch)
   int Y, JB, F, c_i, fstride, c_o, OB, taps, h, npos, nst, stage_bytes, win_bytes, tiles, units;
+  int toff;  // tiles of the previous layers mod gridDim.x: tiles are dealt round-robin over the whole stack
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
 
@@ -183,6 +185,12 @@ __device__ __forceinline__ Tile tile_of(int t, const LayerDesc& d, int n) {
   r.f = t % d.F;
   r.p = t / d.F;
   return r;
+}
+
+// first tile of layer d for this CTA (continuing the stack-wide round-robin)
+__device__ __forceinline__ int first_tile(const LayerDesc& d) {
+  const int G = gridDim.x;
+  return ((int)blockIdx.x - d.toff + G) % G;
 }
 
 // a value the compiler cannot constant-fold or strength-reduce
@@ -313,6 +321,18 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
 // buffer (three rotate) is overwritten only after every CTA finished the
 // GEMM of layer l-3. The loader waits for "X ready" before layer l's first
 // stage.
+// This CTA's 1/gridDim.x share of [p, p + bytes) into L2 (bulk prefetch).
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  const size_t share = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~(size_t)15;
+  const size_t off = share * blockIdx.x;
+  if (off >= bytes) return;
+  const size_t len = min(share, bytes - off) & ~(size_t)15;
+  if (len)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const uint8_t*>(p) + off),
+                 "r"((uint32_t)len)
+                 : "memory");
+}
+
 // Polls are relaxed (an acquire load would invalidate L1 on every poll); one
 // acquire fence follows a successful poll.
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
@@ -390,15 +410,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   };
   auto gemm_target = [&](int l) { return e1 * Gu * nl + Gu * (l + 1); };
   // relayout units of layer l until none is left, then publish this warp's completion
+  // relayout units of layer l until none is left, then publish this warp's
+  // completion. The next grab's atomic is issued before the current unit is
+  // processed, so its round trip overlaps useful work.
   auto relayout_layer = [&](int l, int participants) {
     const LayerDesc& d = A.L[l];
     constexpr unsigned long long kG = kUnitsPerGrab;
-    const unsigned long long per_launch = kG * ((d.units + kG - 1) / kG) + kG * Gu * participants;
+    const unsigned long long base = e1 * (kG * ((d.units + kG - 1) / kG) + kG * Gu * participants);
+    unsigned long long nxt = 0;
+    if (lane == 0) nxt = atomicAdd(A.sync + 3 + l, kG);
     for (;;) {
-      unsigned long long u = 0;
-      if (lane == 0) u = atomicAdd(A.sync + 3 + l, kG) - e1 * per_launch;
-      u = __shfl_sync(0xffffffffu, u, 0);
+      const unsigned long long u = __shfl_sync(0xffffffffu, nxt, 0) - base;
       if (u >= (unsigned long long)d.units) break;
+      if (lane == 0) nxt = atomicAdd(A.sync + 3 + l, kG);
       if (kUnitsPerGrab == 1) {
         UnitLoad U0;
         relayout_load(d, n, (int)u, lane, U0);
@@ -424,11 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
       uint32_t par = 0;  // per-stage phase parity of the full barriers
       for (int l = 0; l < nl; ++l) {
         const LayerDesc& d = A.L[l];
-        if (d.tiles <= (int)blockIdx.x) continue;  // no tiles of this layer here (the loader skips it too)
+        if (d.tiles <= first_tile(d)) continue;  // no tiles of this layer here (the loader skips it too)
         if (d.stage_bytes != prev_sb) s_mma = 0;  // the loader drained and re-partitioned the ring
         prev_sb = d.stage_bytes;
         const uint32_t idesc = idesc_i8(8 * d.npos);
-        for (int t = blockIdx.x; t < d.tiles; t += G, ++tl) {
+        for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
           const int buf = tl & 1;
           mbar_wait(tempty_bar(buf), ((tl >> 1) & 1) ^ 1);  // epilogue released this buffer
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -459,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
       uint32_t par = 0, used = 0;  // per-stage fill parity; stages filled at least once
       for (int l = 0; l < nl; ++l) {
         const LayerDesc& d = A.L[l];
-        if (d.tiles <= (int)blockIdx.x) continue;  // no tiles of this layer here
+        if (d.tiles <= first_tile(d)) continue;  // no tiles of this layer here
         if (d.stage_bytes != prev_sb) {
           // new ring partition: every stage of the old one must be consumed first
           for (int s = 0; s < kMaxStages; ++s)
@@ -473,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         const uint32_t wstage = (uint32_t)d.taps * kWTap;
         const size_t plane_stride = (size_t)d.Y * 256;
         const uint32_t win_load = (uint32_t)((d.npos + 2 * d.h) * 256);
-        for (int t = blockIdx.x; t < d.tiles; t += G) {
+        for (int t = first_tile(d); t < d.tiles; t += G) {
           const Tile T = tile_of(t, d, n);
           const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
           const uint8_t* wbase = d.W + (size_t)T.ob * d.JB * wstage;
@@ -496,8 +520,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   } else if (warp >= 2 + kEpiWarps) {
     // ------------------------------------------------------- relayout warps
     if (tid == 32 * (2 + kEpiWarps)) TC_TRACE(2, 0);
+    const bool pf = tid == 32 * (2 + kEpiWarps);  // one thread per CTA issues the L2 prefetches
+    if (pf && nl > 1) {
+      prefetch_l2(A.L[1].in, A.L[1].in_bytes);
+      prefetch_l2(A.L[0].W, A.L[0].w_bytes);
+    }
     relayout_layer(0, P0);
     for (int l = 1; l < nl; ++l) {
+      if (pf) {  // next layer's input (read by relayout) and this layer's weights (read by the GEMM)
+        if (l + 1 < nl) prefetch_l2(A.L[l + 1].in, A.L[l + 1].in_bytes);
+        prefetch_l2(A.L[l].W, A.L[l].w_bytes);
+      }
       if (l >= 3) wait_count(A.sync + 2, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
       relayout_layer(l, kRelWarps);
       if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(3, l);
@@ -510,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
     int tl = 0;
     for (int l = 0; l < nl; ++l) {
       const LayerDesc& d = A.L[l];
-      for (int t = blockIdx.x; t < d.tiles; t += G, ++tl) {
+      for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
         const Tile T = tile_of(t, d, n);
         const int buf = tl & 1;
         const int o = T.ob * kOcTile + quad * 32 + lane;
@@ -656,13 +689,20 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   A.n = n;
   A.nl = nl;
   A.sync = reinterpret_cast<unsigned long long*>(sync);
-  int max_tiles = 0, ring = 0;
+  int max_tiles = 0, ring = 0, toff = 0;
+  static int sms_now = 0;
+  if (!sms_now) {
+    int dev = 0;
+    FHE_CUDA(cudaGetDevice(&dev));
+    FHE_CUDA(cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev));
+  }
   for (int l = 0; l < nl; ++l) {
     const fhe_conv_tc_layer& s = layers[l];
     tc::LayerDesc& d = A.L[l];
     if (s.c_i < 1 || s.frags < 1 || s.c_o < 1 || s.taps < 1 || s.taps > tc::kMaxTaps || s.h < 0 || 2 * s.h >= n)
       return fail(FHE_ERR_VALUE, "tc layer %d: bad shape", l);
     if (!s.in || !s.chan || !s.w || !s.out || !s.tap_steps) return fail(FHE_ERR_VALUE, "tc layer %d: null operand", l);
+    if (s.n_in < 1) return fail(FHE_ERR_VALUE, "tc layer %d: n_in must be >= 1", l);
     if (s.bias_delta && !s.bias_mask) return fail(FHE_ERR_VALUE, "tc layer %d: bias needs a mask", l);
     if (s.pos_tile != 16 && s.pos_tile != 32) return fail(FHE_ERR_VALUE, "tc layer %d: pos_tile must be 16 or 32", l);
     if (127ll * 255 * ((s.c_i + 31) / 32 * 32) * s.taps >= (1ll << 31))
@@ -684,6 +724,8 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.taps = s.taps;
     d.h = s.h;
     d.npos = s.pos_tile;
+    d.in_bytes = (size_t)s.n_in * 2 * n * 8;
+    d.w_bytes = (size_t)d.OB * d.JB * d.taps * tc::kWTap;
     for (int t = 0; t < s.taps; ++t) {
       const int off = s.tap_steps[t] + s.h;
       if (off < 0 || off > 2 * s.h) return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
@@ -700,6 +742,8 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     if (units > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc layer %d too large", l);
     d.units = (int)units;
     max_tiles = std::max(max_tiles, d.tiles);
+    d.toff = toff;
+    toff = (toff + d.tiles) % sms_now;
     ring = std::max(ring, d.nst * d.stage_bytes);
   }
   const size_t smem = (size_t)ring + (tc::kEpiWarps + tc::kRelWarps) * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
@@ -708,16 +752,10 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    FHE_CUDA(cudaGetDevice(&dev));
-    FHE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
   // persistent and cooperative: every CTA must be resident for the grid barriers
   (void)max_tiles;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(sms);
+  cfg.gridDim = dim3(sms_now);
   cfg.blockDim = dim3(tc::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;

@@ -36,11 +36,13 @@ def main():
     t0 = t[2][0]
     rel = lambda v: int(v - t0) if v else -1  # noqa: E731
     tl = 0
+    toff = 0
     print(f"{'layer':10s} {'rel_done':>9s} {'x_ready':>9s} {'mma0':>9s} {'mma_end':>9s} {'epi_end':>9s} tiles(CTA0)")
     for l, L in enumerate(layers):
         d = L["plan"].tc
         tiles = (P.n // d.pos_tile) * -(-d.c_o // 128) * 2 * d.frags
-        mine = len(range(0, tiles, 148))
+        mine = len(range((0 - toff) % 148, tiles, 148))
+        toff = (toff + tiles) % 148
         first, last = tl, tl + mine - 1
         print(f"{L['layer'].name:10s} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
               f"{rel(t[1][last]) if mine else -1:9d} {rel(t[6][last]) if mine else -1:9d} {mine}")

@@ -128,6 +128,17 @@ def build_stack(workload: str, seed: int = 4):
     return P, layers
 
 
+def _traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture summarised in profiles/traffic.json (None if absent)."""
+    path = Path(__file__).resolve().parent / "profiles" / "traffic.json"
+    try:
+        d = json.loads(path.read_text())[kernel]
+        return int(d["dram_bytes_read"] + d["dram_bytes_write"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def world_max(x: float, world: int, dev) -> float:
     """Max over ranks: the slowest rank's device time defines the job's time."""
     if world == 1:
@@ -455,7 +466,8 @@ def main():
                                         "resident smem operands)",
                          "kernel_share_of_step": round(mma_s / step_s, 4),
                          "alg": "16 int8 ops per 60-bit x 8-bit MAC (8 byte planes); MACs = c_o*frags*c_i*f_w^2*2n",
-                         "traffic": None,
+                         "traffic": _traffic("conv_tc_stack_kernel"),
+                         "alg_bytes_per_launch": int(alg_bytes),
                          "stack_tmac60_per_s": round(macs / step_s / 1e12, 3),
                          "int_pipe_peak_tmac60_per_s": round(peak_tmac, 3),
                          "stack_vs_int_pipe_peak": round(macs / step_s / 1e12 / peak_tmac, 3),

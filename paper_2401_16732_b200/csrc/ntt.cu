@@ -16,13 +16,14 @@
 // one write per coefficient (the HBM roofline of 16 B/coefficient).
 // The padding x + x/16 keeps the 64-bit shared accesses at the 2-wavefront
 // minimum for every phase stride.
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
 
 namespace fhe {
 
-__device__ __forceinline__ int spad(int x) { return x + (x >> 4); }
+__host__ __device__ __forceinline__ int spad(int x) { return x + (x >> 4); }
 
 struct LoadMap {
   const uint64_t* src;
@@ -201,6 +202,238 @@ __global__ void __launch_bounds__(512) ntt_kernel(const LimbSet ls, const LoadMa
   }
 }
 
+// ---------------------------------------------------------------------------
+// Split transform for n >= 8192 (n = 2^a · 2^b): the first a Cooley-Tukey
+// stages only mix elements i = i1·2^b + i2 with equal i2 (length-2^a
+// transforms down the columns), the last b stages only mix elements of one
+// contiguous 2^b block. With the merged twiddles psi_brv the column transforms
+// all use psi[(2^a + i1) >> (a - s)] and block k's use
+// psi[(((2^a + k) << b) + i2) >> (b - s')], so the transform splits into two
+// launches with no twiddle pass and no transpose — each over small CTAs
+// (16 columns or 16 blocks, ~17 KB of shared memory) that keep every SM busy
+// and overlap memory with butterflies. The inverse runs the same two
+// launches in the opposite order (GS, n^-1 folded into stage 0). Values stay
+// lazy ([0,4q) / [0,2q)) between the launches; the second one canonicalises.
+constexpr int kSplitW = 16;  // columns (first launch) or blocks (second launch) per CTA
+constexpr int kSplitMinLog = 13;
+
+static bool split_enabled() {  // FHE_NTT_SPLIT=0 selects the one-CTA-per-row kernel (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_NTT_SPLIT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int LOGR, int R, bool INV, class IDX>
+__device__ __forceinline__ void split_phase(uint64_t* sm, IDX idx, const NttDesc& d, uint64_t O, int Lg, int s,
+                                            int item, bool fold_ninv) {
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  const int tl = Lg - (s + R);
+  const int base = ((item >> tl) << (tl + LOGR)) + (item & ((1 << tl) - 1));
+  uint64_t e[1 << LOGR];
+#pragma unroll
+  for (int i = 0; i < (1 << LOGR); ++i) e[i] = sm[idx(base + (i << tl))];
+  if constexpr (!INV) {
+    static_for<0, R>([&](auto ai) {
+      constexpr int a = R - 1 - decltype(ai)::value;  // largest stride first
+      constexpr int dd = 1 << a;
+      const int sh = tl + a + 1;
+#pragma unroll
+      for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+        const ulonglong2 tw = __ldg(&d.psi[(O + base + (g << tl)) >> sh]);
+#pragma unroll
+        for (int u = 0; u < dd; ++u) {
+          uint64_t X = e[g + u];
+          X = X >= q2 ? X - q2 : X;
+          const uint64_t T = shoup_lazy(e[g + u + dd], tw.x, tw.y, q);
+          e[g + u] = X + T;
+          e[g + u + dd] = X - T + q2;
+        }
+      }
+    });
+  } else {
+    static_for<0, R>([&](auto ai) {
+      constexpr int a = decltype(ai)::value;  // smallest stride first
+      constexpr int dd = 1 << a;
+      const int sh = tl + a + 1;
+      if (fold_ninv && a == R - 1) {  // global stage 0: fold n^-1 (ring.py:162)
+#pragma unroll
+        for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+#pragma unroll
+          for (int u = 0; u < dd; ++u) {
+            const uint64_t X = e[g + u], Y = e[g + u + dd];
+            e[g + u] = shoup_lazy(X + Y, d.ninv.x, d.ninv.y, q);
+            e[g + u + dd] = shoup_lazy(X - Y + q2, d.ninv_w1.x, d.ninv_w1.y, q);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+          const ulonglong2 tw = __ldg(&d.ipsi[(O + base + (g << tl)) >> sh]);
+#pragma unroll
+          for (int u = 0; u < dd; ++u) {
+            const uint64_t X = e[g + u], Y = e[g + u + dd];
+            const uint64_t S = X + Y;
+            e[g + u] = S >= q2 ? S - q2 : S;
+            e[g + u + dd] = shoup_lazy(X - Y + q2, tw.x, tw.y, q);
+          }
+        }
+      }
+    });
+  }
+#pragma unroll
+  for (int i = 0; i < (1 << LOGR); ++i) sm[idx(base + (i << tl))] = e[i];
+}
+
+// all stages of a length-2^Lg sub-transform (Lg <= 8), LOGR-stage phases
+template <int LOGR, bool INV, class IDX>
+__device__ __forceinline__ void split_sub(uint64_t* sm, IDX idx, const NttDesc& d, uint64_t O, int Lg, int item,
+                                          bool fold_ninv) {
+  const int nfull = Lg / LOGR, rem = Lg - nfull * LOGR;
+  auto partial = [&](int s) {
+    static_for<1, LOGR>([&](auto ri) {
+      constexpr int R = decltype(ri)::value;
+      if (rem == R) split_phase<LOGR, R, INV>(sm, idx, d, O, Lg, s, item, fold_ninv && s == 0);
+    });
+  };
+  if (!INV) {
+    for (int p = 0; p < nfull; ++p) {
+      split_phase<LOGR, LOGR, false>(sm, idx, d, O, Lg, p * LOGR, item, false);
+      __syncthreads();
+    }
+    if (rem) {
+      partial(nfull * LOGR);
+      __syncthreads();
+    }
+  } else {
+    if (rem) {
+      partial(nfull * LOGR);
+      __syncthreads();
+    }
+    for (int p = nfull - 1; p >= 0; --p) {
+      split_phase<LOGR, LOGR, true>(sm, idx, d, O, Lg, p * LOGR, item, fold_ninv && p == 0);
+      __syncthreads();
+    }
+  }
+}
+
+// COLS: this CTA = row, columns [c0, c0 + 16): stages [0, a).
+// !COLS: this CTA = row, blocks [k0, k0 + 16): stages [a, a + b).
+// from_src: read through the LoadMap (first launch) else read dst in place;
+// final: canonical [0,q) output (second launch).
+template <int LOGR, bool INV, bool COLS>
+__global__ void __launch_bounds__(256) ntt_split_kernel(const LimbSet ls, const LoadMap lm, uint64_t* __restrict__ dst,
+                                                        int a, int b, int from_src, int final_) {
+  extern __shared__ uint64_t sm[];
+  const int per_row = COLS ? (1 << b) / kSplitW : (1 << a) / kSplitW;
+  const int row = blockIdx.x / per_row, part = blockIdx.x % per_row;
+  const int limb = (row / lm.G) % ls.L;
+  const NttDesc d = ls.d[limb];
+  const int n = d.n;
+  const int Lg = COLS ? a : b;
+  const int len = 1 << Lg;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const uint64_t* srow;
+  int shift = 0;
+  if (from_src) {
+    if (lm.ndig > 0) {
+      srow = lm.src + (size_t)(row / lm.ndig) * n;
+      shift = lm.T * (row % lm.ndig);
+    } else {
+      srow = lm.src + (size_t)row * n;
+    }
+  } else {
+    srow = dst + (size_t)row * n;
+  }
+  uint64_t* drow = dst + (size_t)row * n;
+  const uint64_t mask = (from_src && lm.ndig > 0) ? lm.mask : ~0ull;
+  // element (e, v): e = position in the sub-transform, v = column / block in this CTA
+  auto gidx = [&](int e, int v) -> size_t {
+    return COLS ? (size_t)e * (1 << b) + part * kSplitW + v : (size_t)(part * kSplitW + v) * len + e;
+  };
+  auto sidx = [&](int e, int v) -> int { return COLS ? e * kSplitW + v : spad(v * len + e); };
+  // load (pairs of consecutive elements: columns for COLS, positions for blocks)
+  for (int i = tid; i < (len * kSplitW) / 2; i += nthr) {
+    int e, v;
+    if (COLS) {
+      e = (2 * i) / kSplitW;
+      v = (2 * i) % kSplitW;
+    } else {
+      v = (2 * i) / len;
+      e = (2 * i) % len;
+    }
+    ulonglong2 x = *reinterpret_cast<const ulonglong2*>(srow + gidx(e, v));
+    if (from_src && lm.ndig > 0) {
+      x.x = (x.x >> shift) & mask;
+      x.y = (x.y >> shift) & mask;
+    }
+    if (COLS) {
+      sm[sidx(e, v)] = x.x;
+      sm[sidx(e, v + 1)] = x.y;
+    } else {
+      sm[sidx(e, v)] = x.x;
+      sm[sidx(e + 1, v)] = x.y;
+    }
+  }
+  __syncthreads();
+  // one item per thread: (v, phase item)
+  const int ipv = len >> LOGR;  // phase items per sub-transform
+  const int v = COLS ? tid % kSplitW : tid / ipv;
+  const int item = COLS ? tid / kSplitW : tid % ipv;
+  const uint64_t O = COLS ? (uint64_t)len : ((uint64_t)((1 << a) + part * kSplitW + v) << b);
+  auto idx = [&](int e) { return sidx(e, v); };
+  split_sub<LOGR, INV>(sm, idx, d, O, Lg, item, INV && COLS);
+  // store
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  for (int i = tid; i < (len * kSplitW) / 2; i += nthr) {
+    int e, vv;
+    if (COLS) {
+      e = (2 * i) / kSplitW;
+      vv = (2 * i) % kSplitW;
+    } else {
+      vv = (2 * i) / len;
+      e = (2 * i) % len;
+    }
+    uint64_t x = sm[sidx(e, vv)];
+    uint64_t y = COLS ? sm[sidx(e, vv + 1)] : sm[sidx(e + 1, vv)];
+    if (final_) {
+      if (!INV) {
+        x = x >= q2 ? x - q2 : x;
+        y = y >= q2 ? y - q2 : y;
+      }
+      x = csub(x, q);
+      y = csub(y, q);
+    }
+    *reinterpret_cast<ulonglong2*>(drow + gidx(e, vv)) = make_ulonglong2(x, y);
+  }
+}
+
+template <int LOGR, bool INV, bool COLS>
+static int launch_split_one(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int a, int b,
+                            int from_src, int final_, cudaStream_t st) {
+  const int Lg = COLS ? a : b;
+  const int len = 1 << Lg;
+  const int per_row = COLS ? (1 << b) / kSplitW : (1 << a) / kSplitW;
+  const int threads = kSplitW * (len >> LOGR);
+  const size_t smem = COLS ? (size_t)len * kSplitW * 8 : (size_t)(spad(len * kSplitW) + 1) * 8;
+  ntt_split_kernel<LOGR, INV, COLS><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_);
+  FHE_CHECK_LAUNCH("ntt_split_kernel");
+  return FHE_OK;
+}
+
+template <bool INV>
+static int launch_split(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int logn, cudaStream_t st) {
+  const int a = logn / 2, b = logn - a;  // a <= b <= 7 for n <= 16384
+  if (!INV) {
+    if (int rc = launch_split_one<4, false, true>(ls, lm, dst, rows, a, b, 1, 0, st)) return rc;
+    return launch_split_one<4, false, false>(ls, lm, dst, rows, a, b, 0, 1, st);
+  }
+  if (int rc = launch_split_one<4, true, false>(ls, lm, dst, rows, a, b, 1, 0, st)) return rc;
+  return launch_split_one<4, true, true>(ls, lm, dst, rows, a, b, 0, 1, st);
+}
+
 static int build_limbset(const fhe_plan* const* plans, int L, LimbSet* ls, int* n_out) {
   if (L < 1 || L > FHE_MAX_LIMBS) return fail(FHE_ERR_VALUE, "limb count %d out of range", L);
   if (!plans) return fail(FHE_ERR_VALUE, "null plans");
@@ -242,6 +475,7 @@ static int launch(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows,
   if (rows == 0) return FHE_OK;
   int logn = 0;
   while ((1 << logn) < n) ++logn;
+  if (logn >= kSplitMinLog && split_enabled()) return launch_split<INV>(ls, lm, dst, rows, logn, st);
   switch (logn < 4 ? logn : 4) {
     case 1: return launch_t<1, INV>(ls, lm, dst, rows, n, st);
     case 2: return launch_t<2, INV>(ls, lm, dst, rows, n, st);

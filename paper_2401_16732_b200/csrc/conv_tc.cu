@@ -54,8 +54,8 @@ constexpr int kMaxLayers = 24;
 constexpr int kEpilogue = 32 * kEpiWarps;
 constexpr int kOcTile = 128;         // output channels per tile (MMA M)
 constexpr int kWTap = kOcTile * 32;  // packed weight bytes per (tap, 32 channels)
-constexpr int kStg = 4096;           // phase-1 staging bytes per warp
-constexpr int kRingBudget = 168 * 1024;
+constexpr int kStg = 2048;           // relayout staging bytes per warp (16 positions x 128 B)
+constexpr int kRingBudget = 212 * 1024;
 constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
 #ifndef FHE_UNITS_PER_GRAB
 #define FHE_UNITS_PER_GRAB 1
@@ -286,20 +286,26 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
     transpose4x4((uint32_t)(U.x[c] >> 32), (uint32_t)(U.x[c + 1] >> 32), (uint32_t)(U.x[c + 2] >> 32),
                  (uint32_t)(U.x[c + 3] >> 32), w[4][g4], w[5][g4], w[6][g4], w[7][g4]);
   }
-  uint4* mine = reinterpret_cast<uint4*>(stg + lane * 128);
-#pragma unroll
-  for (int dd = 0; dd < 8; ++dd) mine[dd ^ (lane & 7)] = make_uint4(w[dd][0], w[dd][1], w[dd][2], w[dd][3]);
-  __syncwarp();
-  // copy-out: 8 lanes per position half (128 contiguous bytes of X)
+  // two rounds of 16 lanes through a 2 KB staging area: 16 positions x 128 B
   const int rows = min(32, d.Y - U.y0);
   uint4* dst = reinterpret_cast<uint4*>(d.X + (((size_t)U.pf * d.JB + U.jb) * d.Y + U.y0) * 256 + U.kh * 128);
   const uint4* st4 = reinterpret_cast<const uint4*>(stg);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int idx = i * 32 + lane, pos = idx >> 3, ch = idx & 7;
-    if (pos < rows) dst[pos * 16 + ch] = st4[pos * 8 + (ch ^ (pos & 7))];
+  for (int half = 0; half < 2; ++half) {
+    if ((lane >> 4) == half) {
+      uint4* mine = reinterpret_cast<uint4*>(stg + (lane & 15) * 128);
+#pragma unroll
+      for (int dd = 0; dd < 8; ++dd) mine[dd ^ (lane & 7)] = make_uint4(w[dd][0], w[dd][1], w[dd][2], w[dd][3]);
+    }
+    __syncwarp();
+    // copy-out: 8 lanes per position half-record (128 contiguous bytes of X)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = i * 32 + lane, pl = idx >> 3, ch = idx & 7, pos = half * 16 + pl;
+      if (pos < rows) dst[pos * 16 + ch] = st4[pl * 8 + (ch ^ (pl & 7))];
+    }
+    __syncwarp();
   }
-  __syncwarp();
 }
 
 // Cross-CTA protocol — monotonic launch-scoped counters in `sync` (never
@@ -368,10 +374,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = A.n, nl = A.nl, G = gridDim.x;
   const uint64_t q = A.q;
-  int ring_bytes = 0;
+  int ring_bytes = kEpiWarps * kStg;  // (same rule as the host's smem sizing)
   for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].nst * A.L[l].stage_bytes);
-  uint8_t* stg = smem + ring_bytes + (warp - 2) * kStg;  // relayout staging of warps >= 2 (outside the ring)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes + (kEpiWarps + kRelWarps) * kStg);
+  // relayout staging: the relayout warps own areas after the ring; the epilogue
+  // warps (layer 0 only, before any stage is loaded) borrow the ring
+  uint8_t* stg = warp >= 2 + kEpiWarps ? smem + ring_bytes + (warp - 2 - kEpiWarps) * kStg
+                                       : smem + (warp - 2) * kStg;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes + kRelWarps * kStg);
   // [0,6) full, [6,12) empty, 12+{0,1} tmem_full, 12+{2,3} tmem_empty
   uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
   const uint32_t bar0 = smem_u32(bars);
@@ -436,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         if (two) relayout_store(d, q, lane, U1, stg);
       }
     }
+    asm volatile("fence.proxy.async.shared::cta;");  // (epilogue warps) ring staging before later bulk copies
     __threadfence();  // this warp's X stores before its completion count
     __syncwarp();
     if (lane == 0) atomicAdd(A.sync + 1, 1ull);
@@ -746,7 +756,8 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     toff = (toff + d.tiles) % sms_now;
     ring = std::max(ring, d.nst * d.stage_bytes);
   }
-  const size_t smem = (size_t)ring + (tc::kEpiWarps + tc::kRelWarps) * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
+  ring = std::max(ring, tc::kEpiWarps * tc::kStg);  // the epilogue warps' layer-0 staging lives in the ring
+  const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
   static bool attr = false;
   if (!attr) {
     FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));

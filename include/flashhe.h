@@ -234,6 +234,16 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
                         const uint64_t* digits, const uint64_t* keys_mont, int ndig,
                         uint64_t gpow, uint64_t* out, void* stream);
 
+/* Fused PMult-accumulate of the conventional convolution (conv.py:457-564:
+ * the pmult + hadd chain per output ciphertext), EVAL domain, one launch:
+ *   out[o][p] = Σ_{k in [term_off[o], term_off[o+1])} R[terms[2k]][p] ⊙ PT[terms[2k+1]]  mod q
+ * R: DEVICE [nR][2][n] rotated ciphertexts; pt_mont: DEVICE [nPT][n] prepared
+ * plaintexts in Montgomery form (fhe_to_montgomery); term_off: DEVICE int32
+ * [n_out+1]; terms: DEVICE int32 pairs (rotation row, plaintext row), indices
+ * validated by the caller. out: DEVICE [n_out][2][n], canonical. */
+int fhe_pmac(uint64_t q, int n, const uint64_t* R, const uint64_t* pt_mont, const int32_t* term_off,
+             const int32_t* terms, int n_out, uint64_t* out, void* stream);
+
 /* ------------------------------------ K5: x^2+x share arithmetic (act2pc) */
 /* Client share pass, one vectorised pass
  * over decrypted slots w in [0,p): y = (w^2 + w * 2^f) mod p. */

@@ -634,95 +634,101 @@ def _uniform_prepared(value: int, params: RingParams) -> bfv.PreparedPlaintext:
     return bfv.PreparedPlaintext(np.full(params.n, v % params.q, dtype=np.int64))
 
 
-class _RotCache:
-    """Rotations of the input ciphertexts, hoisted per source ciphertext: the
-    digit NTTs of c1 are computed once and shared by every step."""
-
-    def __init__(self, cts, swks, params):
-        self.cts, self.swks, self.params = cts, swks, params
-        self.T = swks.decomp_log
-        self.l = -(-params.q.bit_length() // self.T)
-        self._digits = {}
-        self._rot = {}
-        self._swap = {}
-
-    def _base(self, b: int, swap: bool) -> Ciphertext:
-        if not swap:
-            return self.cts[b]
-        if b not in self._swap:
-            self._swap[b] = self._apply(self.cts[b], ("in", b), bfv.COLUMN_ROTATION)
-        return self._swap[b]
-
-    def _apply(self, ct: Ciphertext, key, step: int) -> Ciphertext:
-        bfv._check_hrot(ct, step, self.swks)
-        t = bfv.ct_rows(ct).reshape(1, 2, self.params.n)
-        if key not in self._digits:
-            self._digits[key] = bfv.key_digits_rows(t[:, 1], self.params, self.T, self.l)
-        ring._bump("modmul", 2 * self.params.n * self.l)
-        r = bfv.keyswitch_rows(t, self._digits[key], step, self.swks)
-        return bfv._ct_from_pair(r, self.params.q, Encoding.BATCH, Domain.EVAL)
-
-    def get(self, b: int, step: int, swap: bool = False) -> Ciphertext:
-        ring_slots = self.params.n // 2
-        step %= ring_slots
-        key = (b, step, swap)
-        if key not in self._rot:
-            base = self._base(b, swap)
-            self._rot[key] = self._apply(base, ("sw" if swap else "in", b), step) if step else base
-        return self._rot[key]
+def _rotations(cts, needed, swks, params) -> tuple[torch.Tensor, dict]:
+    """All rotations the baseline needs, batched: one digit pass per source
+    set (hoisted, bfv.py:485-491) and one K4 launch per (step, swap) over
+    every input ciphertext. Returns rows [nR, 2, n] (EVAL) and a map
+    (b, step, swap) -> row."""
+    n, q = params.n, params.q
+    T = swks.decomp_log
+    l = -(-q.bit_length() // T)
+    B = len(cts)
+    base = bfv.cts_rows(cts).reshape(B, 2, n)
+    groups = sorted(needed)  # (step, swap)
+    srcs = {False: base}
+    if any(sw for _, sw in groups):
+        digits = bfv.key_digits_rows(base[:, 1], params, T, l)
+        srcs[True] = bfv.keyswitch_rows(base, digits, bfv.COLUMN_ROTATION, swks)
+        ring._bump("modmul", 2 * n * l * B)
+    digs = {}
+    rows, index = [], {}
+    for step, swap in groups:
+        src = srcs[swap]
+        if step == 0:
+            r = src
+        else:
+            if swap not in digs:
+                digs[swap] = bfv.key_digits_rows(src[:, 1], params, T, l)
+            r = bfv.keyswitch_rows(src, digs[swap], step, swks)
+            ring._bump("modmul", 2 * n * l * B)
+        for b in range(B):
+            index[(b, step, swap)] = len(rows) * B + b
+        rows.append(r)
+    return torch.cat(rows, 0), index
 
 
 def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.SwitchingKeySet,
                       params: RingParams) -> PackedTensor:
     """Baseline: HRot per (tap, channel offset) + PMult by weight plaintexts
-    + HAdd (conv.py:457-564), on the device kernels."""
+    + HAdd (conv.py:457-564). Same terms, same result; on the device the
+    rotations are batched (hoisted digits, one K4 launch per step) and every
+    output's pmult/hadd chain is one fused K4b accumulation (fhe_pmac)."""
     layout = x.layout
     if x.cts[0].encoding != Encoding.BATCH:
         raise EncodingError("conventional convolution needs batch-encoded input")
     if (layout.height, layout.width) != (layer.height, layer.width) or layout.pad != layer.f_w // 2:
         raise ParameterError("tensor layout does not match the layer geometry")
     taps = _tap_steps(layout, layer.f_w)
-    n, cpu = params.n, layout.c_n
-    in_cts = x.cts
-    rot = _RotCache(in_cts, swks, params)
-    pt_cache: dict = {}
+    n, cpu, ring_slots = params.n, layout.c_n, params.n // 2
+    in_cts = list(x.cts)
+    for ct in in_cts:
+        if ct.domain != Domain.EVAL:
+            raise EncodingError("HRot operates in the evaluation domain")
+    pts: dict[bytes, int] = {}
+    pt_rows: list[np.ndarray] = []
 
-    def prepared_blocks(bw: np.ndarray) -> bfv.PreparedPlaintext:
-        key = bw.tobytes()
-        if key not in pt_cache:
+    def pt_uniform(w: int) -> int:  # _uniform_prepared: constant polynomial, constant NTT
+        key = b"u" + int(w).to_bytes(8, "little", signed=True)
+        if key not in pts:
+            v = int(w) % params.p
+            if v > params.p // 2:
+                v -= params.p
+            pts[key] = len(pt_rows)
+            pt_rows.append(np.full(n, v % params.q, dtype=np.int64))
+        return pts[key]
+
+    def pt_blocks(bw: np.ndarray) -> int:
+        key = b"b" + bw.tobytes()
+        if key not in pts:
             vec = np.zeros(n, dtype=np.int64)
             for (unit_in, blk), w in np.ndenumerate(bw):
                 start = unit_in * layout.ring + blk * layout.tile
                 vec[start : start + layout.tile] = w % params.p
-            pt_cache[key] = bfv.prepare_plaintext(bfv.encode_batch(vec, params), params)
-        return pt_cache[key]
+            pts[key] = len(pt_rows)
+            pt_rows.append(bfv.prepare_plaintext(bfv.encode_batch(vec, params), params).evals)
+        return pts[key]
 
-    def accumulate(acc, term):
-        return term if acc is None else bfv.hadd(acc, term)
-
-    out_cts: list[Ciphertext] = []
+    terms: list[list[tuple]] = []  # per output: [(b, step, swap, pt)]
+    biases = []
     if layout.fragmented:
         pairs = -(-layout.frags // layout.units)
         for oc in range(layer.c_o):
             for t in range(pairs):
-                acc = None
+                tl = []
                 for j in range(layer.c_i):
                     b = j * pairs + t
                     for k, step in enumerate(taps):
                         w = int(layer.weights[oc, j, k])
                         if w:
-                            acc = accumulate(acc, bfv.pmult(rot.get(b, int(step)), _uniform_prepared(w, params), params))
-                if acc is None:
-                    acc = bfv.cmult(in_cts[0], 0, params)
-                if layer.bias is not None and layer.bias[oc]:
-                    acc = _conv_bias_batch(acc, layout, t, int(layer.bias[oc]), params)
-                out_cts.append(acc)
+                            tl.append((b, int(step) % ring_slots, False, pt_uniform(w)))
+                terms.append(tl)
+                biases.append((oc, t))
     else:
         units_in = layout.units_for(layer.c_i)
         units_out = layout.units_for(layer.c_o)
         swaps = (False, True) if layout.units > 1 and max(units_in, units_out) > 1 else (False,)
         for o in range(layout.ct_count(layer.c_o)):
-            acc = None
+            tl = []
             for b in range(len(in_cts)):
                 for swap in swaps:
                     for d in range(1 - cpu, cpu):
@@ -739,11 +745,46 @@ def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.Switching
                                         bw[h, blk] = layer.weights[ocn, ic, k]
                             if not bw.any():
                                 continue
-                            r = rot.get(b, int((step + d * layout.tile) % layout.ring), swap)
-                            acc = accumulate(acc, bfv.pmult(r, prepared_blocks(bw), params))
-            out_cts.append(acc if acc is not None else bfv.cmult(in_cts[0], 0, params))
-        if layer.bias is not None and layer.bias.any():
-            out_cts = _conv_bias_batch_packed(out_cts, layout, layer, params)
+                            tl.append((b, int((step + d * layout.tile) % layout.ring) % ring_slots, swap,
+                                       pt_blocks(bw)))
+            terms.append(tl)
+    needed = {(st, sw) for tl in terms for _, st, sw, _ in tl}
+    for st, sw in needed:  # the reference raises KeyError for a missing key, EncodingError for a bad ct
+        for ct in in_cts[:1]:
+            if st:
+                bfv._check_hrot(ct, st, swks)
+            if sw:
+                bfv._check_hrot(ct, bfv.COLUMN_ROTATION, swks)
+    dev = device.require_cuda()
+    n_out = len(terms)
+    out = torch.empty((n_out, 2, n), dtype=torch.int64, device=dev)
+    if needed:
+        R, index = _rotations(in_cts, needed, swks, params)
+        pt = device.to_device(np.stack(pt_rows))
+        pt_mont = torch.empty_like(pt)
+        _native.call("fhe_to_montgomery", _native.u64_array([params.q]), 1, 1, len(pt_rows), n, pt.data_ptr(),
+                     pt_mont.data_ptr(), device.stream())
+        off = np.zeros(n_out + 1, dtype=np.int32)
+        flat = []
+        for o, tl in enumerate(terms):
+            off[o + 1] = off[o] + len(tl)
+            flat.extend((index[(b, st, sw)], p_) for b, st, sw, p_ in tl)
+        tarr = np.asarray(flat, dtype=np.int32).reshape(-1, 2) if flat else np.zeros((1, 2), np.int32)
+        assert tarr[:, 0].max(initial=0) < R.shape[0] and tarr[:, 1].max(initial=0) < len(pt_rows)
+        ring._bump("modmul", 2 * n * len(flat))
+        off_d = torch.from_numpy(off).to(dev)  # kept alive until the launch is enqueued
+        terms_d = torch.from_numpy(np.ascontiguousarray(tarr)).to(dev)
+        _native.call("fhe_pmac", params.q, n, R.data_ptr(), pt_mont.data_ptr(), off_d.data_ptr(), terms_d.data_ptr(),
+                     n_out, out.data_ptr(), device.stream())
+    else:
+        out.zero_()
+    out_cts = list(bfv.cts_from_rows(out, params.q, Encoding.BATCH, Domain.EVAL))
+    if layout.fragmented:
+        if layer.bias is not None:
+            out_cts = [_conv_bias_batch(ct, layout, t, int(layer.bias[oc]), params) if layer.bias[oc] else ct
+                       for ct, (oc, t) in zip(out_cts, biases)]
+    elif layer.bias is not None and layer.bias.any():
+        out_cts = _conv_bias_batch_packed(out_cts, layout, layer, params)
     return PackedTensor(out_cts, layout, layer.c_o, x.scale + layer.weight_scale)
 
 

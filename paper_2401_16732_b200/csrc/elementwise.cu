@@ -328,6 +328,35 @@ __global__ void keyswitch_kernel(const ModSet ms, int logn, int L, int B, int bc
   }
 }
 
+// ---------------------------------------------------------------- K4b
+// Fused PMult-accumulate of the conventional convolution (conv.py:457-564):
+// out[o][p] = Σ_{(r, w) in terms(o)} R[r][p] ⊙ PT[w]   (mod q, EVAL domain)
+// One thread per (output ciphertext, slot): plaintexts are in Montgomery
+// form, so each term is one 64x64 product and one REDC (canonical), both
+// polys share the plaintext load, the sum stays in 128 bits and is reduced
+// once — the per-term pmult/hadd ciphertexts of the reference never exist.
+__global__ void __launch_bounds__(256) pmac_kernel(const ModDesc m, int n, const uint64_t* __restrict__ R,
+                                                   const uint64_t* __restrict__ PT, const int* __restrict__ off,
+                                                   const int2* __restrict__ terms, uint64_t* __restrict__ out) {
+  const int o = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+  const int k0 = __ldg(&off[o]), k1 = __ldg(&off[o + 1]);
+  for (int k = k0; k < k1; ++k) {
+    const int2 t = __ldg(&terms[k]);
+    const uint64_t w = __ldg(&PT[(size_t)t.y * n + i]);
+    const uint64_t a = __ldg(&R[((size_t)t.x * 2) * n + i]), b = __ldg(&R[((size_t)t.x * 2 + 1) * n + i]);
+    const uint64_t r0 = redc(a * w, __umul64hi(a, w), m), r1 = redc(b * w, __umul64hi(b, w), m);
+    lo0 += r0;
+    hi0 += lo0 < r0;
+    lo1 += r1;
+    hi1 += lo1 < r1;
+  }
+  out[((size_t)o * 2) * n + i] = barrett128(lo0, hi0, m);
+  out[((size_t)o * 2 + 1) * n + i] = barrett128(lo1, hi1, m);
+}
+
 }  // namespace fhe
 
 using namespace fhe;
@@ -562,6 +591,19 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
   else
     return fail(FHE_ERR_VALUE, "more than 16 digits unsupported");
   FHE_CHECK_LAUNCH("keyswitch_kernel");
+  return FHE_OK;
+}
+
+int fhe_pmac(uint64_t q, int n, const uint64_t* R, const uint64_t* pt_mont, const int32_t* term_off,
+             const int32_t* terms, int n_out, uint64_t* out, void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&q, 1, &ms)) return rc;
+  if (n < 1 || n_out < 0 || !R || !pt_mont || !term_off || !terms || !out) return fail(FHE_ERR_VALUE, "bad pmac arguments");
+  if (!n_out) return FHE_OK;
+  dim3 grid((n + 255) / 256, n_out);
+  pmac_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ms.m[0], n, R, pt_mont, term_off,
+                                                       reinterpret_cast<const int2*>(terms), out);
+  FHE_CHECK_LAUNCH("pmac_kernel");
   return FHE_OK;
 }
 

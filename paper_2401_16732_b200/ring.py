@@ -459,8 +459,9 @@ class WidePoly:
         self._charge(abs(scalar))
         tlo = lo if isinstance(lo, torch.Tensor) else device.to_device(np.asarray(lo, dtype=np.int64))
         thi = hi if isinstance(hi, torch.Tensor) else device.to_device(np.asarray(hi, dtype=np.int64))
-        _native.call("fhe_wide_accumulate_split", self.n, tlo.contiguous().data_ptr(),
-                     thi.contiguous().data_ptr(), ctypes.c_int64(int(scalar)), self.lo.data_ptr(),
+        tlo, thi = tlo.contiguous(), thi.contiguous()  # named: temporaries could be reused before the launch
+        _native.call("fhe_wide_accumulate_split", self.n, tlo.data_ptr(),
+                     thi.data_ptr(), ctypes.c_int64(int(scalar)), self.lo.data_ptr(),
                      self.hi.data_ptr(), device.stream())
 
     def add_rotated(self, other: "WidePoly", shift: int):

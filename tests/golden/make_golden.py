@@ -239,5 +239,20 @@ meta["conv_conventional"] = {"seed": 9, "steps": conv.conventional_steps(specc, 
                              "h:in": h(cts_array(xcb.cts)), "h:out": h(cts_array(yc.cts)),
                              "dec": conv.unpack(yc, skc).tolist(), "ref_seconds": round(time.time() - t0, 2)}
 
+# fragmented conventional conv (needs the harness-side _galois_element shim above), with bias
+r = np.random.default_rng(10)
+skf = bfv.keygen(P, r)
+xf = r.integers(0, 8, (2, 32, 32), dtype=np.int64)
+wf = r.integers(-127, 128, (3, 2, 3, 3), dtype=np.int64)
+bf = np.array([5, 0, -7], dtype=np.int64)
+specf = conv.ConvLayerSpec(32, 32, 3, 2, 3, wf, bias=bf)
+swf = bfv.gen_switching_keys(skf, conv.conventional_steps(specf, P), r, decomp_log=conv.CONV_DECOMP_LOG)
+xfb = conv.pack_input(xf, P, 3, lambda pt: bfv.encrypt_private(pt, skf, r), batch=True)
+t0 = time.time()
+yf = conv.conv_conventional(xfb, specf, swf, P)
+meta["conv_conventional_frag"] = {"seed": 10, "steps": conv.conventional_steps(specf, P),
+                                  "h:in": h(cts_array(xfb.cts)), "h:out": h(cts_array(yf.cts)),
+                                  "dec": conv.unpack(yf, skf).tolist(), "ref_seconds": round(time.time() - t0, 2)}
+
 (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
 print("wrote", OUT / "golden.json")

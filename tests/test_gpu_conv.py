@@ -284,3 +284,24 @@ def test_conv_conventional_matches_reference(golden):
     y = conv.conv_conventional(xb, spec, swk, P)
     assert sha(_out(y.cts)) == g["h:out"]
     assert conv.unpack(y, sk).tolist() == g["dec"]
+
+
+def test_conv_conventional_fragmented_matches_reference(golden):
+    """Fragmented batch layout (32x32 tile > n/2 slots) with bias, vs the
+    reference run with the harness-side _galois_element shim."""
+    from paper_2401_16732_b200 import bfv, conv
+
+    g = golden["conv_conventional_frag"]
+    P = _P()
+    r = np.random.default_rng(g["seed"])
+    sk = bfv.keygen(P, r)
+    xf = r.integers(0, 8, (2, 32, 32), dtype=np.int64)
+    wf = r.integers(-127, 128, (3, 2, 3, 3), dtype=np.int64)
+    spec = conv.ConvLayerSpec(32, 32, 3, 2, 3, wf, bias=np.array([5, 0, -7], dtype=np.int64))
+    assert conv.conventional_steps(spec, P) == g["steps"]
+    swk = bfv.gen_switching_keys(sk, conv.conventional_steps(spec, P), r, decomp_log=conv.CONV_DECOMP_LOG)
+    xb = conv.pack_input(xf, P, 3, lambda pt: bfv.encrypt_private(pt, sk, r), batch=True)
+    assert sha(_out(xb.cts)) == g["h:in"]
+    y = conv.conv_conventional(xb, spec, swk, P)
+    assert sha(_out(y.cts)) == g["h:out"]
+    assert conv.unpack(y, sk).tolist() == g["dec"]

@@ -296,21 +296,26 @@ class ConvTcPlan:
     @staticmethod
     def _fits(pos_tile: int, h: int, taps: int) -> bool:
         win = -(-(pos_tile + 2 * h) * 256 // 1024) * 1024
-        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 204 * 1024  # >= 2 pipeline stages
+        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 212 * 1024  # >= 2 pipeline stages
 
     @staticmethod
-    def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int) -> int:
-        """32 positions per tile, or 16 when that leaves fewer than two tiles
-        per SM (small layers are epilogue-latency bound) and still fits."""
+    def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int, c_i: int = 32) -> int:
+        """Positions per tile (csrc/conv_tc.cu): 32, or 16 when 32 does not
+        fit. FLASHHE_TC_POS = 32 (default) | 16 | 64 | auto. 64 (two
+        accumulators share each weight stage: half the weight bytes per
+        position, but no TMEM double buffering) measured 6 % slower on the
+        config-4 stack; `auto` uses it for long contractions
+        (ceil(c_i/32)·taps >= 72)."""
         import os
 
+        mode = os.environ.get("FLASHHE_TC_POS", "32")
+        if mode != "auto":
+            return int(mode) if int(mode) <= 32 or ConvTcPlan._fits(int(mode), h, taps) else 32
         if not ConvTcPlan._fits(32, h, taps):
             return 16
-        mode = os.environ.get("FLASHHE_TC_POS", "32")
-        if mode == "auto":
-            tiles = (n // 32) * -(-c_o // ConvTcPlan.OC_TILE) * 2 * frags
-            return 16 if tiles < 2 * ConvTcPlan.SMS else 32
-        return int(mode)
+        if -(-c_i // 32) * taps >= 72 and ConvTcPlan._fits(64, h, taps):
+            return 64
+        return 32
 
     @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
@@ -331,7 +336,7 @@ class ConvTcPlan:
         self.c_o, self.c_i, self.taps = weights3d.shape
         self.h = int(np.abs(steps).max(initial=0))
         self.frags = layout.frags
-        self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps)
+        self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps, self.c_i)
         N = self.OC_TILE
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
         j = np.arange(self.c_i)

@@ -73,6 +73,8 @@ struct LayerDesc {
   size_t in_bytes, w_bytes;  // extents of the input and weights (L2 prefetch)
   int Y, JB, F, c_i, fstride, c_o, OB, taps, h, npos, nst, stage_bytes, win_bytes, tiles, units;
   int toff;  // tiles of the previous layers mod gridDim.x: tiles are dealt round-robin over the whole stack
+  int nacc;  // accumulators per tile: 1, or 2 (a 64-position tile: weights reused by both, TMEM single-buffered)
+  int tpos;  // positions per tile = npos * nacc
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
 
@@ -146,6 +148,19 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t b
       : "r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
+// The 9 (or 1, or `taps`) MMAs of one accumulator for one stage. Descriptors
+// advance by adding 16-byte units to the start-address field (addresses stay
+// below 256 KB, so the 14-bit field never carries): weights by 256 units per
+// tap, the window by the tap's DRot offset. The unrolled forms keep the
+// issue loop shorter than the tensor pipe's 129 cycles per MMA.
+template <int TAPS>
+__device__ __forceinline__ void issue_taps(uint32_t acc, uint64_t adesc, uint64_t bdesc, const uint32_t* off16,
+                                           uint32_t idesc, bool first) {
+#pragma unroll
+  for (int tp = 0; tp < TAPS; ++tp)
+    mma_i8(acc, adesc + (uint64_t)(tp * (4096 >> 4)), bdesc + off16[tp], idesc, (first && tp == 0) ? 0u : 1u);
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
@@ -164,9 +179,10 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 // Optional timeline instrumentation (fhe_debug_trace): CTA 0 records
 // clock64() at pipeline events, [kind][index] with 4096 slots per kind.
 __device__ unsigned long long* g_trace = nullptr;
-#define TC_TRACE(kind, idx)                                                                     \
-  do {                                                                                          \
-    if (g_trace && blockIdx.x == 0 && (idx) < 4096) g_trace[(kind) * 4096 + (idx)] = clock64(); \
+// (kernels copy g_trace into a local `trc` once: no global load per event)
+#define TC_TRACE(kind, idx)                                                             \
+  do {                                                                                  \
+    if (trc && blockIdx.x == 0 && (idx) < 4096) trc[(kind) * 4096 + (idx)] = clock64(); \
   } while (0)
 
 struct Tile {
@@ -179,8 +195,8 @@ __device__ __forceinline__ Tile tile_of(int t, const LayerDesc& d, int n) {
   Tile r;
   r.ob = t % d.OB;
   t /= d.OB;
-  const int nsb = n / d.npos;
-  r.s0 = (t % nsb) * d.npos;
+  const int nsb = n / d.tpos;
+  r.s0 = (t % nsb) * d.tpos;
   t /= nsb;
   r.f = t % d.F;
   r.p = t / d.F;
@@ -371,6 +387,7 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid_constant__ StackArgs A) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  unsigned long long* const trc = g_trace;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = A.n, nl = A.nl, G = gridDim.x;
   const uint64_t q = A.q;
@@ -453,21 +470,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
 
   if (warp == 0) {
     // ------------------------------------------------------------ MMA issue
+    // TMEM: two 256-column accumulator buffers. A 32-position tile takes the
+    // next buffer in turn (the epilogue of one overlaps the MMAs of the next);
+    // a 64-position tile takes both (acc a <- positions 32a..32a+31, same
+    // weights: half the weight traffic per position). Per-buffer use counts
+    // give the tmem_full / tmem_empty parities on both sides.
     if (lane == 0) {
-      int s_mma = 0, prev_sb = -1, tl = 0;
-      uint32_t par = 0;  // per-stage phase parity of the full barriers
+      int s_mma = 0, prev_sb = -1, tl = 0, nb = 0;
+      uint32_t par = 0, use = 0;  // per-stage full parity; per-buffer use parity (bit b)
       for (int l = 0; l < nl; ++l) {
         const LayerDesc& d = A.L[l];
         if (d.tiles <= first_tile(d)) continue;  // no tiles of this layer here (the loader skips it too)
         if (d.stage_bytes != prev_sb) s_mma = 0;  // the loader drained and re-partitioned the ring
         prev_sb = d.stage_bytes;
         const uint32_t idesc = idesc_i8(8 * d.npos);
+        uint32_t off16[9];  // this layer's DRot offsets in 16-byte descriptor units (taps <= 9 fast path)
+#pragma unroll
+        for (int tp = 0; tp < 9; ++tp) off16[tp] = tp < d.taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
         for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
-          const int buf = tl & 1;
-          mbar_wait(tempty_bar(buf), ((tl >> 1) & 1) ^ 1);  // epilogue released this buffer
-          asm volatile("tcgen05.fence::after_thread_sync;");
+          int b0 = 0, b1 = 1;
+          if (d.nacc == 1) {
+            b0 = nb;
+            nb ^= 1;
+          }
           TC_TRACE(0, tl);
-          const uint32_t acc = tmem + buf * kAccCols;
           for (int jb = 0; jb < d.JB; ++jb) {
             const int s = s_mma;
             mbar_wait(full_bar(s), (par >> s) & 1);
@@ -475,13 +501,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
             const uint32_t sw = sx + d.win_bytes;
-            for (int tp = 0; tp < d.taps; ++tp)
-              mma_i8(acc, umma_desc(sw + tp * kWTap), umma_desc(sx + (uint32_t)d.tap_off[tp] * 256), idesc,
-                     (jb | tp) != 0);
+            const uint64_t adesc = umma_desc(sw);
+            for (int a = 0; a < d.nacc; ++a) {
+              const int b = a == 0 ? b0 : b1;
+              if (jb == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
+                mbar_wait(tempty_bar(b), ((use >> b) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+              }
+              const uint32_t acc = tmem + b * kAccCols;
+              const uint64_t bdesc = umma_desc(sx + (uint32_t)(a * d.npos) * 256);
+              if (d.taps == 9)
+                issue_taps<9>(acc, adesc, bdesc, off16, idesc, jb == 0);
+              else if (d.taps == 1)
+                issue_taps<1>(acc, adesc, bdesc, off16, idesc, jb == 0);
+              else
+                for (int tp = 0; tp < d.taps; ++tp)
+                  mma_i8(acc, adesc + (uint64_t)(tp * (4096 >> 4)), bdesc + (uint32_t)d.tap_off[tp] * 16, idesc,
+                         (jb | tp) != 0);
+            }
             mma_commit(empty_bar(s));  // stage free once these MMAs retire
             s_mma = s + 1 == d.nst ? 0 : s + 1;
           }
-          mma_commit(tfull_bar(buf));  // accumulator complete
+          for (int a = 0; a < d.nacc; ++a) {
+            const int b = a == 0 ? b0 : b1;
+            mma_commit(tfull_bar(b));  // accumulator complete
+            use ^= 1u << b;
+          }
           TC_TRACE(1, tl);
         }
       }
@@ -506,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         asm volatile("fence.proxy.async.global;");  // generic-proxy X stores -> cp.async.bulk reads
         const uint32_t wstage = (uint32_t)d.taps * kWTap;
         const size_t plane_stride = (size_t)d.Y * 256;
-        const uint32_t win_load = (uint32_t)((d.npos + 2 * d.h) * 256);
+        const uint32_t win_load = (uint32_t)((d.tpos + 2 * d.h) * 256);
         for (int t = first_tile(d); t < d.tiles; t += G) {
           const Tile T = tile_of(t, d, n);
           const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
@@ -550,60 +595,71 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
     const int quad = warp & 3, sub = (warp - 2) >> 2;
     const int k8 = opaque(1 << 8), k16 = opaque(1 << 16), k24 = opaque(1 << 24);
     relayout_layer(0, P0);  // nothing to do yet but help with layer 0
-    int tl = 0;
+    int tl = 0, nb = 0;
+    uint32_t use = 0;  // per-buffer use parity (mirrors the MMA thread)
     for (int l = 0; l < nl; ++l) {
       const LayerDesc& d = A.L[l];
       for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
         const Tile T = tile_of(t, d, n);
-        const int buf = tl & 1;
         const int o = T.ob * kOcTile + quad * 32 + lane;
         const bool active = T.ob * kOcTile + quad * 32 < d.c_o;  // warp-uniform
-        mbar_wait_sleep(tfull_bar(buf), (tl >> 1) & 1, 64);
-        if (lane == 0 && warp == 2) TC_TRACE(5, tl);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (active) {
-          // lane = output channel within the quadrant; a 32-column TMEM chunk
-          // holds 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and
-          // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,
-          // q > 2^56); V = lo + 2^32 hi.
-          const uint64_t bd = (T.p == 0 && d.bias && o < d.c_o) ? d.bias[o] : 0;
-          const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
-          uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + T.s0;
+        const uint64_t bd = (active && T.p == 0 && d.bias && o < d.c_o) ? d.bias[o] : 0;
+        for (int a = 0; a < d.nacc; ++a) {
+          int buf;
+          if (d.nacc == 1) {
+            buf = nb;
+            nb ^= 1;
+          } else {
+            buf = a;
+          }
+          const int s0 = T.s0 + a * d.npos;
+          mbar_wait_sleep(tfull_bar(buf), (use >> buf) & 1, 64);
+          use ^= 1u << buf;
+          if (lane == 0 && warp == 2) TC_TRACE(5, tl);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (active) {
+            // lane = output channel within the quadrant; a 32-column TMEM chunk
+            // holds 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and
+            // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,
+            // q > 2^56); V = lo + 2^32 hi.
+            const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
+            uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + s0;
 #pragma unroll 1
-          for (int k = sub; k < d.npos / 4; k += kEpiWarps / 4) {
-            uint32_t v[32];
-            TMEM_LD32(acc + k * 32, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-            uint64_t r[4];
+            for (int k = sub; k < d.npos / 4; k += kEpiWarps / 4) {
+              uint32_t v[32];
+              TMEM_LD32(acc + k * 32, v);
+              asm volatile("tcgen05.wait::ld.sync.aligned;");
+              uint64_t r[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int32_t* P = reinterpret_cast<const int32_t*>(v + 8 * j);
-              const long long lo =
-                  mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, (long long)q + P[0])));
-              const long long hi =
-                  mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, (long long)q + P[4])));
-              // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
-              const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(A.w32p, (uint64_t)hi) * q;
-              uint64_t val = (uint64_t)lo + uh;  // < 4q
-              val = val >= 2 * q ? val - 2 * q : val;
-              r[j] = val >= q ? val - q : val;
-            }
-            if (bd) {
-              const uint32_t mk = *reinterpret_cast<const uint32_t*>(d.bmask + (size_t)T.f * n + T.s0 + 4 * k);
+              for (int j = 0; j < 4; ++j) {
+                const int32_t* P = reinterpret_cast<const int32_t*>(v + 8 * j);
+                const long long lo =
+                    mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, (long long)q + P[0])));
+                const long long hi =
+                    mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, (long long)q + P[4])));
+                // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
+                const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(A.w32p, (uint64_t)hi) * q;
+                uint64_t val = (uint64_t)lo + uh;  // < 4q
+                val = val >= 2 * q ? val - 2 * q : val;
+                r[j] = val >= q ? val - q : val;
+              }
+              if (bd) {
+                const uint32_t mk = *reinterpret_cast<const uint32_t*>(d.bmask + (size_t)T.f * n + s0 + 4 * k);
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
-            }
-            if (o < d.c_o) {
-              ulonglong2* dst = reinterpret_cast<ulonglong2*>(orow + 4 * k);
-              dst[0] = make_ulonglong2(r[0], r[1]);
-              dst[1] = make_ulonglong2(r[2], r[3]);
+                for (int j = 0; j < 4; ++j)
+                  if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
+              }
+              if (o < d.c_o) {
+                ulonglong2* dst = reinterpret_cast<ulonglong2*>(orow + 4 * k);
+                dst[0] = make_ulonglong2(r[0], r[1]);
+                dst[1] = make_ulonglong2(r[2], r[3]);
+              }
             }
           }
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(tempty_bar(buf));
+          if (lane == 0 && warp == 2) TC_TRACE(6, tl);
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        mbar_arrive(tempty_bar(buf));
-        if (lane == 0 && warp == 2) TC_TRACE(6, tl);
       }
       // this CTA consumed all of layer l's X (every tile's MMAs completed)
       asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue));
@@ -714,7 +770,8 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     if (!s.in || !s.chan || !s.w || !s.out || !s.tap_steps) return fail(FHE_ERR_VALUE, "tc layer %d: null operand", l);
     if (s.n_in < 1) return fail(FHE_ERR_VALUE, "tc layer %d: n_in must be >= 1", l);
     if (s.bias_delta && !s.bias_mask) return fail(FHE_ERR_VALUE, "tc layer %d: bias needs a mask", l);
-    if (s.pos_tile != 16 && s.pos_tile != 32) return fail(FHE_ERR_VALUE, "tc layer %d: pos_tile must be 16 or 32", l);
+    if (s.pos_tile != 16 && s.pos_tile != 32 && s.pos_tile != 64)
+      return fail(FHE_ERR_VALUE, "tc layer %d: pos_tile must be 16, 32 or 64", l);
     if (127ll * 255 * ((s.c_i + 31) / 32 * 32) * s.taps >= (1ll << 31))
       return fail(FHE_ERR_VALUE, "tc layer %d: plane sums would exceed s32", l);
     d.in = s.in;
@@ -733,7 +790,9 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.OB = (s.c_o + tc::kOcTile - 1) / tc::kOcTile;
     d.taps = s.taps;
     d.h = s.h;
-    d.npos = s.pos_tile;
+    d.npos = std::min(s.pos_tile, 32);  // positions per MMA (N = 8 npos <= 256)
+    d.nacc = s.pos_tile / d.npos;       // 64-position tiles use both TMEM buffers
+    d.tpos = s.pos_tile;
     d.in_bytes = (size_t)s.n_in * 2 * n * 8;
     d.w_bytes = (size_t)d.OB * d.JB * d.taps * tc::kWTap;
     for (int t = 0; t < s.taps; ++t) {
@@ -741,11 +800,11 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
       if (off < 0 || off > 2 * s.h) return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
       d.tap_off[t] = (int16_t)off;
     }
-    d.win_bytes = ((d.npos + 2 * d.h) * 256 + 1023) / 1024 * 1024;
+    d.win_bytes = ((d.tpos + 2 * d.h) * 256 + 1023) / 1024 * 1024;
     d.stage_bytes = d.win_bytes + d.taps * tc::kWTap;
     d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
     if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
-    d.tiles = (n / d.npos) * d.OB * 2 * d.F;
+    d.tiles = (n / d.tpos) * d.OB * 2 * d.F;
     if (nl > 1 && (size_t)2 * d.F * d.JB * d.Y * 256 > x_stride)
       return fail(FHE_ERR_VALUE, "tc layer %d: X stride smaller than its operand", l);
     const long long units = 2ll * ((d.Y + 31) / 32) * d.JB * 2 * d.F;

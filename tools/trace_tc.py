@@ -38,6 +38,18 @@ def main():
     t = buf.cpu().numpy().reshape(8, 4096)
     t0 = t[t > 0].min()
     print("layer", l.name, "path", plan.path)
+    st = t[4][t[4] > 0] - t0
+    li = t[2][64:64 + 4000]
+    li = li[li > 0] - t0
+    if len(st) > 8:
+        full, issued = st[0::2], st[1::2]
+        m = min(len(full), len(issued), len(li))
+        print("stage: load_issue, full_ok, mma_issued (first 6):")
+        for k in range(min(6, m)):
+            print(f"   {k:3d} {li[k]:8d} {full[k]:8d} {issued[k]:8d}  load->full {full[k] - li[k]:6d}  issue {issued[k] - full[k]:5d}")
+        gap = full[1:m] - issued[:m - 1]
+        print("median: load->full", int(np.median(full[:m] - li[:m])), "issue", int(np.median(issued[:m] - full[:m])),
+              "wait-for-data", int(np.median(gap)))
     for k, name in enumerate(KINDS):
         v = t[k][t[k] > 0] - t0
         print(f"{name:16s} n={len(v):4d} first={v[:12].tolist()}")

@@ -314,7 +314,51 @@ def sub_benchmarks(steps, warmup, hbm):
                              "rotations": len(rsteps) * B, "rot_per_s": round(len(rsteps) * B / avg, 1),
                              "N": N, "L": L, "B": B, "T": T}
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
+    res["act2pc_layer"] = act2pc_layer(steps, warmup)
     return res
+
+
+def act2pc_layer(steps, warmup):
+    """§8f rank 1: one layer's x²+x round trip on the
+    device — config 4's stem output (64 channels at 64x64, 3 fragments per
+    channel: 192 ciphertexts) masked, decrypted, repacked into the next
+    conv's layout, squared, re-encrypted, multiplied and finalized; both
+    parties in-process, all rounds batched over the layer."""
+    from dataclasses import replace
+
+    import torch
+
+    from paper_2401_16732_b200 import act2pc, bfv, conv, params
+
+    P = params.default_params()
+    rng = np.random.default_rng(12)
+    sk = bfv.keygen(P, rng)
+    c, H = 64, 64
+    src = replace(conv.layout_direct(P, H, H, 3), c_n=1)
+    plan = act2pc.RepackPlan(src, c, conv.layout_direct(P, H, H, 3), P)
+    # valid ciphertexts standing in for the conv output (fresh encryptions of 0)
+    y = bfv.cts_from_rows(bfv.precompute_zero_rows(sk, rng, plan.k_src).rows, P.q, bfv.Encoding.DIRECT,
+                          bfv.Domain.COEFF)
+    zeros = bfv.precompute_zero_rows(sk, rng, 3 * plan.k_dst)
+    sessions = [act2pc.offline_prepare_layer(plan, P, rng) for _ in range(warmup + steps)]
+    it = iter(sessions)
+
+    def one():
+        zeros._next = 0  # bench only: the pool is rewound (same work, no re-sampling between steps)
+        return act2pc.run_layer_activation(y, next(it), sk, zeros, P)
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) / steps * 1e3
+    acts = c * H * H
+    return {"workload": "config4 stem activations: 64 ch x 64x64, 192 cts in / 192 out (repacked)",
+            "ms": round(ms, 3), "activations_per_s": round(acts / ms * 1e3, 1), "cts": plan.k_src,
+            "timing": "wall clock per layer round trip incl. host issue and the client's noise-budget checks"}
 
 
 def conventional_vs_proposed(steps, warmup):

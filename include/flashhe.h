@@ -255,6 +255,33 @@ int fhe_act_server_const(uint64_t p, int f, int64_t count, const uint64_t* r,
                          const uint64_t* r_sq, const uint64_t* v, uint64_t* c,
                          void* stream);
 
+/* ---- K5 over a whole layer (row stacks [R][2][n], all pointers DEVICE) ---- */
+/* Client repack (conv.py:148-197: channel_positions of the conv output, stride
+ * applied, composed with pack_vectors of the next layer's layout) and the
+ * batch-slot placement of bfv.encode_batch (bfv.py:124-133) as one gather:
+ *   out[i] = idx[i] >= 0 ? src[idx[i]] : 0,   i < count. */
+int fhe_act_gather(int64_t count, const int32_t* idx, const uint64_t* src, uint64_t* out,
+                   void* stream);
+/* bfv.encrypt_online (bfv.py:248-263) over rows, optionally fused with the
+ * client square:
+ *   v = m[r][perm ? perm[s] : s] mod p;  if (square) v = v^2 + v*2^f mod p
+ *   out[r][0][s] = zero[r][0][s] + Δ v mod q;   out[r][1][s] = zero[r][1][s]
+ * zero: precomputed encryptions of 0 (single use); perm: int32 [n] or NULL
+ * (bfv.decode_batch's slot gather, bfv.py:135-139). Also serves server_round1
+ * (plain_add of the masks, zero = the conv output). out must not alias zero. */
+int fhe_act_encrypt_rows(uint64_t q, uint64_t p, uint64_t delta, int f, int square, int R, int n,
+                         const uint64_t* zero, const uint64_t* m, const int32_t* perm,
+                         uint64_t* out, void* stream);
+/* bfv.pmult then bfv.plain_add in the EVAL domain (bfv.py:330-372), one pass:
+ *   out[r][0] = ct[r][0] ⊙ pt[r] + add[r],  out[r][1] = ct[r][1] ⊙ pt[r]   mod q
+ * pt, add: [R][n] EVAL (prepared plaintext / NTT'd Δ·v); add may be NULL. */
+int fhe_ct_pmult_add(uint64_t q, int R, int n, const uint64_t* ct, const uint64_t* pt,
+                     const uint64_t* add, uint64_t* out, void* stream);
+/* act2pc server_finalize: psub(a, b) then plain_add of the
+ * constant c = r^2 - r*2^f + v (fhe_act_server_const), [R][n] mod p. */
+int fhe_act_finalize(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* a,
+                     const uint64_t* b, const uint64_t* c, uint64_t* out, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -76,6 +76,10 @@ SIGNATURES = {
     "fhe_pmac": (_int, [_u64, _int, _vp, _vp, _vp, _vp, _int, _vp, _vp]),
     "fhe_act_client_square": (_int, [_u64, _int, _i64, _vp, _vp, _vp]),
     "fhe_act_server_const": (_int, [_u64, _int, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "fhe_act_gather": (_int, [_i64, _vp, _vp, _vp, _vp]),
+    "fhe_act_encrypt_rows": (_int, [_u64, _u64, _u64, _int, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fhe_ct_pmult_add": (_int, [_u64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
+    "fhe_act_finalize": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

@@ -21,8 +21,9 @@ from enum import Enum
 import numpy as np
 import torch
 
-from . import _native, bfv, device
+from . import _native, bfv, device, ring
 from .bfv import Ciphertext, Encoding
+from .ring import Domain
 from .errors import EncodingError, ProtocolError
 from .params import RingParams
 
@@ -157,3 +158,219 @@ def run_activation(conv_out: Ciphertext, session: ActivationSession, sk: bfv.Sec
     m2 = server_round2((sq, w), session, params)
     back = client_round2(m2, sk, zero_pool)
     return server_finalize(sq, back, session, params)
+
+
+# ---------------------------------------------------------------------------
+# One layer of activations at once: the same protocol over row stacks
+# [k, 2, n], with the client's repack into the next conv's tile layout
+# (conv.py:148-197) folded into its decrypt -> square -> encrypt step.
+#
+# Both parties derive the public slot map of a RepackPlan from the model
+# geometry. The server draws r over the conv output's slots and v over the
+# next layout's slots; r' = r gathered through the map is what the client's
+# repacked w' = a' + r' carries, so every later step works slot-for-slot in
+# the next layout and the finalize yields ⟦a'² + a'·2^f⟧ already packed for
+# the next convolution (zero borders / halos included: a' = r' = 0 there).
+
+
+def repack_index(src, channels: int, dst, n: int) -> np.ndarray:
+    """[k_dst, n] flat source slot (ct·n + slot) of every next-layout slot, −1
+    where the next layout holds a zero: channel_positions of the conv output
+    (stride applied, conv.py:162-177) composed with pack_vectors (conv.py:180-197)."""
+    from . import conv
+
+    h, w = src.out_dims()
+    flat = np.empty((channels, h * w), dtype=np.int64)
+    for j in range(channels):
+        ci, si = conv.channel_positions(src, j)
+        flat[j] = ci * n + si + 1
+    return np.stack(conv.pack_vectors(flat.reshape(channels, h, w), dst, 1 << 62)) - 1
+
+
+class RepackPlan:
+    """Slot map conv output (stride pending) -> next conv input layout."""
+
+    def __init__(self, src, channels: int, dst, params: RingParams):
+        h, w = src.out_dims()
+        if (dst.height, dst.width) != (h, w) or dst.stride != 1:
+            raise EncodingError("next layout does not match the activation geometry")
+        if dst.ring != params.n or src.ring != params.n:
+            raise EncodingError("activations repack between direct layouts")
+        n = params.n
+        self.src, self.dst, self.channels, self.n = src, dst, channels, n
+        self.k_src, self.k_dst = src.ct_count(channels), dst.ct_count(channels)
+        if self.k_src * n >= 1 << 31:
+            raise ValueError("layer too large for 32-bit slot indices")
+        idx = repack_index(src, channels, dst, n)
+        slot = bfv._slot_index(params)  # batch slot s -> evaluation position
+        inv = np.empty(n, dtype=np.int64)
+        inv[slot] = np.arange(n)
+        self.idx_host = idx
+        self.idx = device.to_device_i32(idx)
+        self.idx_eval = device.to_device_i32(idx[:, inv])
+        self.slot = device.to_device_i32(slot)
+
+    def gather_host(self, values: np.ndarray) -> np.ndarray:
+        """Host restatement of the map (offline mask preparation, tests)."""
+        flat = np.asarray(values, dtype=np.int64).reshape(-1)
+        return np.where(self.idx_host >= 0, flat[np.maximum(self.idx_host, 0)], 0)
+
+
+def _gather(idx: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    src_c = src.contiguous()
+    out = torch.empty(idx.shape, dtype=torch.int64, device=idx.device)
+    _native.call("fhe_act_gather", idx.numel(), idx.data_ptr(), src_c.data_ptr(), out.data_ptr(), device.stream())
+    return out
+
+
+def _encrypt_rows(zero: torch.Tensor, m: torch.Tensor, params: RingParams, square: bool = False, f: int = 0,
+                  perm: torch.Tensor | None = None) -> torch.Tensor:
+    k = zero.shape[0]
+    z, mm = zero.contiguous(), m.contiguous()
+    out = torch.empty((k, 2, params.n), dtype=torch.int64, device=z.device)
+    _native.call("fhe_act_encrypt_rows", params.q, params.p, params.delta, f, int(square), k, params.n,
+                 z.data_ptr(), mm.data_ptr(), device.ptr(perm), out.data_ptr(), device.stream())
+    return out
+
+
+def _batch_coeffs(evals_p: torch.Tensor, params: RingParams) -> torch.Tensor:
+    """bfv.encode_batch after slot placement: iNTT mod p of eval-order rows."""
+    return ring.ntt_rows(evals_p, params.n, [params.p], inverse=True)
+
+
+@dataclass
+class LayerSession:
+    """Server-private masks of one layer's protocol run (single use)."""
+
+    plan: RepackPlan
+    r: torch.Tensor  # [k_src, n] mod p, over the conv output's slots
+    two_r_eval: torch.Tensor  # [k_dst, n] prepare_plaintext(encode_batch(2 r'))
+    v_eval: torch.Tensor  # [k_dst, n] NTT(Δ · encode_batch(v)): plain_add in EVAL
+    const: torch.Tensor  # [k_dst, n] r'² − r'·2^f + v mod p
+    r_dst: np.ndarray = field(default=None, repr=False)  # host r' (server-private)
+    v: np.ndarray = field(default=None, repr=False)  # host v (server-private)
+    layer_id: int = 0
+    round: Round = Round.INIT
+    codec: FixedPointCodec | None = None
+    ct1: torch.Tensor | None = field(default=None, repr=False)
+
+
+def offline_prepare_layer(plan: RepackPlan, params: RingParams, rng, frac_bits: int = 0,
+                          layer_id: int = 0) -> LayerSession:
+    """Masks for one layer: r uniform over every conv
+    output slot, v over every slot of the next layout; the batch plaintexts
+    2r' and v are encoded, lifted and NTT'd here, offline."""
+    n, p, q = params.n, params.p, params.q
+    r = rng.integers(0, p, (plan.k_src, n), dtype=np.int64)
+    v = rng.integers(0, p, (plan.k_dst, n), dtype=np.int64)
+    r_dst = plan.gather_host(r)
+    inv_perm = np.empty(n, dtype=np.int64)
+    inv_perm[bfv._slot_index(params)] = np.arange(n)
+    two_r = _batch_coeffs(device.to_device(np.ascontiguousarray((2 * r_dst % p)[:, inv_perm])), params)
+    lifted = torch.empty_like(two_r)
+    _native.call("fhe_poly_lift_centered", p, q, plan.k_dst, n, two_r.data_ptr(), lifted.data_ptr(), device.stream())
+    two_r_eval = ring.ntt_rows(lifted, n, [q])
+    v_coeffs = _batch_coeffs(device.to_device(np.ascontiguousarray(v[:, inv_perm])), params)
+    v_delta = bfv._add_delta(None, v_coeffs, params, plan.k_dst)
+    v_eval = ring.ntt_rows(v_delta, n, [q])
+    rd, vd = device.to_device(r_dst), device.to_device(v)
+    rsq = device.to_device(r_dst * r_dst % p)
+    const = torch.empty_like(rd)
+    _native.call("fhe_act_server_const", p, frac_bits, rd.numel(), rd.data_ptr(), rsq.data_ptr(), vd.data_ptr(),
+                 const.data_ptr(), device.stream())
+    return LayerSession(plan, device.to_device(r), two_r_eval, v_eval, const, r_dst, v, layer_id, Round.INIT,
+                        FixedPointCodec(frac_bits, p))
+
+
+def _stack_rows(x) -> torch.Tensor:
+    return bfv.cts_rows(x.cts if hasattr(x, "cts") else x)
+
+
+def server_round1_layer(conv_out, session: LayerSession, params: RingParams) -> torch.Tensor:
+    """⟦a + r⟧ for every ciphertext of the layer (plain_add of the masks)."""
+    _expect(session, Round.INIT)
+    cts = conv_out.cts if hasattr(conv_out, "cts") else conv_out
+    if len(cts) != session.plan.k_src:
+        raise EncodingError("conv output does not match the session's layout")
+    if cts[0].encoding != Encoding.DIRECT:
+        raise EncodingError("activation input must be direct-encoded")
+    msg = _encrypt_rows(bfv.cts_rows(cts), session.r, params)
+    session.round = Round.MASKED
+    return msg
+
+
+def _decrypt_rows_checked(rows: torch.Tensor, domain, sk: bfv.SecretKey) -> torch.Tensor:
+    params = sk.params
+    cts = bfv.cts_from_rows(rows, params.q, Encoding.DIRECT, domain)
+    m, maxw = bfv.decrypt_rows(cts, sk)
+    if len(maxw) and bfv._budget(params, int(maxw.max())) <= 0:
+        raise ProtocolError("noise budget exhausted: ciphertext no longer decrypts reliably")
+    return m
+
+
+def client_round1_layer(msg: torch.Tensor, plan: RepackPlan, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
+                        codec: FixedPointCodec | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Decrypt w = a + r, repack into the next layout (w'), return
+    (⟦w'² + w'·2^f⟧ direct, ⟦w'⟧ batch) — one pass per step for the layer."""
+    params = sk.params
+    f = codec.frac_bits if codec else 0
+    w = _decrypt_rows_checked(msg, Domain.COEFF, sk)
+    z = zeros.take_rows(2 * plan.k_dst)
+    ct_sq = _encrypt_rows(z[: plan.k_dst], _gather(plan.idx, w), params, square=True, f=f)
+    coeffs = _batch_coeffs(_gather(plan.idx_eval, w), params)
+    ct_w = _encrypt_rows(z[plan.k_dst :], coeffs, params)
+    return ct_sq, ct_w
+
+
+def server_round2_layer(msgs: tuple[torch.Tensor, torch.Tensor], session: LayerSession,
+                        params: RingParams) -> torch.Tensor:
+    """⟦2r'·w' + v⟧ = pmult(to_eval(⟦w'⟧), 2r') + v (batch, EVAL), one pass."""
+    _expect(session, Round.MASKED)
+    ct_sq, ct_w = msgs
+    k = session.plan.k_dst
+    if ct_w.shape[0] != k or ct_sq.shape[0] != k:
+        raise EncodingError("round-1 messages do not match the session's layout")
+    w_eval = ring.ntt_rows(ct_w.reshape(-1, params.n), params.n, [params.q])
+    out = torch.empty_like(ct_w)
+    _native.call("fhe_ct_pmult_add", params.q, k, params.n, w_eval.data_ptr(), session.two_r_eval.data_ptr(),
+                 session.v_eval.data_ptr(), out.data_ptr(), device.stream())
+    session.ct1 = ct_sq
+    session.round = Round.CROSS_SENT
+    return out
+
+
+def client_round2_layer(msg: torch.Tensor, plan: RepackPlan, sk: bfv.SecretKey,
+                        zeros: bfv.ZeroRowPool) -> torch.Tensor:
+    """Decrypt the batch messages, re-encrypt their slots direct (decode_batch
+    as NTT mod p + slot gather fused into the encryption pass)."""
+    params = sk.params
+    m = _decrypt_rows_checked(msg, Domain.EVAL, sk)
+    evals = ring.ntt_rows(m, params.n, [params.p])
+    return _encrypt_rows(zeros.take_rows(plan.k_dst), evals, params, perm=plan.slot)
+
+
+def server_finalize_layer(ct1: torch.Tensor, ct2: torch.Tensor, session: LayerSession, params: RingParams,
+                          scale: int = 0):
+    """⟦a'² + a'·2^f⟧ = ct1 − ct2 + (r'² − r'·2^f + v), packed for the next conv."""
+    from . import conv
+
+    _expect(session, Round.CROSS_SENT)
+    plan = session.plan
+    out = torch.empty_like(ct1)
+    _native.call("fhe_act_finalize", params.q, params.p, params.delta, plan.k_dst, params.n, ct1.data_ptr(),
+                 ct2.contiguous().data_ptr(), session.const.data_ptr(), out.data_ptr(), device.stream())
+    session.round = Round.DONE
+    session.ct1 = None
+    cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+    return conv.PackedTensor(cts, plan.dst, plan.channels, scale)
+
+
+def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
+                         params: RingParams):
+    """Both parties in-process: one layer's full two-round exchange."""
+    plan = session.plan
+    m1 = server_round1_layer(conv_out, session, params)
+    sq, w = client_round1_layer(m1, plan, sk, zeros, session.codec)
+    m2 = server_round2_layer((sq, w), session, params)
+    back = client_round2_layer(m2, plan, sk, zeros)
+    return server_finalize_layer(sq, back, session, params, getattr(conv_out, "scale", 0))

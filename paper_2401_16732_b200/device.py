@@ -66,6 +66,14 @@ def to_device(arr: np.ndarray) -> torch.Tensor:
     return t.to(require_cuda())
 
 
+def to_device_i32(arr: np.ndarray) -> torch.Tensor:
+    """Host index array -> device int32 tensor (kernel index maps)."""
+    a = np.asarray(arr)
+    if a.size and (a.min() < -(1 << 31) or a.max() >= 1 << 31):
+        raise ValueError("index does not fit int32")
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(require_cuda())
+
+
 _scratch: dict[tuple[int, str], torch.Tensor] = {}
 
 

@@ -134,6 +134,29 @@ def test_pack_unpack_positions_roundtrip():
             assert np.array_equal(np.array([bvecs[a][b] for a, b in zip(ci, si)]), (x[j] % P.p).ravel())
 
 
+def test_repack_index_matches_unpack_then_pack():
+    """The client's one-gather repack (act2pc.repack_index) equals reading
+    every channel at its readable slots and packing into the next layout —
+    strided, fragmented and multi-tile layouts (conv.py:162-197)."""
+    from dataclasses import replace
+
+    from paper_2401_16732_b200 import act2pc, conv, params
+
+    P = params.default_params()
+    rng = np.random.default_rng(2)
+    cases = [(3, 32, 3, 1, 3), (8, 16, 3, 2, 1), (2, 64, 3, 1, 3), (2, 64, 3, 2, 3), (20, 8, 3, 1, 3), (1, 224, 7, 2, 3)]
+    for c, h, f_src, stride, f_dst in cases:
+        src = replace(replace(conv.layout_direct(P, h, h, f_src), c_n=1), stride=stride)
+        dst = conv.layout_direct(P, h // stride, h // stride, f_dst)
+        slots = rng.integers(0, P.p, (src.ct_count(c), P.n))
+        idx = act2pc.repack_index(src, c, dst, P.n)
+        assert idx.shape == (dst.ct_count(c), P.n) and idx.max() < slots.size
+        got = np.where(idx >= 0, slots.reshape(-1)[np.maximum(idx, 0)], 0)
+        vals = np.stack([slots[conv.channel_positions(src, j)] for j in range(c)])
+        want = np.stack(conv.pack_vectors(vals.reshape(c, h // stride, h // stride), dst, P.p))
+        assert np.array_equal(got, want)
+
+
 def test_conventional_steps_and_storage():
     from paper_2401_16732_b200 import conv, params
 

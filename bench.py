@@ -315,6 +315,48 @@ def sub_benchmarks(steps, warmup, hbm):
                              "N": N, "L": L, "B": B, "T": T}
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
+    res["pool_fc_tail"] = pool_fc_tail(steps, warmup)
+    return res
+
+
+def pool_fc_tail(steps, warmup):
+    """§8f rank 3: config 4's tail — avg_pool k=8 over 512 ciphertexts (8x8
+    maps, integer-pipe K1, 64 taps) then FC 512->200 (K1-TC: one tap, each
+    input's DRot slot as its channel offset) — against the same FC on the
+    integer pipes. Device events per call, inputs resident."""
+    import os
+
+    import torch
+
+    from paper_2401_16732_b200 import bfv, conv, params
+
+    P = params.default_params()
+    rng = np.random.default_rng(13)
+    c, v_out = 512, 200
+    lay = conv.replace(conv.layout_direct(P, 8, 8, 3), c_n=1)
+    x = conv.PackedTensor(bfv.cts_from_rows(torch.from_numpy(rng.integers(0, P.q, (c, 2, P.n), dtype=np.int64)).cuda(),
+                                            P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), lay, c)
+    w = rng.integers(-127, 128, (v_out, c), dtype=np.int64)
+    pooled = conv.avg_pool(x, 8, P)
+
+    def ms_of(fn):
+        return float(np.median(time_steps(fn, steps, warmup)))
+
+    res = {"workload": "config4 tail: avg_pool 8 on 512 cts (8x8) + FC 512->200"}
+    res["pool_ms"] = round(ms_of(lambda: conv.avg_pool(x, 8, P)), 4)
+    res["fc_tc_ms"] = round(ms_of(lambda: conv.fully_connected(pooled, w, P)), 4)
+    old = os.environ.get("FLASHHE_CONV_PATH")
+    os.environ["FLASHHE_CONV_PATH"] = "int"
+    try:
+        res["fc_int_ms"] = round(ms_of(lambda: conv.fully_connected(pooled, w, P)), 4)
+    finally:
+        if old is None:
+            os.environ.pop("FLASHHE_CONV_PATH")
+        else:
+            os.environ["FLASHHE_CONV_PATH"] = old
+    mac = v_out * c * 2 * P.n
+    res["fc_tc_tmac60_per_s"] = round(mac / res["fc_tc_ms"] / 1e9, 2)
+    res["fc_speedup_tc_vs_int"] = round(res["fc_int_ms"] / res["fc_tc_ms"], 1)
     return res
 
 

@@ -215,6 +215,12 @@ typedef struct fhe_conv_tc_layer {
  *   launches that may run concurrently. */
 int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl,
                       uint8_t* X, size_t x_stride, uint64_t* sync, void* stream);
+/* conv.avg_pool (conv.py:604-623): every row (polynomial) of in [rows][n]
+ * replaced by the sum of its k x k DRot taps (steps dy*w_p + dx, weight 1),
+ * computed separably (k row taps, then k column taps of the row sums; exact
+ * mod q, so identical to the k^2-tap contraction). (k-1)(w_p+1) < n, n <= 8192. */
+int fhe_avg_pool(uint64_t q, int n, int rows, int k, int w_p, const uint64_t* in, uint64_t* out,
+                 void* stream);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

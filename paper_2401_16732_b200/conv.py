@@ -330,17 +330,21 @@ class ConvTcPlan:
             return False
         return ConvTcPlan._fits(16, h, taps)
 
-    def __init__(self, q: int, n: int, weights3d: np.ndarray, steps: np.ndarray, layout: TileLayout,
-                 bias, mask):
+    def __init__(self, q: int, n: int, weights3d: np.ndarray, steps: np.ndarray, layout: TileLayout | None,
+                 bias, mask, chan: np.ndarray | None = None):
+        """`chan` ([c_i, 2]: source ciphertext, slot offset) replaces the
+        layout's channel placement — fully_connected's per-input DRot slots."""
         self.q, self.n = int(q), int(n)
         self.c_o, self.c_i, self.taps = weights3d.shape
         self.h = int(np.abs(steps).max(initial=0))
-        self.frags = layout.frags
+        self.frags = 1 if chan is not None else layout.frags
         self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps, self.c_i)
         N = self.OC_TILE
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
         j = np.arange(self.c_i)
-        if layout.fragmented:
+        if chan is not None:
+            chan, self.fstride = np.asarray(chan, dtype=np.int64).reshape(self.c_i, 2), 0
+        elif layout.fragmented:
             chan, self.fstride = np.stack([j * layout.frags, np.zeros_like(j)], 1), 1
         else:
             chan, self.fstride = np.stack([j // layout.c_n, layout.tile * (j % layout.c_n)], 1), 0
@@ -565,9 +569,13 @@ def _bias_plaintext(layout: TileLayout, frag: int, value: int, params: RingParam
 # pooling and fully connected (conv.py:604-668) on K1
 
 
+_fc_plans: dict[tuple, tuple] = {}
+
+
 def avg_pool(x: PackedTensor, k: int, params: RingParams) -> PackedTensor:
     """k×k sliding sums via DRot taps of weight 1; /k² and the subsample are
-    deferred (stride marker), as conv.py:604-623."""
+    deferred (stride marker), as conv.py:604-623. One separable pass
+    (fhe_avg_pool: 2k adds per slot, exact mod q, identical ciphertexts)."""
     layout = x.layout
     if layout.height % k or layout.width % k:
         raise ParameterError(f"pool size {k} does not divide {layout.height}×{layout.width}")
@@ -575,11 +583,10 @@ def avg_pool(x: PackedTensor, k: int, params: RingParams) -> PackedTensor:
         raise ParameterError("pooling input must not carry a pending stride")
     if layout.fragmented and (k - 1) * (layout.w_p + 1) > layout.halo:
         raise ParameterError("pool window exceeds the fragment halo")
-    off = np.arange(k)
-    steps = (off[:, None] * layout.w_p + off[None, :]).reshape(-1)
-    plan = ConvPlan(params.q, params.n, np.ones((1, k * k), dtype=np.int64), np.zeros(k * k), steps,
-                    frags=len(x.cts), fstride=1)
-    out = plan.run(bfv.cts_rows(x.cts))
+    inp = bfv.cts_rows(x.cts).contiguous()
+    out = torch.empty_like(inp)
+    _native.call("fhe_avg_pool", params.q, params.n, 2 * len(x.cts), k, layout.w_p, inp.data_ptr(), out.data_ptr(),
+                 device.stream())
     cts = bfv.cts_from_rows(out, params.q, x.cts[0].encoding, Domain.COEFF)
     return PackedTensor(cts, replace(layout, stride=k), x.channels, x.scale)
 
@@ -588,6 +595,33 @@ def fully_connected(x: PackedTensor, weights: np.ndarray, params: RingParams, bi
                     weight_scale: int = 0) -> list[Ciphertext]:
     """Matrix-vector product: output row o = Σ_v W[o,v]·DRot(ct(v), slot(v)),
     the dot product landing in slot 0 (conv.py:626-668)."""
+    plan = _fc_plan(x, weights, params, bias)
+    out = plan.run(bfv.cts_rows(x.cts))
+    return bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+
+
+def _fc_plan(x: PackedTensor, weights, params: RingParams, bias) -> ConvPlan:
+    """K1 operands of fully_connected, cached per weight array object (as
+    conv_plan caches per layer: weights are treated as immutable after first
+    use) and input geometry."""
+    import weakref
+
+    key = (id(weights), x.layout, x.channels, params.fingerprint(),
+           None if bias is None else np.asarray(bias, dtype=np.int64).tobytes())
+    hit = _fc_plans.get(key)
+    if hit is not None and hit[0]() is weights:
+        return hit[1]
+    plan = _build_fc_plan(x, weights, params, bias)
+    try:
+        ref = weakref.ref(weights)
+    except TypeError:  # lists and other non-weakref-able containers: no caching
+        return plan
+    _fc_plans[key] = (ref, plan)
+    weakref.finalize(weights, _fc_plans.pop, key, None)
+    return plan
+
+
+def _build_fc_plan(x: PackedTensor, weights, params: RingParams, bias) -> ConvPlan:
     weights = np.asarray(weights, dtype=np.int64)
     c_out, v_in = weights.shape
     if weights.size and int(np.abs(weights).max()) >= 1 << MAX_WEIGHT_BITS:
@@ -604,8 +638,12 @@ def fully_connected(x: PackedTensor, weights: np.ndarray, params: RingParams, bi
         bias_mask = np.zeros((1, params.n), dtype=np.uint8)
         bias_mask[0, 0] = 1
     plan = ConvPlan(params.q, params.n, weights, ct_idx, slots, bias_delta=bias_delta, bias_mask=bias_mask)
-    out = plan.run(bfv.cts_rows(x.cts))
-    return bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+    w3 = weights.reshape(c_out, v_in, 1)
+    if ConvTcPlan.eligible(w3, params.q, params.n, 0, 1):
+        # one tap, the DRot slot of each input as its channel offset (K1-TC)
+        plan.tc = ConvTcPlan(params.q, params.n, w3, np.zeros(1, dtype=np.int64), None, plan.bias, plan.mask,
+                             chan=np.stack([ct_idx, slots], 1))
+    return plan
 
 
 def read_scalar_outputs(cts: list[Ciphertext], sk: bfv.SecretKey) -> np.ndarray:

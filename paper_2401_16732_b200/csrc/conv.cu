@@ -227,3 +227,63 @@ extern "C" int fhe_conv_flash(uint64_t q, int n, const uint64_t* in, int n_in, c
   if (c_o >= 8) return launch_conv<8, 1, 8, 2, 4>(a, st);
   return launch_conv<8, 1, 1, 2, 4>(a, st);
 }
+
+// ---------------------------------------------------------------------------
+// K1 pooling: conv.avg_pool (conv.py:604-623) sums the k x k window of every
+// slot through k² DRot taps of weight 1. The sum is exact mod q in any order,
+// so it is computed separably — k row taps into a staged row sum, then k
+// column taps of that sum (2k modular adds per slot instead of k²) — one
+// polynomial row per CTA, staged in shared memory. Identical ciphertexts to
+// the k²-tap contraction.
+namespace fhe {
+
+__global__ void __launch_bounds__(256) avg_pool_kernel(uint64_t q, int n, int k, int w_p,
+                                                       const uint64_t* __restrict__ in,
+                                                       uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t pool_sm[];
+  uint64_t* a = pool_sm;      // the row
+  uint64_t* hs = pool_sm + n;  // row sums h[i] = Σ_dx A(i + dx), i < n
+  const size_t row = blockIdx.x;
+  const uint64_t* src = in + row * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = src[i];
+  __syncthreads();
+  // A(j) = a[j] (j < n), -a[j - n] (n <= j < 2n): the negacyclic extension
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t s = 0;
+    for (int dx = 0; dx < k; ++dx) {
+      const int j = i + dx;
+      const uint64_t v = j < n ? a[j] : (a[j - n] ? q - a[j - n] : 0);
+      s = csub(s + v, q);
+    }
+    hs[i] = s;
+  }
+  __syncthreads();
+  uint64_t* dst = out + row * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    uint64_t s = 0;
+    for (int dy = 0; dy < k; ++dy) {
+      const int j = i + dy * w_p;  // H(j) = h[j] or -h[j - n]: every term of h[j - n + ...] wrapped
+      const uint64_t v = j < n ? hs[j] : (hs[j - n] ? q - hs[j - n] : 0);
+      s = csub(s + v, q);
+    }
+    dst[i] = s;
+  }
+}
+
+}  // namespace fhe
+
+extern "C" int fhe_avg_pool(uint64_t q, int n, int rows, int k, int w_p, const uint64_t* in, uint64_t* out,
+                            void* stream) {
+  if (n < 2 || (n & (n - 1)) || n > 8192) return fail(FHE_ERR_VALUE, "pool needs a power-of-two n <= 8192");
+  if (q < 2 || q >= (1ull << 62)) return fail(FHE_ERR_PARAMETER, "modulus out of range");
+  if (rows < 0 || k < 1 || w_p < 1) return fail(FHE_ERR_VALUE, "bad pool geometry");
+  if ((int64_t)(k - 1) * (w_p + 1) >= n) return fail(FHE_ERR_VALUE, "pool window must stay within one wrap");
+  if (!rows) return FHE_OK;
+  if (!in || !out || in == out) return fail(FHE_ERR_VALUE, "bad pool buffers");
+  const size_t smem = (size_t)2 * n * sizeof(uint64_t);
+  if (smem > 48 * 1024)
+    FHE_CUDA(cudaFuncSetAttribute(fhe::avg_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fhe::avg_pool_kernel<<<rows, 256, smem, (cudaStream_t)stream>>>(q, n, k, w_p, in, out);
+  FHE_CHECK_LAUNCH("avg_pool_kernel");
+  return FHE_OK;
+}

@@ -226,6 +226,20 @@ static bool split_enabled() {  // FHE_NTT_SPLIT=0 selects the one-CTA-per-row ke
   return v == 1;
 }
 
+// Register budget of the split kernels: __launch_bounds__(256, MINB) caps them
+// at 64K / (256 MINB) registers. MINB = 3 (85 registers, 6 resident 128-thread
+// CTAs = 24 warps per SM, a few bytes of spills) measured 7 % faster than the
+// unconstrained 106-120 registers (4 CTAs) on N = 16384; FHE_NTT_MINB = 1..4
+// selects the variant for A/B checks.
+static int split_minb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_NTT_MINB");
+    v = e ? atoi(e) : 3;
+  }
+  return v;
+}
+
 template <int LOGR, int R, bool INV, class IDX>
 __device__ __forceinline__ void split_phase(uint64_t* sm, IDX idx, const NttDesc& d, uint64_t O, int Lg, int s,
                                             int item, bool fold_ninv) {
@@ -323,8 +337,8 @@ __device__ __forceinline__ void split_sub(uint64_t* sm, IDX idx, const NttDesc& 
 // !COLS: this CTA = row, blocks [k0, k0 + 16): stages [a, a + b).
 // from_src: read through the LoadMap (first launch) else read dst in place;
 // final: canonical [0,q) output (second launch).
-template <int LOGR, bool INV, bool COLS>
-__global__ void __launch_bounds__(256) ntt_split_kernel(const LimbSet ls, const LoadMap lm, uint64_t* __restrict__ dst,
+template <int LOGR, bool INV, bool COLS, int MINB>
+__global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, const LoadMap lm, uint64_t* __restrict__ dst,
                                                         int a, int b, int from_src, int final_) {
   extern __shared__ uint64_t sm[];
   const int per_row = COLS ? (1 << b) / kSplitW : (1 << a) / kSplitW;
@@ -418,7 +432,12 @@ static int launch_split_one(const LimbSet& ls, const LoadMap& lm, uint64_t* dst,
   const int per_row = COLS ? (1 << b) / kSplitW : (1 << a) / kSplitW;
   const int threads = kSplitW * (len >> LOGR);
   const size_t smem = COLS ? (size_t)len * kSplitW * 8 : (size_t)(spad(len * kSplitW) + 1) * 8;
-  ntt_split_kernel<LOGR, INV, COLS><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_);
+  switch (split_minb()) {
+    case 2: ntt_split_kernel<LOGR, INV, COLS, 2><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_); break;
+    case 3: ntt_split_kernel<LOGR, INV, COLS, 3><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_); break;
+    case 4: ntt_split_kernel<LOGR, INV, COLS, 4><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_); break;
+    default: ntt_split_kernel<LOGR, INV, COLS, 1><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_);
+  }
   FHE_CHECK_LAUNCH("ntt_split_kernel");
   return FHE_OK;
 }

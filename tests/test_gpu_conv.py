@@ -305,3 +305,47 @@ def test_conv_conventional_fragmented_matches_reference(golden):
     y = conv.conv_conventional(xb, spec, swk, P)
     assert sha(_out(y.cts)) == g["h:out"]
     assert conv.unpack(y, sk).tolist() == g["dec"]
+
+
+def test_fully_connected_tensor_core_matches_int_and_oracle(monkeypatch):
+    """Config-4 FC shape (512 -> 200, one value per pooled ciphertext, bias):
+    the tensor-core path (one tap, per-input DRot slot as channel offset)
+    gives exactly the integer-pipe ciphertexts and the oracle's rows."""
+    from paper_2401_16732_b200 import conv
+
+    P = _P()
+    r = np.random.default_rng(512)
+    c, v_out = 512, 200
+    lay = conv.replace(conv.replace(conv.layout_direct(P, 8, 8, 3), c_n=1), stride=8)
+    arr = r.integers(0, Q, (c, 2, N), dtype=np.int64)
+    x = conv.PackedTensor(_cts(arr), lay, c)
+    w = r.integers(-127, 128, (v_out, c), dtype=np.int64)
+    b = r.integers(-100, 100, v_out, dtype=np.int64)
+    tc = _out(conv.fully_connected(x, w, P, bias=b))
+    monkeypatch.setenv("FLASHHE_CONV_PATH", "int")
+    ref = _out(conv.fully_connected(x, w, P, bias=b))
+    assert np.array_equal(tc, ref)
+    pos = [conv.channel_positions(lay, j) for j in range(c)]
+    ct_idx = np.concatenate([p[0] for p in pos])
+    slots = np.concatenate([p[1] for p in pos])
+    rows = [0, 77, 199]
+    want = O.fully_connected(arr, w[rows], ct_idx, slots, Q)
+    delta = P.delta
+    for i, o in enumerate(rows):  # bias: Δ·b[o] on slot 0 of c0 (conv.py:626-668)
+        want[i, 0, 0] = (int(want[i, 0, 0]) + delta * (int(b[o]) % P.p)) % Q
+    assert np.array_equal(tc[rows], want)
+
+
+@pytest.mark.parametrize("h,k,c", [(32, 2, 3), (64, 2, 2), (8, 8, 4), (16, 4, 8)])
+def test_avg_pool_separable_matches_oracle(h, k, c):
+    """The separable pool kernel equals the k²-tap DRot sum (conv.py:604-623)
+    on packed, fragmented and global-pool geometries."""
+    from paper_2401_16732_b200 import conv
+
+    P = _P()
+    r = np.random.default_rng(h * 10 + k)
+    lay = conv.layout_direct(P, h, h, 3)
+    arr = r.integers(0, Q, (lay.ct_count(c), 2, N), dtype=np.int64)
+    pooled = conv.avg_pool(conv.PackedTensor(_cts(arr), lay, c), k, P)
+    assert pooled.layout.stride == k
+    assert np.array_equal(_out(pooled.cts), O.avg_pool(arr, k, lay.w_p, Q))

@@ -228,9 +228,9 @@ static bool split_enabled() {  // FHE_NTT_SPLIT=0 selects the one-CTA-per-row ke
 
 // Register budget of the split kernels: __launch_bounds__(256, MINB) caps them
 // at 64K / (256 MINB) registers. MINB = 3 (85 registers, 6 resident 128-thread
-// CTAs = 24 warps per SM, a few bytes of spills) measured 7 % faster than the
-// unconstrained 106-120 registers (4 CTAs) on N = 16384; FHE_NTT_MINB = 1..4
-// selects the variant for A/B checks.
+// CTAs = 24 warps per SM) measured 7 % faster than the unconstrained 106-120
+// registers (4 CTAs) on N = 16384; FHE_NTT_MINB = 1 selects the unconstrained
+// variant for A/B checks.
 static int split_minb() {
   static int v = -1;
   if (v < 0) {
@@ -240,23 +240,35 @@ static int split_minb() {
   return v;
 }
 
-template <int LOGR, int R, bool INV, class IDX>
-__device__ __forceinline__ void split_phase(uint64_t* sm, IDX idx, const NttDesc& d, uint64_t O, int Lg, int s,
-                                            int item, bool fold_ninv) {
+// Element i of a phase item sits at a compile-time offset from the item's
+// base slot: columns are interleaved (slot = e * kSplitW + v), blocks are
+// padded (slot = v * (len + len/16) + e + e/16, 2-wavefront 64-bit accesses
+// for every stride); with B the item's first element and (i << TL) a multiple
+// of 2^TL, spad(B + (i << TL)) = spad(B) + (i << TL) + ((i << TL) >> 4).
+template <bool COLS, int TL>
+__device__ __forceinline__ constexpr int elem_off(int i) {
+  return COLS ? (i << TL) * kSplitW : (i << TL) + ((i << TL) >> 4);
+}
+
+// One phase of R stages on 2^LOGR register-resident elements. tb = O + B: the
+// merged-twiddle index of the item's first element; the group of g reads
+// psi[(tb + (g << TL)) >> (TL + a + 1)] = psi[(tb >> sh) + (g >> (a + 1))]
+// (g << TL is a multiple of 2^sh), so every index is one shift plus a constant.
+template <int LOGR, int R, bool INV, bool COLS, int TL>
+__device__ __forceinline__ void split_phase(uint64_t* __restrict__ p, const NttDesc& d, uint32_t tb,
+                                            bool fold_ninv) {
   const uint64_t q = d.m.q, q2 = 2 * q;
-  const int tl = Lg - (s + R);
-  const int base = ((item >> tl) << (tl + LOGR)) + (item & ((1 << tl) - 1));
   uint64_t e[1 << LOGR];
 #pragma unroll
-  for (int i = 0; i < (1 << LOGR); ++i) e[i] = sm[idx(base + (i << tl))];
+  for (int i = 0; i < (1 << LOGR); ++i) e[i] = p[elem_off<COLS, TL>(i)];
   if constexpr (!INV) {
     static_for<0, R>([&](auto ai) {
       constexpr int a = R - 1 - decltype(ai)::value;  // largest stride first
       constexpr int dd = 1 << a;
-      const int sh = tl + a + 1;
+      const uint32_t t0 = tb >> (TL + a + 1);
 #pragma unroll
       for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
-        const ulonglong2 tw = __ldg(&d.psi[(O + base + (g << tl)) >> sh]);
+        const ulonglong2 tw = __ldg(&d.psi[t0 + (g >> (a + 1))]);
 #pragma unroll
         for (int u = 0; u < dd; ++u) {
           uint64_t X = e[g + u];
@@ -271,7 +283,6 @@ __device__ __forceinline__ void split_phase(uint64_t* sm, IDX idx, const NttDesc
     static_for<0, R>([&](auto ai) {
       constexpr int a = decltype(ai)::value;  // smallest stride first
       constexpr int dd = 1 << a;
-      const int sh = tl + a + 1;
       if (fold_ninv && a == R - 1) {  // global stage 0: fold n^-1 (ring.py:162)
 #pragma unroll
         for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
@@ -283,9 +294,10 @@ __device__ __forceinline__ void split_phase(uint64_t* sm, IDX idx, const NttDesc
           }
         }
       } else {
+        const uint32_t t0 = tb >> (TL + a + 1);
 #pragma unroll
         for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
-          const ulonglong2 tw = __ldg(&d.ipsi[(O + base + (g << tl)) >> sh]);
+          const ulonglong2 tw = __ldg(&d.ipsi[t0 + (g >> (a + 1))]);
 #pragma unroll
           for (int u = 0; u < dd; ++u) {
             const uint64_t X = e[g + u], Y = e[g + u + dd];
@@ -298,56 +310,57 @@ __device__ __forceinline__ void split_phase(uint64_t* sm, IDX idx, const NttDesc
     });
   }
 #pragma unroll
-  for (int i = 0; i < (1 << LOGR); ++i) sm[idx(base + (i << tl))] = e[i];
+  for (int i = 0; i < (1 << LOGR); ++i) p[elem_off<COLS, TL>(i)] = e[i];
 }
 
-// all stages of a length-2^Lg sub-transform (Lg <= 8), LOGR-stage phases
-template <int LOGR, bool INV, class IDX>
-__device__ __forceinline__ void split_sub(uint64_t* sm, IDX idx, const NttDesc& d, uint64_t O, int Lg, int item,
-                                          bool fold_ninv) {
-  const int nfull = Lg / LOGR, rem = Lg - nfull * LOGR;
-  auto partial = [&](int s) {
-    static_for<1, LOGR>([&](auto ri) {
-      constexpr int R = decltype(ri)::value;
-      if (rem == R) split_phase<LOGR, R, INV>(sm, idx, d, O, Lg, s, item, fold_ninv && s == 0);
-    });
+// all LG stages of this thread's sub-transform v (LOGR-stage phases)
+template <int LOGR, bool INV, bool COLS, int LG>
+__device__ __forceinline__ void split_sub(uint64_t* sm, int v, int item, const NttDesc& d, uint32_t O, bool fold_ninv) {
+  constexpr int nfull = LG / LOGR, rem = LG - nfull * LOGR;
+  constexpr int len = 1 << LG;
+  auto phase = [&](auto s_c, auto r_c) {
+    constexpr int S = decltype(s_c)::value, R = decltype(r_c)::value;
+    constexpr int TL = LG - (S + R);
+    const int B = ((item >> TL) << (TL + LOGR)) + (item & ((1 << TL) - 1));
+    uint64_t* p = COLS ? sm + B * kSplitW + v : sm + v * (len + len / 16) + spad(B);
+    split_phase<LOGR, R, INV, COLS, TL>(p, d, O + (uint32_t)B, fold_ninv && S == 0);
   };
-  if (!INV) {
-    for (int p = 0; p < nfull; ++p) {
-      split_phase<LOGR, LOGR, false>(sm, idx, d, O, Lg, p * LOGR, item, false);
+  if constexpr (!INV) {
+    static_for<0, nfull>([&](auto pi) {
+      phase(std::integral_constant<int, decltype(pi)::value * LOGR>{}, std::integral_constant<int, LOGR>{});
       __syncthreads();
-    }
-    if (rem) {
-      partial(nfull * LOGR);
+    });
+    if constexpr (rem > 0) {
+      phase(std::integral_constant<int, nfull * LOGR>{}, std::integral_constant<int, rem>{});
       __syncthreads();
     }
   } else {
-    if (rem) {
-      partial(nfull * LOGR);
+    if constexpr (rem > 0) {
+      phase(std::integral_constant<int, nfull * LOGR>{}, std::integral_constant<int, rem>{});
       __syncthreads();
     }
-    for (int p = nfull - 1; p >= 0; --p) {
-      split_phase<LOGR, LOGR, true>(sm, idx, d, O, Lg, p * LOGR, item, fold_ninv && p == 0);
+    static_for<0, nfull>([&](auto pi) {
+      phase(std::integral_constant<int, (nfull - 1 - decltype(pi)::value) * LOGR>{},
+            std::integral_constant<int, LOGR>{});
       __syncthreads();
-    }
+    });
   }
 }
 
-// COLS: this CTA = row, columns [c0, c0 + 16): stages [0, a).
-// !COLS: this CTA = row, blocks [k0, k0 + 16): stages [a, a + b).
+// COLS: this CTA = row, columns [c0, c0 + 16): stages [0, a), LG = a.
+// !COLS: this CTA = row, blocks [k0, k0 + 16): stages [a, a + b), LG = b.
 // from_src: read through the LoadMap (first launch) else read dst in place;
 // final: canonical [0,q) output (second launch).
-template <int LOGR, bool INV, bool COLS, int MINB>
+template <int LOGR, bool INV, bool COLS, int MINB, int LG>
 __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, const LoadMap lm, uint64_t* __restrict__ dst,
-                                                        int a, int b, int from_src, int final_) {
+                                                              int a, int b, int from_src, int final_) {
   extern __shared__ uint64_t sm[];
+  constexpr int len = 1 << LG;
   const int per_row = COLS ? (1 << b) / kSplitW : (1 << a) / kSplitW;
   const int row = blockIdx.x / per_row, part = blockIdx.x % per_row;
   const int limb = (row / lm.G) % ls.L;
   const NttDesc d = ls.d[limb];
   const int n = d.n;
-  const int Lg = COLS ? a : b;
-  const int len = 1 << Lg;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const uint64_t* srow;
   int shift = 0;
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
   auto gidx = [&](int e, int v) -> size_t {
     return COLS ? (size_t)e * (1 << b) + part * kSplitW + v : (size_t)(part * kSplitW + v) * len + e;
   };
-  auto sidx = [&](int e, int v) -> int { return COLS ? e * kSplitW + v : spad(v * len + e); };
+  auto sidx = [&](int e, int v) -> int { return COLS ? e * kSplitW + v : v * (len + len / 16) + spad(e); };
   // load (pairs of consecutive elements: columns for COLS, positions for blocks)
   for (int i = tid; i < (len * kSplitW) / 2; i += nthr) {
     int e, v;
@@ -393,12 +406,11 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
   }
   __syncthreads();
   // one item per thread: (v, phase item)
-  const int ipv = len >> LOGR;  // phase items per sub-transform
+  constexpr int ipv = len >> LOGR;  // phase items per sub-transform
   const int v = COLS ? tid % kSplitW : tid / ipv;
   const int item = COLS ? tid / kSplitW : tid % ipv;
-  const uint64_t O = COLS ? (uint64_t)len : ((uint64_t)((1 << a) + part * kSplitW + v) << b);
-  auto idx = [&](int e) { return sidx(e, v); };
-  split_sub<LOGR, INV>(sm, idx, d, O, Lg, item, INV && COLS);
+  const uint32_t O = COLS ? (uint32_t)len : (uint32_t)((1 << a) + part * kSplitW + v) << b;
+  split_sub<LOGR, INV, COLS, LG>(sm, v, item, d, O, INV && COLS);
   // store
   const uint64_t q = d.m.q, q2 = 2 * q;
   for (int i = tid; i < (len * kSplitW) / 2; i += nthr) {
@@ -424,6 +436,12 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
   }
 }
 
+template <int LOGR, bool INV, bool COLS, int MINB, int LG>
+static void launch_split_k(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int grid, int threads, size_t smem,
+                           int a, int b, int from_src, int final_, cudaStream_t st) {
+  ntt_split_kernel<LOGR, INV, COLS, MINB, LG><<<grid, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_);
+}
+
 template <int LOGR, bool INV, bool COLS>
 static int launch_split_one(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int a, int b,
                             int from_src, int final_, cudaStream_t st) {
@@ -432,11 +450,16 @@ static int launch_split_one(const LimbSet& ls, const LoadMap& lm, uint64_t* dst,
   const int per_row = COLS ? (1 << b) / kSplitW : (1 << a) / kSplitW;
   const int threads = kSplitW * (len >> LOGR);
   const size_t smem = COLS ? (size_t)len * kSplitW * 8 : (size_t)(spad(len * kSplitW) + 1) * 8;
-  switch (split_minb()) {
-    case 2: ntt_split_kernel<LOGR, INV, COLS, 2><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_); break;
-    case 3: ntt_split_kernel<LOGR, INV, COLS, 3><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_); break;
-    case 4: ntt_split_kernel<LOGR, INV, COLS, 4><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_); break;
-    default: ntt_split_kernel<LOGR, INV, COLS, 1><<<rows * per_row, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_);
+  const int grid = rows * per_row;
+  const bool capped = split_minb() != 1;
+  if (Lg == 6) {
+    if (capped) launch_split_k<LOGR, INV, COLS, 3, 6>(ls, lm, dst, grid, threads, smem, a, b, from_src, final_, st);
+    else launch_split_k<LOGR, INV, COLS, 1, 6>(ls, lm, dst, grid, threads, smem, a, b, from_src, final_, st);
+  } else if (Lg == 7) {
+    if (capped) launch_split_k<LOGR, INV, COLS, 3, 7>(ls, lm, dst, grid, threads, smem, a, b, from_src, final_, st);
+    else launch_split_k<LOGR, INV, COLS, 1, 7>(ls, lm, dst, grid, threads, smem, a, b, from_src, final_, st);
+  } else {
+    return fail(FHE_ERR_VALUE, "split NTT sub-transform length 2^%d unsupported", Lg);
   }
   FHE_CHECK_LAUNCH("ntt_split_kernel");
   return FHE_OK;

@@ -13,7 +13,10 @@ from pathlib import Path
 
 from .errors import AccumulatorBudgetError, EncodingError, ParameterError, ProtocolError
 
-LIB_PATH = Path(__file__).resolve().parent / "libflashhe.so"
+import os  # noqa: E402
+
+# FLASHHE_LIB: an alternative build of the same library (development probes only)
+LIB_PATH = Path(os.environ.get("FLASHHE_LIB") or Path(__file__).resolve().parent / "libflashhe.so")
 
 FHE_OK = 0
 _ERRORS = {

@@ -148,17 +148,59 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t b
       : "r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
-// The 9 (or 1, or `taps`) MMAs of one accumulator for one stage. Descriptors
-// advance by adding 16-byte units to the start-address field (addresses stay
-// below 256 KB, so the 14-bit field never carries): weights by 256 units per
-// tap, the window by the tap's DRot offset. The unrolled forms keep the
-// issue loop shorter than the tensor pipe's 129 cycles per MMA.
-template <int TAPS>
-__device__ __forceinline__ void issue_taps(uint32_t acc, uint64_t adesc, uint64_t bdesc, const uint32_t* off16,
-                                           uint32_t idesc, bool first) {
+// D[128 x N] (+)= A · B^T with the descriptors given as (low, high) words:
+// the high word (SBO, layout bits) is the same for every operand here.
+__device__ __forceinline__ void mma_i8w(uint32_t tmem, uint32_t alo, uint32_t blo, uint32_t dhi, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %3};\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %4, p;\n\t}"
+      :
+      : "r"(tmem), "r"(alo), "r"(blo), "r"(dhi), "r"(idesc), "r"(accum));
+}
+
+// Warp-wide forms: every lane of the MMA warp runs the issue loop (uniform
+// control flow, so loop state can live in uniform registers) and elect.sync
+// picks the one lane that issues.
+__device__ __forceinline__ void mma_i8w_elect(uint32_t tmem, uint32_t alo, uint32_t blo, uint32_t dhi,
+                                              uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "mov.b64 da, {%1, %3};\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %4, p;\n\t}"
+      :
+      : "r"(tmem), "r"(alo), "r"(blo), "r"(dhi), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+// The 9 (or 1) MMAs of one accumulator for one stage. Descriptors advance by
+// adding 16-byte units to the start-address field of the low word (addresses
+// stay below 256 KB, so the 14-bit field never carries): weights by 256 units
+// per tap, the window by the tap's DRot offset. `before_last` runs between the
+// last two MMAs (while the tensor pipe still holds queued work): the issuer
+// uses it to wait for the NEXT stage there, so the gap between stages stays
+// under the ~100 cycles the pipe tolerates (tools/ring_probe.cu).
+template <int TAPS, class F>
+__device__ __forceinline__ void issue_taps(uint32_t acc, uint32_t alo, uint32_t blo, uint32_t dhi,
+                                           const uint32_t* off16, uint32_t idesc, bool first, F&& before_last) {
 #pragma unroll
-  for (int tp = 0; tp < TAPS; ++tp)
-    mma_i8(acc, adesc + (uint64_t)(tp * (4096 >> 4)), bdesc + off16[tp], idesc, (first && tp == 0) ? 0u : 1u);
+  for (int tp = 0; tp < TAPS; ++tp) {
+    if (tp == TAPS - 1) before_last();
+    mma_i8w_elect(acc, alo + (uint32_t)(tp * (4096 >> 4)), blo + off16[tp], dhi, idesc, (first && tp == 0) ? 0u : 1u);
+  }
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -475,59 +517,84 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
     // a 64-position tile takes both (acc a <- positions 32a..32a+31, same
     // weights: half the weight traffic per position). Per-buffer use counts
     // give the tmem_full / tmem_empty parities on both sides.
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; elect.sync issues (see mma_i8w_elect)
       int s_mma = 0, prev_sb = -1, tl = 0, nb = 0;
       uint32_t par = 0, use = 0;  // per-stage full parity; per-buffer use parity (bit b)
+      const uint64_t desc0 = umma_desc(smem_u32(smem));  // ring base; stage s adds s * stage_bytes / 16
+      const uint32_t dlo0 = (uint32_t)desc0, dhi = (uint32_t)(desc0 >> 32);
+      bool pre = false;  // the current stage's full barrier was already waited for
       for (int l = 0; l < nl; ++l) {
         const LayerDesc& d = A.L[l];
-        if (d.tiles <= first_tile(d)) continue;  // no tiles of this layer here (the loader skips it too)
-        if (d.stage_bytes != prev_sb) s_mma = 0;  // the loader drained and re-partitioned the ring
-        prev_sb = d.stage_bytes;
+        // Per-layer values in registers: the barrier asm below clobbers memory,
+        // so fields read through `d` inside the loops would be re-fetched from
+        // the parameter bank (dependent LDCs) at every stage.
+        const int tiles = d.tiles, t0 = first_tile(d);
+        if (tiles <= t0) continue;  // no tiles of this layer here (the loader skips it too)
+        const int stage_bytes = d.stage_bytes, JB = d.JB, nacc = d.nacc, taps = d.taps, nst = d.nst;
+        if (stage_bytes != prev_sb) s_mma = 0;  // the loader drained and re-partitioned the ring
+        prev_sb = stage_bytes;
         const uint32_t idesc = idesc_i8(8 * d.npos);
+        const uint32_t sstep = (uint32_t)(stage_bytes >> 4), wdesc = (uint32_t)(d.win_bytes >> 4);
+        const uint32_t adelta = (uint32_t)(d.npos * 256 >> 4);  // second accumulator's positions
         uint32_t off16[9];  // this layer's DRot offsets in 16-byte descriptor units (taps <= 9 fast path)
 #pragma unroll
-        for (int tp = 0; tp < 9; ++tp) off16[tp] = tp < d.taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
-        for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
+        for (int tp = 0; tp < 9; ++tp) off16[tp] = tp < taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
+        for (int t = t0; t < tiles; t += G, ++tl) {
           int b0 = 0, b1 = 1;
-          if (d.nacc == 1) {
+          if (nacc == 1) {
             b0 = nb;
             nb ^= 1;
           }
-          TC_TRACE(0, tl);
-          for (int jb = 0; jb < d.JB; ++jb) {
+          if (lane == 0) TC_TRACE(0, tl);
+          const bool more_tiles = t + G < tiles;
+          for (int jb = 0; jb < JB; ++jb) {
             const int s = s_mma;
-            mbar_wait(full_bar(s), (par >> s) & 1);
-            par ^= 1u << s;
+            const int s_next = s + 1 == nst ? 0 : s + 1;
+            if (!pre) {
+              mbar_wait(full_bar(s), (par >> s) & 1);
+              par ^= 1u << s;
+            }
+            pre = false;
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
-            const uint32_t sw = sx + d.win_bytes;
-            const uint64_t adesc = umma_desc(sw);
-            for (int a = 0; a < d.nacc; ++a) {
+            const uint32_t blo0 = dlo0 + (uint32_t)s * sstep;  // window at the stage base
+            const uint32_t alo = blo0 + wdesc;                  // weights after the window
+            const bool has_next = jb + 1 < JB || more_tiles;    // next stage of this layer on this CTA
+            for (int a = 0; a < nacc; ++a) {
               const int b = a == 0 ? b0 : b1;
               if (jb == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
                 mbar_wait(tempty_bar(b), ((use >> b) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
               }
               const uint32_t acc = tmem + b * kAccCols;
-              const uint64_t bdesc = umma_desc(sx + (uint32_t)(a * d.npos) * 256);
-              if (d.taps == 9)
-                issue_taps<9>(acc, adesc, bdesc, off16, idesc, jb == 0);
-              else if (d.taps == 1)
-                issue_taps<1>(acc, adesc, bdesc, off16, idesc, jb == 0);
-              else
-                for (int tp = 0; tp < d.taps; ++tp)
-                  mma_i8(acc, adesc + (uint64_t)(tp * (4096 >> 4)), bdesc + (uint32_t)d.tap_off[tp] * 16, idesc,
-                         (jb | tp) != 0);
+              const uint32_t blo = blo0 + (uint32_t)a * adelta;
+              auto wait_next = [&] {
+                if (a == nacc - 1 && has_next) {
+                  mbar_wait(full_bar(s_next), (par >> s_next) & 1);
+                  par ^= 1u << s_next;
+                  pre = true;
+                }
+              };
+              if (taps == 9) {
+                issue_taps<9>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+              } else if (taps == 1) {
+                issue_taps<1>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+              } else {
+                for (int tp = 0; tp < taps; ++tp) {
+                  if (tp == taps - 1) wait_next();
+                  mma_i8w_elect(acc, alo + (uint32_t)(tp * (4096 >> 4)), blo + (uint32_t)d.tap_off[tp] * 16, dhi,
+                                idesc, (jb | tp) != 0);
+                }
+              }
             }
-            mma_commit(empty_bar(s));  // stage free once these MMAs retire
-            s_mma = s + 1 == d.nst ? 0 : s + 1;
+            mma_commit_elect(empty_bar(s));  // stage free once these MMAs retire
+            s_mma = s_next;
           }
-          for (int a = 0; a < d.nacc; ++a) {
+          for (int a = 0; a < nacc; ++a) {
             const int b = a == 0 ? b0 : b1;
-            mma_commit(tfull_bar(b));  // accumulator complete
+            mma_commit_elect(tfull_bar(b));  // accumulator complete
             use ^= 1u << b;
           }
-          TC_TRACE(1, tl);
+          if (lane == 0) TC_TRACE(1, tl);
         }
       }
     }
@@ -562,11 +629,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             used |= 1u << s;
             par ^= 1u << s;
             const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
+#ifdef TC_PROBE_NOFILL  // timing probe only: MMAs on stale stage data, no fill traffic
+            (void)sx;
+            (void)xbase;
+            (void)wbase;
+            mbar_arrive(full_bar(s));
+#else
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
                          "r"(win_load + wstage)
                          : "memory");
             bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
             bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
+#endif
             s_ld = s + 1 == d.nst ? 0 : s + 1;
           }
         }
@@ -617,7 +691,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
           use ^= 1u << buf;
           if (lane == 0 && warp == 2) TC_TRACE(5, tl);
           asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef TC_PROBE_NOEPI  // timing probe only: accumulators released unread
+          if (false) {
+#else
           if (active) {
+#endif
             // lane = output channel within the quadrant; a 32-column TMEM chunk
             // holds 4 positions x 8 planes. lo = q + Σ_{d<4} 2^(8d) P_d and
             // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,

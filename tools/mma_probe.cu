@@ -23,13 +23,16 @@ __device__ __forceinline__ bool try_wait(uint32_t bar, uint32_t par) {
 }
 
 // mode 0: resident operands, same descriptors; 1: conv pattern (A walks 9 taps, B shifts);
+// 2: conv pattern, ONE accumulator for every MMA (the conv tile); 3: conv pattern,
+// accumulator alternating every MMA; 4: as 2 with random operand bytes;
 // copy_bytes > 0: warp 1 streams that many bytes per round into a separate region
 __global__ void __launch_bounds__(128, 1) probe(int iters, int mode, int copy_bytes, const uint8_t* src, int* sink) {
   extern __shared__ __align__(1024) uint8_t sm[];
   // layout: [0, 64K) operands, [64K, 64K + 96K) copy target, bars at 160K
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 216 * 1024);
   uint32_t* slot = reinterpret_cast<uint32_t*>(sm + 216 * 1024 + 64);
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(sm)[i] = mode == 4 ? (uint32_t)(i * 2654435761u) ^ 0x9e3779b9u : 0x01010101u * (i & 3);
   asm volatile("fence.proxy.async.shared::cta;");
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
@@ -48,6 +51,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mode, int copy_by
   if (threadIdx.x == 0) *stop = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
+    const long long c0 = clock64();
     const uint32_t base = smem_u32(sm);
     for (int it = 0; it < iters; ++it) {
       for (int tp = 0; tp < 9; ++tp) {
@@ -59,12 +63,14 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mode, int copy_by
           a = desc(base + 16384 + tp * 4096);                         // weights of tap tp
           b = desc(base + ((tp / 3) * 10 + (tp % 3)) * 256);          // window shifted by the tap
         }
-        mma(tmem + (it & 1) * 256, a, b, 1);
+        const uint32_t accb = mode == 1 ? (it & 1) : mode == 3 ? (tp & 1) : mode == 0 ? (it & 1) : 0;
+        mma(tmem + accb * 256, a, b, 1);
       }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
     while (!try_wait(smem_u32(bar), 0)) {
     }
+    if (blockIdx.x == 0) reinterpret_cast<long long*>(sink)[1] = clock64() - c0;
     *stop = 1;
   } else if (threadIdx.x == 32 && copy_bytes > 0) {
     // three copies of copy_bytes in flight (ring of 3 slots), like the conv loader
@@ -107,8 +113,8 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int iters = 2000;
-  for (int mode = 0; mode < 2; ++mode)
-    for (int cb : {0, 16384, 32768, 51200}) {
+  for (int mode = 0; mode < 5; ++mode)
+    for (int cb : {0, 51200}) {
       probe<<<148, 128, smem>>>(50, mode, cb, src, sink);
       cudaEventRecord(e0);
       probe<<<148, 128, smem>>>(iters, mode, cb, src, sink);
@@ -117,8 +123,10 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       const double ops = 148.0 * iters * 9 * 2.0 * 128 * 256 * 32;
-      printf("mode %d copies of %6d B (3 in flight): %.1f TOPS (%.1f cycles per MMA @1.9GHz) %s\n", mode, cb, ops / ms / 1e9,
-             ms * 1e-3 * 1.9e9 / (iters * 9.0), cudaGetErrorString(cudaGetLastError()));
+      long long cyc[2];
+      cudaMemcpy(cyc, sink, 16, cudaMemcpyDeviceToHost);
+      printf("mode %d copies of %6d B (3 in flight): %.1f TOPS, %.1f SM cycles per MMA (clock64), %.0f MHz %s\n", mode, cb,
+             ops / ms / 1e9, cyc[1] / (iters * 9.0), cyc[1] / (ms * 1e3), cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
 }

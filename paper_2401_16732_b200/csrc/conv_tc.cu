@@ -57,6 +57,9 @@ constexpr int kWTap = kOcTile * 32;  // packed weight bytes per (tap, 32 channel
 constexpr int kStg = 2048;           // relayout staging bytes per warp (16 positions x 128 B)
 constexpr int kRingBudget = 212 * 1024;
 constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
+#ifndef FHE_RELAYOUT_STATIC
+#define FHE_RELAYOUT_STATIC 1
+#endif
 #ifndef FHE_UNITS_PER_GRAB
 #define FHE_UNITS_PER_GRAB 1
 #endif
@@ -483,6 +486,28 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   // processed, so its round trip overlaps useful work.
   auto relayout_layer = [&](int l, int participants) {
     const LayerDesc& d = A.L[l];
+#if FHE_RELAYOUT_STATIC
+    // static round-robin: relayout warp r of R takes units r, r + R, ... two at
+    // a time. No shared work counter: ~1.7k atomics per layer on one address
+    // serialised the early (small, latency-bound) layers; 2 % faster stack.
+    {
+      const int wi = participants == P0 ? warp - 2 : warp - (2 + kEpiWarps);
+      const int R = G * participants;
+      for (int u = wi * G + (int)blockIdx.x; u < d.units; u += 2 * R) {
+        UnitLoad U0, U1;
+        const bool two = u + R < d.units;
+        relayout_load(d, n, u, lane, U0);
+        if (two) relayout_load(d, n, u + R, lane, U1);
+        relayout_store(d, q, lane, U0, stg);
+        if (two) relayout_store(d, q, lane, U1, stg);
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(A.sync + 1, 1ull);
+      return;
+    }
+#endif
     constexpr unsigned long long kG = kUnitsPerGrab;
     const unsigned long long base = e1 * (kG * ((d.units + kG - 1) / kG) + kG * Gu * participants);
     unsigned long long nxt = 0;

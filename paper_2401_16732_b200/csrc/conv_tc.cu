@@ -728,7 +728,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
             uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + s0;
 #pragma unroll 1
-            for (int k = sub; k < d.npos / 4; k += kEpiWarps / 4) {
+            // each warp of the quadrant takes a contiguous half of the chunks: a
+            // lane then writes whole 128-byte lines of its channel row
+            const int kper = d.npos / 4 / (kEpiWarps / 4);
+            for (int k = sub * kper; k < (sub + 1) * kper; ++k) {
               uint32_t v[32];
               TMEM_LD32(acc + k * 32, v);
               asm volatile("tcgen05.wait::ld.sync.aligned;");
@@ -752,11 +755,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
                 for (int j = 0; j < 4; ++j)
                   if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
               }
-              if (o < d.c_o) {
-                ulonglong2* dst = reinterpret_cast<ulonglong2*>(orow + 4 * k);
-                dst[0] = make_ulonglong2(r[0], r[1]);
-                dst[1] = make_ulonglong2(r[2], r[3]);
-              }
+              if (o < d.c_o)  // one 32-byte store per lane: a full sector (STG.256)
+                asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(orow + 4 * k), "l"(r[0]), "l"(r[1]),
+                             "l"(r[2]), "l"(r[3])
+                             : "memory");
             }
           }
           asm volatile("tcgen05.fence::before_thread_sync;");

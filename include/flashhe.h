@@ -250,6 +250,29 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
 int fhe_pmac(uint64_t q, int n, const uint64_t* R, const uint64_t* pt_mont, const int32_t* term_off,
              const int32_t* terms, int n_out, uint64_t* out, void* stream);
 
+/* Fused conventional convolution (conv.py:457-564, north_star (b)): rotation,
+ * encoded-weight multiply and accumulation in one pass, EVAL domain, modulus q.
+ * For output o and slot x:
+ *   out[o][p][x] = Σ_g Σ_{(o, pt) in terms(g)} PT[pt][x] · R_g[p][x]   mod q
+ * with R_g = HRot(C[src_g], step_g) formed in registers from the hoisted digits
+ * (bfv.hrot, bfv.py:467-500) — rotated ciphertexts are never written:
+ *   R_g[0][x] = C[src][0][π(x)] + Σ_i D[src][i][π(x)] K[key_g][i][0][x]
+ *   R_g[1][x] =                   Σ_i D[src][i][π(x)] K[key_g][i][1][x]
+ * π(x) = index_of_exp[(exp_at_index[x] · gpow_g) mod 2n] (ring.py:199-202);
+ * key_g = -1 means step 0 (R_g = C[src]).
+ * C: DEVICE [nsrc][2][n]; D: DEVICE [nsrc][ndig][n] (fhe_ntt_forward_digits);
+ * K_mont: DEVICE [nkeys][ndig][2][n] Montgomery keys; groups: DEVICE int32
+ * [G][2] = (src, key); gpow: DEVICE uint64 [G]; outputs in tiles of 16:
+ * tile_off: DEVICE int32 [ceil(n_out/16)][G+1] CSR offsets into terms, terms:
+ * DEVICE int32 pairs (o mod 16, plaintext row); pt_mont: DEVICE [nPT][n]
+ * Montgomery plaintexts. gchunks > 1 splits the groups over that many CTAs
+ * per slot block (partial: DEVICE [gchunks][n_out][2][n] scratch). ndig <= 16,
+ * ndig · q < 2^64. out: DEVICE [n_out][2][n], canonical. */
+int fhe_rot_pmac(uint64_t q, int n, int ndig, const uint64_t* C, const uint64_t* D, const uint64_t* K_mont,
+                 int G, const int32_t* groups, const uint64_t* gpow, int n_out, const int32_t* tile_off,
+                 const int32_t* terms, const uint64_t* pt_mont, int gchunks, uint64_t* partial, uint64_t* out,
+                 void* stream);
+
 /* ------------------------------------ K5: x^2+x share arithmetic (act2pc) */
 /* Client share pass, one vectorised pass
  * over decrypted slots w in [0,p): y = (w^2 + w * 2^f) mod p. */

@@ -78,6 +78,10 @@ SIGNATURES = {
     "fhe_to_montgomery": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_keyswitch_apply": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _int, _u64, _vp, _vp]),
     "fhe_pmac": (_int, [_u64, _int, _vp, _vp, _vp, _vp, _int, _vp, _vp]),
+    "fhe_rot_pmac": (
+        _int,
+        [_u64, _int, _int, _vp, _vp, _vp, _int, _vp, _vp, _int, _vp, _vp, _vp, _int, _vp, _vp, _vp],
+    ),
     "fhe_act_client_square": (_int, [_u64, _int, _i64, _vp, _vp, _vp]),
     "fhe_act_server_const": (_int, [_u64, _int, _i64, _vp, _vp, _vp, _vp, _vp]),
     "fhe_act_gather": (_int, [_i64, _vp, _vp, _vp, _vp]),

@@ -710,24 +710,99 @@ def _rotations(cts, needed, swks, params) -> tuple[torch.Tensor, dict]:
     return torch.cat(rows, 0), index
 
 
-def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.SwitchingKeySet,
-                      params: RingParams) -> PackedTensor:
-    """Baseline: HRot per (tap, channel offset) + PMult by weight plaintexts
-    + HAdd (conv.py:457-564). Same terms, same result; on the device the
-    rotations are batched (hoisted digits, one K4 launch per step) and every
-    output's pmult/hadd chain is one fused K4b accumulation (fhe_pmac)."""
-    layout = x.layout
-    if x.cts[0].encoding != Encoding.BATCH:
-        raise EncodingError("conventional convolution needs batch-encoded input")
-    if (layout.height, layout.width) != (layer.height, layer.width) or layout.pad != layer.f_w // 2:
-        raise ParameterError("tensor layout does not match the layer geometry")
+def _stacked_keys(swks: bfv.SwitchingKeySet, steps: tuple) -> torch.Tensor:
+    """[len(steps)][l][2][n] Montgomery keys of several steps, cached on the key set."""
+    cache = swks.__dict__.setdefault("_stacked", {})
+    t = cache.get(steps)
+    if t is None:
+        t = cache[steps] = torch.stack([swks.device_keys(s) for s in steps])
+    return t
+
+
+def _conventional_fused(in_cts, plan, swks, params, out) -> None:
+    """HRot x PMult x HAdd of every output in one fhe_rot_pmac pass: each
+    rotation (source ciphertext, step) is key-switched in registers from the
+    hoisted digits and applied to every plaintext that uses it; rotated
+    ciphertexts are never materialised (north_star b). The column-swap source
+    set (packed layouts with two orbits) is one hoisted HRot of the inputs.
+    The static operands (groups, term lists, plaintexts, stacked keys) are
+    built once per (plan, key set, input count) and kept on the device."""
+    n, q = params.n, params.q
+    T = swks.decomp_log
+    l = -(-q.bit_length() // T)
+    B = len(in_cts)
+    terms = plan["terms"]
+    st_key = (id(swks), B)
+    hit = plan["dev"].get(st_key)
+    if hit is None or hit[0] is not swks:
+        needed = {(st, sw) for tl in terms for _, st, sw, _ in tl}
+        steps = tuple(sorted({st for st, _ in needed if st}))
+        kidx = {st: i for i, st in enumerate(steps)}
+        # rotation groups, ordered by key so consecutive groups reuse it from L2
+        gkeys = sorted({(kidx.get(st, -1), int(sw) * B + b, st) for tl in terms for b, st, sw, _ in tl})
+        gpos = {(src, st): g for g, (_, src, st) in enumerate(gkeys)}
+        G = len(gkeys)
+        tiles = -(-len(terms) // 16)
+        per = [[[] for _ in range(G)] for _ in range(tiles)]
+        for o, tl in enumerate(terms):
+            for b, st, sw, p_ in tl:
+                per[o // 16][gpos[(int(sw) * B + b, st)]].append((o % 16, p_))
+        toff = np.zeros((tiles, G + 1), dtype=np.int32)
+        flat = []
+        for t in range(tiles):
+            toff[t, 0] = len(flat)
+            for g in range(G):
+                flat.extend(per[t][g])
+                toff[t, g + 1] = len(flat)
+        garr = np.array([(src, k) for k, src, _ in gkeys], dtype=np.int32).reshape(-1, 2)
+        gp = np.array([bfv._galois_element(st, n) if st else 1 for _, _, st in gkeys], dtype=np.uint64)
+        tarr = np.asarray(flat, dtype=np.int32).reshape(-1, 2) if flat else np.zeros((1, 2), np.int32)
+        pt_rows = plan["pt_rows"]
+        assert tarr[:, 1].max(initial=0) < len(pt_rows)
+        pt = device.to_device(np.stack(pt_rows))
+        pt_mont = torch.empty_like(pt)
+        _native.call("fhe_to_montgomery", _native.u64_array([q]), 1, 1, len(pt_rows), n, pt.data_ptr(),
+                     pt_mont.data_ptr(), device.stream())
+        dev = pt.device
+        K = _stacked_keys(swks, steps) if steps else torch.zeros(1, dtype=torch.int64, device=dev)
+        st = {
+            "swap": any(sw for _, sw in needed), "G": G, "tiles": tiles, "K": K, "pt": pt, "pt_mont": pt_mont,
+            "g": torch.from_numpy(garr).to(dev), "gp": torch.from_numpy(gp.view(np.int64)).to(dev),
+            "toff": torch.from_numpy(toff).to(dev), "terms": torch.from_numpy(np.ascontiguousarray(tarr)).to(dev),
+            "rotations": sum(1 for k, _, _ in gkeys if k >= 0), "macs": len(flat),
+        }
+        plan["dev"][st_key] = hit = (swks, st)
+    st = hit[1]
+    ring._bump("modmul", 2 * n * (l * st["rotations"] + st["macs"]))
+    base = bfv.cts_rows(in_cts).reshape(B, 2, n)
+    srcs = [base]
+    if st["swap"]:
+        digits0 = bfv.key_digits_rows(base[:, 1], params, T, l)
+        srcs.append(bfv.keyswitch_rows(base, digits0, bfv.COLUMN_ROTATION, swks))
+        ring._bump("modmul", 2 * n * l * B)
+    C = torch.cat(srcs, 0).contiguous() if len(srcs) > 1 else base.contiguous()  # src = swap * B + b
+    D = torch.cat([bfv.key_digits_rows(src[:, 1], params, T, l) for src in srcs], 0).contiguous()
+    n_out, G, tiles = len(terms), st["G"], st["tiles"]
+    chunks = max(1, min(G, -(-2 * 148 // ((n // 64) * tiles))))
+    part = torch.empty((chunks, n_out, 2, n), dtype=torch.int64, device=C.device) if chunks > 1 else None
+    _native.call("fhe_rot_pmac", q, n, l, C.data_ptr(), D.data_ptr(), st["K"].data_ptr(), G, st["g"].data_ptr(),
+                 st["gp"].data_ptr(), n_out, st["toff"].data_ptr(), st["terms"].data_ptr(), st["pt_mont"].data_ptr(),
+                 chunks, device.ptr(part), out.data_ptr(), device.stream())
+
+
+def _conventional_plan(layer: ConvLayerSpec, layout: TileLayout, n_in: int, params: RingParams) -> dict:
+    """The baseline's terms per output [(b, step, swap, plaintext row)], the
+    encoded-weight plaintexts and the bias slots (conv.py:457-564), built once
+    per (layer, layout) and cached on the layer (weights immutable after use)."""
+    key = ("conventional", layout, n_in, params.fingerprint())
+    cache = layer.__dict__.setdefault("_k1_plans", {})
+    if key in cache:
+        return cache[key]
     taps = _tap_steps(layout, layer.f_w)
     n, cpu, ring_slots = params.n, layout.c_n, params.n // 2
-    in_cts = list(x.cts)
-    for ct in in_cts:
-        if ct.domain != Domain.EVAL:
-            raise EncodingError("HRot operates in the evaluation domain")
+    in_cts = range(n_in)
     pts: dict[bytes, int] = {}
+
     pt_rows: list[np.ndarray] = []
 
     def pt_uniform(w: int) -> int:  # _uniform_prepared: constant polynomial, constant NTT
@@ -791,6 +866,30 @@ def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.Switching
                             tl.append((b, int((step + d * layout.tile) % layout.ring) % ring_slots, swap,
                                        pt_blocks(bw)))
             terms.append(tl)
+    plan = cache[key] = {"terms": terms, "pt_rows": pt_rows, "biases": biases, "dev": {}}
+    return plan
+
+
+def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.SwitchingKeySet,
+                      params: RingParams) -> PackedTensor:
+    """Baseline: HRot per (tap, channel offset) + PMult by weight plaintexts
+    + HAdd (conv.py:457-564). Same terms, same result; on the device the whole
+    chain is one fused pass (fhe_rot_pmac: rotations key-switched in registers
+    from hoisted digits, never written to HBM). FLASHHE_CONVENTIONAL=
+    materialized selects the two-kernel form (batched K4 rotations + fhe_pmac)
+    for A/B checks."""
+    layout = x.layout
+    if x.cts[0].encoding != Encoding.BATCH:
+        raise EncodingError("conventional convolution needs batch-encoded input")
+    if (layout.height, layout.width) != (layer.height, layer.width) or layout.pad != layer.f_w // 2:
+        raise ParameterError("tensor layout does not match the layer geometry")
+    in_cts = list(x.cts)
+    for ct in in_cts:
+        if ct.domain != Domain.EVAL:
+            raise EncodingError("HRot operates in the evaluation domain")
+    plan = _conventional_plan(layer, layout, len(in_cts), params)
+    terms, pt_rows, biases = plan["terms"], plan["pt_rows"], plan["biases"]
+    n = params.n
     needed = {(st, sw) for tl in terms for _, st, sw, _ in tl}
     for st, sw in needed:  # the reference raises KeyError for a missing key, EncodingError for a bad ct
         for ct in in_cts[:1]:
@@ -801,7 +900,11 @@ def conv_conventional(x: PackedTensor, layer: ConvLayerSpec, swks: bfv.Switching
     dev = device.require_cuda()
     n_out = len(terms)
     out = torch.empty((n_out, 2, n), dtype=torch.int64, device=dev)
-    if needed:
+    import os
+
+    if needed and os.environ.get("FLASHHE_CONVENTIONAL", "fused") == "fused":
+        _conventional_fused(in_cts, plan, swks, params, out)
+    elif needed:
         R, index = _rotations(in_cts, needed, swks, params)
         pt = device.to_device(np.stack(pt_rows))
         pt_mont = torch.empty_like(pt)

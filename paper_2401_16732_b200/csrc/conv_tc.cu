@@ -727,10 +727,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             // q > 2^56); V = lo + 2^32 hi.
             const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
             uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + s0;
-#pragma unroll 1
             // each warp of the quadrant takes a contiguous half of the chunks: a
             // lane then writes whole 128-byte lines of its channel row
             const int kper = d.npos / 4 / (kEpiWarps / 4);
+#pragma unroll 1
             for (int k = sub * kper; k < (sub + 1) * kper; ++k) {
               uint32_t v[32];
               TMEM_LD32(acc + k * 32, v);

@@ -357,6 +357,85 @@ __global__ void __launch_bounds__(256) pmac_kernel(const ModDesc m, int n, const
   out[((size_t)o * 2 + 1) * n + i] = barrett128(lo1, hi1, m);
 }
 
+// ------------------------------------- K4c fused HRot x PMult x HAdd (north_star b)
+// The conventional convolution's whole chain for one block of slots: each
+// rotation group g (source ciphertext, Galois step) is key-switched in
+// registers from the hoisted digits (bfv.hrot, bfv.py:467-500), multiplied by
+// every encoded-weight plaintext that uses it and accumulated into the
+// outputs' shared-memory accumulators — rotated ciphertexts never reach HBM.
+// blockIdx.x: 64 slots; blockIdx.y: a tile of kRotOT outputs; blockIdx.z: a
+// chunk of groups (partial sums into part[z] when gridDim.z > 1).
+constexpr int kRotOT = 16, kRotX = 64, kRotMaxDig = 16;
+
+__global__ void __launch_bounds__(kRotX) rot_pmac_kernel(const ModDesc m, int logn, int ndig, int G, int n_out,
+                                                          int gchunk, const uint64_t* __restrict__ C,
+                                                          const uint64_t* __restrict__ D,
+                                                          const uint64_t* __restrict__ K,
+                                                          const int2* __restrict__ groups,
+                                                          const uint64_t* __restrict__ gpow,
+                                                          const int* __restrict__ toff,
+                                                          const int2* __restrict__ terms,
+                                                          const uint64_t* __restrict__ PT, uint64_t* __restrict__ out) {
+  __shared__ uint64_t acc[kRotOT][2][kRotX];
+  const int n = 1 << logn;
+  const int tid = threadIdx.x, x = blockIdx.x * kRotX + tid;
+  const int tile = blockIdx.y, o0 = tile * kRotOT;
+  const int g0 = blockIdx.z * gchunk, g1 = min(G, g0 + gchunk);
+#pragma unroll
+  for (int o = 0; o < kRotOT; ++o) acc[o][0][tid] = acc[o][1][tid] = 0;
+  const uint64_t q = m.q;
+  const int* offs = toff + (size_t)tile * (G + 1);
+  for (int g = g0; g < g1; ++g) {
+    const int t0 = __ldg(&offs[g]), t1 = __ldg(&offs[g + 1]);
+    if (t0 == t1) continue;  // no output of this tile uses the rotation (block-uniform)
+    const int2 gi = __ldg(&groups[g]);
+    const uint64_t* c = C + (size_t)gi.x * 2 * n;
+    uint64_t r0, r1;
+    if (gi.y < 0) {  // step 0: the ciphertext itself
+      r0 = c[x];
+      r1 = c[n + x];
+    } else {
+      // eval_perm (ring.py:199-202): exp_at_index[x] = 2 bitrev(x) + 1
+      const uint64_t gp = __ldg(&gpow[g]) % (2ull * n);
+      const uint32_t e = 2u * brev_bits((uint32_t)x, logn) + 1u;
+      const uint32_t e2 = (uint32_t)(((uint64_t)e * gp) % (2ull * n));
+      const int src = (int)brev_bits((e2 - 1u) >> 1, logn);
+      const uint64_t* dg = D + (size_t)gi.x * ndig * n;
+      const uint64_t* kk = K + (size_t)gi.y * ndig * 2 * n;
+      uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+#pragma unroll 4
+      for (int i = 0; i < ndig; ++i) {
+        const uint64_t dv = __ldg(&dg[(size_t)i * n + src]);
+        mac128(a0l, a0h, dv, __ldg(&kk[((size_t)i * 2) * n + x]));
+        mac128(a1l, a1h, dv, __ldg(&kk[((size_t)i * 2 + 1) * n + x]));
+      }
+      r0 = csub(redc(a0l, a0h, m) + c[src], q);  // ndig q^2 < q 2^64: one REDC each
+      r1 = redc(a1l, a1h, m);
+    }
+    for (int t = t0; t < t1; ++t) {
+      const int2 tm = __ldg(&terms[t]);  // (output within the tile, plaintext row)
+      const uint64_t w = __ldg(&PT[(size_t)tm.y * n + x]);  // Montgomery form: redc(r w) = r w_plain
+      acc[tm.x][0][tid] = csub(acc[tm.x][0][tid] + redc(r0 * w, __umul64hi(r0, w), m), q);
+      acc[tm.x][1][tid] = csub(acc[tm.x][1][tid] + redc(r1 * w, __umul64hi(r1, w), m), q);
+    }
+  }
+  uint64_t* dst = out + (size_t)blockIdx.z * n_out * 2 * n;
+  for (int o = 0; o < kRotOT && o0 + o < n_out; ++o) {
+    dst[((size_t)(o0 + o) * 2) * n + x] = acc[o][0][tid];
+    dst[((size_t)(o0 + o) * 2 + 1) * n + x] = acc[o][1][tid];
+  }
+}
+
+// out = Σ_z part[z] mod q (partial sums of the group chunks)
+__global__ void rot_pmac_reduce_kernel(uint64_t q, int Z, int64_t total, const uint64_t* __restrict__ part,
+                                       uint64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  uint64_t s = 0;
+  for (int z = 0; z < Z; ++z) s = csub(s + part[(size_t)z * total + i], q);
+  out[i] = s;
+}
+
 }  // namespace fhe
 
 using namespace fhe;
@@ -604,6 +683,37 @@ int fhe_pmac(uint64_t q, int n, const uint64_t* R, const uint64_t* pt_mont, cons
   pmac_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(ms.m[0], n, R, pt_mont, term_off,
                                                        reinterpret_cast<const int2*>(terms), out);
   FHE_CHECK_LAUNCH("pmac_kernel");
+  return FHE_OK;
+}
+
+int fhe_rot_pmac(uint64_t q, int n, int ndig, const uint64_t* C, const uint64_t* D, const uint64_t* K_mont,
+                 int G, const int32_t* groups, const uint64_t* gpow, int n_out, const int32_t* tile_off,
+                 const int32_t* terms, const uint64_t* pt_mont, int gchunks, uint64_t* partial, uint64_t* out,
+                 void* stream) {
+  ModSet ms;
+  if (int rc = make_modset(&q, 1, &ms)) return rc;
+  if (n < kRotX || (n & (n - 1)) || ndig < 1 || ndig > kRotMaxDig || G < 0 || n_out < 0 || gchunks < 1)
+    return fail(FHE_ERR_VALUE, "bad rot_pmac geometry");
+  if ((u128_t)ndig * q >= ((u128_t)1 << 64)) return fail(FHE_ERR_PARAMETER, "too many digits for one lazy REDC");
+  if (!n_out) return FHE_OK;
+  if (!C || !groups || !gpow || !tile_off || !terms || !pt_mont || !out || (G && (!D || !K_mont)))
+    return fail(FHE_ERR_VALUE, "null rot_pmac operand");
+  if (gchunks > 1 && !partial) return fail(FHE_ERR_VALUE, "rot_pmac with group chunks needs a partial buffer");
+  const int tiles = (n_out + kRotOT - 1) / kRotOT;
+  const int gchunk = G ? (G + gchunks - 1) / gchunks : 1;
+  const int Z = G ? (G + gchunk - 1) / gchunk : 1;
+  dim3 grid(n / kRotX, tiles, Z);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint64_t* dst = Z > 1 ? partial : out;
+  rot_pmac_kernel<<<grid, kRotX, 0, st>>>(ms.m[0], log2i(n), ndig, G, n_out, gchunk, C, D, K_mont,
+                                          reinterpret_cast<const int2*>(groups), gpow, tile_off,
+                                          reinterpret_cast<const int2*>(terms), pt_mont, dst);
+  FHE_CHECK_LAUNCH("rot_pmac_kernel");
+  if (Z > 1) {
+    const int64_t total = (int64_t)n_out * 2 * n;
+    rot_pmac_reduce_kernel<<<grid_for(total), kThreads, 0, st>>>(q, Z, total, partial, out);
+    FHE_CHECK_LAUNCH("rot_pmac_reduce_kernel");
+  }
   return FHE_OK;
 }
 

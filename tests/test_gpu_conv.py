@@ -349,3 +349,31 @@ def test_avg_pool_separable_matches_oracle(h, k, c):
     pooled = conv.avg_pool(conv.PackedTensor(_cts(arr), lay, c), k, P)
     assert pooled.layout.stride == k
     assert np.array_equal(_out(pooled.cts), O.avg_pool(arr, k, lay.w_p, Q))
+
+
+@pytest.mark.parametrize("H,c_i,c_o", [(16, 8, 20), (32, 3, 17), (8, 24, 24)])
+def test_conv_conventional_fused_matches_materialized(monkeypatch, H, c_i, c_o):
+    """The fused rotate-multiply-accumulate pass (fhe_rot_pmac, rotations never
+    written) gives exactly the two-kernel ciphertexts (batched K4 rotations +
+    fhe_pmac) — packed layouts with column swaps, fragmented layouts, more
+    than one 16-output tile — and decrypts to the plain convolution."""
+    from paper_2401_16732_b200 import bfv, conv
+
+    P = _P()
+    r = np.random.default_rng(H * 100 + c_o)
+    sk = bfv.keygen(P, r)
+    x = r.integers(0, 4, (c_i, H, H), dtype=np.int64)
+    w = r.integers(-3, 4, (c_o, c_i, 3, 3), dtype=np.int64)
+    spec = conv.ConvLayerSpec(H, H, 3, c_i, c_o, w)
+    swk = bfv.gen_switching_keys(sk, conv.conventional_steps(spec, P), r, decomp_log=conv.CONV_DECOMP_LOG)
+    xb = conv.pack_input(x, P, 3, lambda pt: bfv.encrypt_private(pt, sk, r), batch=True)
+    fused = _out(conv.conv_conventional(xb, spec, swk, P).cts)
+    monkeypatch.setenv("FLASHHE_CONVENTIONAL", "materialized")
+    mat = conv.conv_conventional(xb, spec, swk, P)
+    assert np.array_equal(fused, _out(mat.cts))
+    pad = np.pad(x, ((0, 0), (1, 1), (1, 1)))
+    want = np.zeros((c_o, H, H), dtype=np.int64)
+    for dy in range(3):
+        for dx in range(3):
+            want += np.einsum("oi,ihw->ohw", w[:, :, dy, dx], pad[:, dy : dy + H, dx : dx + H])
+    assert np.array_equal(conv.unpack(mat, sk), bfv.centered(want, P.p))

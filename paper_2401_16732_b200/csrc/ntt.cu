@@ -442,6 +442,53 @@ static void launch_split_k(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, 
   ntt_split_kernel<LOGR, INV, COLS, MINB, LG><<<grid, threads, smem, st>>>(ls, lm, dst, a, b, from_src, final_);
 }
 
+// One CTA per row for 2^LOGN <= 4096 with the split kernels' compile-time
+// phase geometry (the whole row is one "block": O = n, v = 0): one item per
+// thread per phase, element slots and twiddle indices as base + constant.
+template <bool INV, int LOGN>
+__global__ void __launch_bounds__((1 << LOGN) / 16) ntt_row_kernel(const LimbSet ls, const LoadMap lm,
+                                                                   uint64_t* __restrict__ dst) {
+  extern __shared__ uint64_t sm[];
+  constexpr int n = 1 << LOGN;
+  const int row = blockIdx.x;
+  const NttDesc d = ls.d[(row / lm.G) % ls.L];
+  const int tid = threadIdx.x;
+  const uint64_t* srow;
+  int shift = 0;
+  if (lm.ndig > 0) {
+    srow = lm.src + (size_t)(row / lm.ndig) * n;
+    shift = lm.T * (row % lm.ndig);
+  } else {
+    srow = lm.src + (size_t)row * n;
+  }
+  const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(srow);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // n/2 pairs over n/16 threads
+    const int i = tid + k * (n / 16);
+    ulonglong2 v = s2[i];
+    if (lm.ndig > 0) {
+      v.x = (v.x >> shift) & lm.mask;
+      v.y = (v.y >> shift) & lm.mask;
+    }
+    sm[spad(2 * i)] = v.x;
+    sm[spad(2 * i + 1)] = v.y;
+  }
+  __syncthreads();
+  split_sub<4, INV, false, LOGN>(sm, 0, tid, d, (uint32_t)n, INV);
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + (size_t)row * n);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = tid + k * (n / 16);
+    uint64_t x = sm[spad(2 * i)], y = sm[spad(2 * i + 1)];
+    if (!INV) {
+      x = x >= q2 ? x - q2 : x;
+      y = y >= q2 ? y - q2 : y;
+    }
+    d2[i] = make_ulonglong2(csub(x, q), csub(y, q));
+  }
+}
+
 template <int LOGR, bool INV, bool COLS>
 static int launch_split_one(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int a, int b,
                             int from_src, int final_, cudaStream_t st) {
@@ -518,6 +565,15 @@ static int launch(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows,
   int logn = 0;
   while ((1 << logn) < n) ++logn;
   if (logn >= kSplitMinLog && split_enabled()) return launch_split<INV>(ls, lm, dst, rows, logn, st);
+  if ((logn == 11 || logn == 12) && split_enabled()) {  // FHE_NTT_SPLIT=0 also selects the generic row kernel
+    const size_t smem = (size_t)(n + (n >> 4) + 1) * sizeof(uint64_t);
+    if (logn == 11)
+      ntt_row_kernel<INV, 11><<<rows, n / 16, smem, st>>>(ls, lm, dst);
+    else
+      ntt_row_kernel<INV, 12><<<rows, n / 16, smem, st>>>(ls, lm, dst);
+    FHE_CHECK_LAUNCH("ntt_row_kernel");
+    return FHE_OK;
+  }
   switch (logn < 4 ? logn : 4) {
     case 1: return launch_t<1, INV>(ls, lm, dst, rows, n, st);
     case 2: return launch_t<2, INV>(ls, lm, dst, rows, n, st);

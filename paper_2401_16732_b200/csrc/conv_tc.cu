@@ -755,10 +755,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
                 for (int j = 0; j < 4; ++j)
                   if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
               }
+#ifdef TC_PROBE_NOSTORE  // timing probe only: results reduced but not stored
+              if (o < d.c_o && (r[0] ^ r[1] ^ r[2] ^ r[3]) == 0x5eed5eedull) orow[0] = 1;
+#else
               if (o < d.c_o)  // one 32-byte store per lane: a full sector (STG.256)
                 asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(orow + 4 * k), "l"(r[0]), "l"(r[1]),
                              "l"(r[2]), "l"(r[3])
                              : "memory");
+#endif
             }
           }
           asm volatile("tcgen05.fence::before_thread_sync;");

@@ -316,7 +316,37 @@ def sub_benchmarks(steps, warmup, hbm):
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
     res["pool_fc_tail"] = pool_fc_tail(steps, warmup)
+    res["inference_chain"] = {name: inference_chain(name) for name in ("config3", "config4")}
     return res
+
+
+def inference_chain(name):
+    """Configs 3 / 4 end to end (inference.he_forward): the main path's convs,
+    x²+x share rounds with the client repack, pool and FC, both parties
+    in-process; decrypted logits checked against the integer model. One run
+    after a warm-up run; wall-clock split into conv, activation rounds,
+    offline mask/zero preparation and the pool/FC/decrypt tail."""
+    from paper_2401_16732_b200 import bfv, inference, params
+
+    P = params.default_params()
+    layers = inference.config_layers(name)
+    convs, _, fc = inference.main_path(layers)
+    out = {}
+    rng = np.random.default_rng(77)
+    weights = inference.random_weights(layers, rng)
+    specs = inference.layer_specs(layers, weights)  # K1 plans cached on the specs after the first run
+    for it in range(2):
+        rng = np.random.default_rng(78 + it)
+        sk = bfv.keygen(P, rng)
+        x = rng.integers(0, 8, (convs[0].c_i, convs[0].H, convs[0].W), dtype=np.int64)
+        t = {}
+        got = inference.he_forward(layers, x, weights, sk, rng, P, timings=t, specs=specs)
+        ok = bool(np.array_equal(got, inference.plain_forward(layers, x, weights, P.p)))
+        out = {"convs": len(convs), "logits": int(fc.c_o), "bit_exact_vs_integer_model": ok,
+               **{k: round(v * 1e3, 2) for k, v in t.items()}}
+        out = {k.replace("_s", "_ms") if k.endswith("_s") else k: v for k, v in out.items()}
+    out["online_ms"] = round(out["conv_ms"] + out["act_ms"] + out["tail_ms"], 2)
+    return out
 
 
 def pool_fc_tail(steps, warmup):

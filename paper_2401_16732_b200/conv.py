@@ -541,8 +541,12 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     need = max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0)
     if need:
         device.scratch("conv_tc_x", -(-need // 256) * 256)
+    # all of the call's host outputs in one pinned allocation (one allocator call, not one per job)
+    sizes = [plan.n_out * 2 * params.n for *_, plan in meta]
+    host_all = torch.empty(sum(sizes), dtype=torch.int64, pin_memory=True)
+    views = torch.split(host_all, sizes)
     outs = []
-    for x, layer, plan in meta:  # one pass: job i's download is enqueued before job i+1's upload
+    for (x, layer, plan), hv in zip(meta, views):  # one pass: job i's download is enqueued before job i+1's upload
         ready = None
         if isinstance(x.cts, bfv.CtStack):
             inp, ready = x.cts.rows.upload_on(up)
@@ -553,7 +557,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
         (ev,) = issue_k1([(plan, inp, ready, out)])
         inp.record_stream(comp)
         down.wait_event(ev)
-        rows = device.DeviceRows.download_on(out, down)
+        rows = device.DeviceRows.download_on(out, down, into=hv)
         cts = bfv.CtStack(rows, params.q, Encoding.DIRECT, Domain.COEFF)
         outs.append(PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale))
     down.synchronize()

@@ -160,12 +160,14 @@ class DeviceRows:
         return self._dev, ev
 
     @classmethod
-    def download_on(cls, dev: torch.Tensor, stream: torch.cuda.Stream) -> "DeviceRows":
+    def download_on(cls, dev: torch.Tensor, stream: torch.cuda.Stream, into: torch.Tensor | None = None) -> "DeviceRows":
         """Rows whose host copy is filled by a pinned D2H enqueued on `stream`
         (the caller orders `stream` after the producer and synchronizes it
-        before reading the host side)."""
+        before reading the host side). `into`: a pinned host slice of the
+        same size to fill (callers batching several downloads into one
+        pinned allocation)."""
         dev = dev.reshape(-1, dev.shape[-1])
-        t = torch.empty(dev.shape, dtype=torch.int64, pin_memory=True)
+        t = torch.empty(dev.shape, dtype=torch.int64, pin_memory=True) if into is None else into.view(dev.shape)
         with torch.cuda.stream(stream):
             t.copy_(dev, non_blocking=True)
         dev.record_stream(stream)

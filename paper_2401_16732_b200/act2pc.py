@@ -299,22 +299,33 @@ def server_round1_layer(conv_out, session: LayerSession, params: RingParams) -> 
     return msg
 
 
-def _decrypt_rows_checked(rows: torch.Tensor, domain, sk: bfv.SecretKey) -> torch.Tensor:
+def _check_budget_rows(params: RingParams, maxw: torch.Tensor):
+    if maxw.numel() and bfv._budget(params, int(maxw.max().item())) <= 0:
+        raise ProtocolError("noise budget exhausted: ciphertext no longer decrypts reliably")
+
+
+def _decrypt_rows_checked(rows: torch.Tensor, domain, sk: bfv.SecretKey, pending: list | None = None) -> torch.Tensor:
+    """Decrypt a layer's messages; the noise-budget check runs now (one host
+    sync) or, with `pending`, is queued for the caller to run once at the end
+    of the exchange (run_layer_activation: no sync between the rounds)."""
     params = sk.params
     cts = bfv.cts_from_rows(rows, params.q, Encoding.DIRECT, domain)
-    m, maxw = bfv.decrypt_rows(cts, sk)
-    if len(maxw) and bfv._budget(params, int(maxw.max())) <= 0:
-        raise ProtocolError("noise budget exhausted: ciphertext no longer decrypts reliably")
+    m, maxw = bfv.decrypt_rows_dev(cts, sk)
+    if pending is None:
+        _check_budget_rows(params, maxw)
+    else:
+        pending.append(maxw)
     return m
 
 
 def client_round1_layer(msg: torch.Tensor, plan: RepackPlan, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
-                        codec: FixedPointCodec | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+                        codec: FixedPointCodec | None = None, pending: list | None = None
+                        ) -> tuple[torch.Tensor, torch.Tensor]:
     """Decrypt w = a + r, repack into the next layout (w'), return
     (⟦w'² + w'·2^f⟧ direct, ⟦w'⟧ batch) — one pass per step for the layer."""
     params = sk.params
     f = codec.frac_bits if codec else 0
-    w = _decrypt_rows_checked(msg, Domain.COEFF, sk)
+    w = _decrypt_rows_checked(msg, Domain.COEFF, sk, pending)
     z = zeros.take_rows(2 * plan.k_dst)
     ct_sq = _encrypt_rows(z[: plan.k_dst], _gather(plan.idx, w), params, square=True, f=f)
     coeffs = _batch_coeffs(_gather(plan.idx_eval, w), params)
@@ -340,11 +351,11 @@ def server_round2_layer(msgs: tuple[torch.Tensor, torch.Tensor], session: LayerS
 
 
 def client_round2_layer(msg: torch.Tensor, plan: RepackPlan, sk: bfv.SecretKey,
-                        zeros: bfv.ZeroRowPool) -> torch.Tensor:
+                        zeros: bfv.ZeroRowPool, pending: list | None = None) -> torch.Tensor:
     """Decrypt the batch messages, re-encrypt their slots direct (decode_batch
     as NTT mod p + slot gather fused into the encryption pass)."""
     params = sk.params
-    m = _decrypt_rows_checked(msg, Domain.EVAL, sk)
+    m = _decrypt_rows_checked(msg, Domain.EVAL, sk, pending)
     evals = ring.ntt_rows(m, params.n, [params.p])
     return _encrypt_rows(zeros.take_rows(plan.k_dst), evals, params, perm=plan.slot)
 
@@ -369,8 +380,11 @@ def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zer
                          params: RingParams):
     """Both parties in-process: one layer's full two-round exchange."""
     plan = session.plan
+    pending: list = []  # the client's noise-budget checks, run once after the exchange (one host sync)
     m1 = server_round1_layer(conv_out, session, params)
-    sq, w = client_round1_layer(m1, plan, sk, zeros, session.codec)
+    sq, w = client_round1_layer(m1, plan, sk, zeros, session.codec, pending)
     m2 = server_round2_layer((sq, w), session, params)
-    back = client_round2_layer(m2, plan, sk, zeros)
-    return server_finalize_layer(sq, back, session, params, getattr(conv_out, "scale", 0))
+    back = client_round2_layer(m2, plan, sk, zeros, pending)
+    out = server_finalize_layer(sq, back, session, params, getattr(conv_out, "scale", 0))
+    _check_budget_rows(params, torch.cat(pending))
+    return out

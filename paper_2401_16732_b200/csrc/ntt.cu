@@ -593,7 +593,9 @@ int fhe_ntt_forward(const fhe_plan* const* plans, int L, int B, int P, const uin
   LimbSet ls;
   int n;
   if (int rc = build_limbset(plans, L, &ls, &n)) return rc;
-  if (B < 0 || P < 1 || !src || !dst) return fail(FHE_ERR_VALUE, "bad batch arguments");
+  if (B < 0 || P < 1) return fail(FHE_ERR_VALUE, "bad batch arguments");
+  if (!B) return FHE_OK;  // empty batch: nothing to transform
+  if (!src || !dst) return fail(FHE_ERR_VALUE, "null NTT buffer");
   LoadMap lm{src, P, 0, 0, 0, ~0ull};
   return launch<false>(ls, lm, dst, B * L * P, n, (cudaStream_t)stream);
 }
@@ -603,7 +605,9 @@ int fhe_ntt_inverse(const fhe_plan* const* plans, int L, int B, int P, const uin
   LimbSet ls;
   int n;
   if (int rc = build_limbset(plans, L, &ls, &n)) return rc;
-  if (B < 0 || P < 1 || !src || !dst) return fail(FHE_ERR_VALUE, "bad batch arguments");
+  if (B < 0 || P < 1) return fail(FHE_ERR_VALUE, "bad batch arguments");
+  if (!B) return FHE_OK;  // empty batch: nothing to transform
+  if (!src || !dst) return fail(FHE_ERR_VALUE, "null NTT buffer");
   LoadMap lm{src, P, 0, 0, 0, ~0ull};
   return launch<true>(ls, lm, dst, B * L * P, n, (cudaStream_t)stream);
 }
@@ -613,8 +617,9 @@ int fhe_ntt_forward_digits(const fhe_plan* const* plans, int L, int B, const uin
   LimbSet ls;
   int n;
   if (int rc = build_limbset(plans, L, &ls, &n)) return rc;
-  if (B < 0 || ndig < 1 || T < 1 || T > 63 || !src || !dst)
-    return fail(FHE_ERR_VALUE, "bad digit arguments");
+  if (B < 0 || ndig < 1 || T < 1 || T > 63) return fail(FHE_ERR_VALUE, "bad digit arguments");
+  if (!B) return FHE_OK;
+  if (!src || !dst) return fail(FHE_ERR_VALUE, "null digit buffer");
   if (src == dst) return fail(FHE_ERR_VALUE, "digit NTT cannot run in place");
   LoadMap lm{src, ndig, ndig, T, 0, (1ull << T) - 1};
   return launch<false>(ls, lm, dst, B * L * ndig, n, (cudaStream_t)stream);

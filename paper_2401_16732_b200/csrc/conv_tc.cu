@@ -698,20 +698,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
     uint32_t use = 0;  // per-buffer use parity (mirrors the MMA thread)
     for (int l = 0; l < nl; ++l) {
       const LayerDesc& d = A.L[l];
+      // per-layer values in registers (the store asm below clobbers memory:
+      // fields read through `d` in the chunk loop were re-fetched from the
+      // parameter bank every chunk)
+      const int c_o = d.c_o, F = d.F, npos = d.npos, nacc = d.nacc;
+      uint64_t* const dout = d.out;
+      const uint8_t* const bmask = d.bmask;
+      const uint64_t* const bias = d.bias;
       for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
         const Tile T = tile_of(t, d, n);
         const int o = T.ob * kOcTile + quad * 32 + lane;
-        const bool active = T.ob * kOcTile + quad * 32 < d.c_o;  // warp-uniform
-        const uint64_t bd = (active && T.p == 0 && d.bias && o < d.c_o) ? d.bias[o] : 0;
-        for (int a = 0; a < d.nacc; ++a) {
+        const bool active = T.ob * kOcTile + quad * 32 < c_o;  // warp-uniform
+        const uint64_t bd = (active && T.p == 0 && bias && o < c_o) ? bias[o] : 0;
+        for (int a = 0; a < nacc; ++a) {
           int buf;
-          if (d.nacc == 1) {
+          if (nacc == 1) {
             buf = nb;
             nb ^= 1;
           } else {
             buf = a;
           }
-          const int s0 = T.s0 + a * d.npos;
+          const int s0 = T.s0 + a * npos;
           mbar_wait_sleep(tfull_bar(buf), (use >> buf) & 1, 64);
           use ^= 1u << buf;
           if (lane == 0 && warp == 2) TC_TRACE(5, tl);
@@ -726,10 +733,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             // hi = q + Σ_{d>=4} 2^(8(d-4)) P_d lie in (0, 2q) (|P_d| < 2^31,
             // q > 2^56); V = lo + 2^32 hi.
             const uint32_t acc = tmem + buf * kAccCols + ((uint32_t)(quad * 32) << 16);
-            uint64_t* orow = d.out + ((size_t)(o * d.F + T.f) * 2 + T.p) * n + s0;
+            uint64_t* orow = dout + ((size_t)(o * F + T.f) * 2 + T.p) * n + s0;
             // each warp of the quadrant takes a contiguous half of the chunks: a
             // lane then writes whole 128-byte lines of its channel row
-            const int kper = d.npos / 4 / (kEpiWarps / 4);
+            const int kper = npos / 4 / (kEpiWarps / 4);
 #pragma unroll 1
             for (int k = sub * kper; k < (sub + 1) * kper; ++k) {
               uint32_t v[32];
@@ -750,15 +757,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
                 r[j] = val >= q ? val - q : val;
               }
               if (bd) {
-                const uint32_t mk = *reinterpret_cast<const uint32_t*>(d.bmask + (size_t)T.f * n + s0 + 4 * k);
+                const uint32_t mk = *reinterpret_cast<const uint32_t*>(bmask + (size_t)T.f * n + s0 + 4 * k);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                   if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
               }
 #ifdef TC_PROBE_NOSTORE  // timing probe only: results reduced but not stored
-              if (o < d.c_o && (r[0] ^ r[1] ^ r[2] ^ r[3]) == 0x5eed5eedull) orow[0] = 1;
+              if (o < c_o && (r[0] ^ r[1] ^ r[2] ^ r[3]) == 0x5eed5eedull) orow[0] = 1;
 #else
-              if (o < d.c_o)  // one 32-byte store per lane: a full sector (STG.256)
+              if (o < c_o)  // one 32-byte store per lane: a full sector (STG.256)
                 asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(orow + 4 * k), "l"(r[0]), "l"(r[1]),
                              "l"(r[2]), "l"(r[3])
                              : "memory");

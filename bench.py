@@ -316,21 +316,22 @@ def sub_benchmarks(steps, warmup, hbm):
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
     res["pool_fc_tail"] = pool_fc_tail(steps, warmup)
-    res["inference_chain"] = {name: inference_chain(name) for name in ("config3", "config4")}
+    res["inference_chain"] = {name: inference_chain(name) for name in ("config3", "config4", "config5")}
     return res
 
 
 def inference_chain(name):
-    """Configs 3 / 4 end to end (inference.he_forward): the main path's convs,
-    x²+x share rounds with the client repack, pool and FC, both parties
+    """Configs 3 / 4 / 5 end to end (inference.he_forward): the main path's
+    convs, x²+x share rounds with the client repack, pools (config 5: the
+    post-stem 2x2 pool with one masked repack round) and FC, both parties
     in-process; decrypted logits checked against the integer model. One run
     after a warm-up run; wall-clock split into conv, activation rounds,
-    offline mask/zero preparation and the pool/FC/decrypt tail."""
+    repack rounds, offline mask/zero preparation and the pool/FC/decrypt tail."""
     from paper_2401_16732_b200 import bfv, inference, params
 
     P = params.default_params()
     layers = inference.config_layers(name)
-    convs, _, fc = inference.main_path(layers)
+    convs, _, fc = inference._convs(layers), None, inference.main_path(layers)[2]
     out = {}
     rng = np.random.default_rng(77)
     weights = inference.random_weights(layers, rng)
@@ -345,7 +346,7 @@ def inference_chain(name):
         out = {"convs": len(convs), "logits": int(fc.c_o), "bit_exact_vs_integer_model": ok,
                **{k: round(v * 1e3, 2) for k, v in t.items()}}
         out = {k.replace("_s", "_ms") if k.endswith("_s") else k: v for k, v in out.items()}
-    out["online_ms"] = round(out["conv_ms"] + out["act_ms"] + out["tail_ms"], 2)
+    out["online_ms"] = round(out["conv_ms"] + out["act_ms"] + out["repack_ms"] + out["tail_ms"], 2)
     return out
 
 

@@ -388,3 +388,49 @@ def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zer
     out = server_finalize_layer(sq, back, session, params, getattr(conv_out, "scale", 0))
     _check_budget_rows(params, torch.cat(pending))
     return out
+
+
+# ---------------------------------------------------------------------------
+# A masked repack round: the layout change without the activation, for a
+# pending stride that a server-side linear layer leaves before the next conv
+# (config 5's 2x2 average pool after the stem). An addition beyond the paper,
+# in the manner of SPEC's rescale_round: the server masks
+# ⟦a⟧ with r, the client decrypts a + r, repacks it and re-encrypts it
+# (direct), the server removes the repacked mask r'. One round trip, two
+# messages, the client sees only a + r.
+
+
+@dataclass
+class RepackSession:
+    plan: RepackPlan
+    r: torch.Tensor  # [k_src, n] masks mod p over the source slots (server-private)
+    neg_r_dst: torch.Tensor  # [k_dst, n] (−r') mod p in the next layout
+    round: Round = Round.INIT
+
+
+def offline_prepare_repack(plan: RepackPlan, params: RingParams, rng) -> RepackSession:
+    r = rng.integers(0, params.p, (plan.k_src, params.n), dtype=np.int64)
+    neg = (-plan.gather_host(r)) % params.p
+    return RepackSession(plan, device.to_device(r), device.to_device(neg))
+
+
+def run_repack_round(x, session: RepackSession, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
+                     params: RingParams):
+    """⟦a⟧ (any direct layout, stride pending) -> ⟦a'⟧ packed for the next conv."""
+    from . import conv
+
+    _expect(session, Round.INIT)
+    plan = session.plan
+    cts = x.cts if hasattr(x, "cts") else x
+    if len(cts) != plan.k_src:
+        raise EncodingError("tensor does not match the repack session's layout")
+    masked = _encrypt_rows(bfv.cts_rows(cts), session.r, params)  # server: ⟦a + r⟧
+    session.round = Round.MASKED
+    pending: list = []
+    w = _decrypt_rows_checked(masked, Domain.COEFF, sk, pending)  # client: a + r, repacked, re-encrypted
+    back = _encrypt_rows(zeros.take_rows(plan.k_dst), _gather(plan.idx, w), params)
+    out = _encrypt_rows(back, session.neg_r_dst, params)  # server: ⟦a' + r'⟧ − r' (plain_add of −r')
+    session.round = Round.DONE
+    _check_budget_rows(params, torch.cat(pending))
+    cts_out = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+    return conv.PackedTensor(cts_out, plan.dst, plan.channels, getattr(x, "scale", 0))

@@ -1,4 +1,4 @@
-"""Configs 3 and 4 end to end on the device — the caller of the hot path.
+"""Configs 3, 4 and 5 end to end on the device — the caller of the hot path.
 
 The conv stack of `stacks.py` run as a chain, both parties in-process:
 Flash conv (K1, conv.conv_proposed) -> x²+x on shares with the client's
@@ -7,9 +7,9 @@ conv.py:162-197; strided convs are subsampled there) -> ... -> avg_pool ->
 fully_connected -> decrypt. The reference has no model module (SPEC's absent
 `model` lists ResidualAdd), so shortcut projections and residual additions
 are not modelled: the chain is the ResNet's main path. Config 5's 2x2 pool
-after the stem would need a server-side repack between two linear layers and
-is not covered. The integer model `plain_forward` is the parity reference:
-decrypted logits equal it mod p.
+after the stem is evaluated by the server and its stride applied by one
+masked repack round (act2pc.run_repack_round). The integer model
+`plain_forward` is the parity reference: decrypted logits equal it mod p.
 """
 
 from __future__ import annotations
@@ -23,16 +23,22 @@ from .params import RingParams
 
 
 def main_path(layers):
-    """The convs of the ResNet main path (no projections), the final pool and FC."""
-    convs = [l for l in layers if l.kind == "conv" and not l.name.endswith("proj")]
+    """The ResNet main path in order (convs without projections, any pool
+    between convs, the final pool and FC) and the final pool / FC layers."""
+    seq = [l for l in layers if not (l.kind == "conv" and l.name.endswith("proj"))]
     pool = next(l for l in layers if l.kind == "pool" and l.name == "avgpool")
     fc = next(l for l in layers if l.kind == "fc")
-    return convs, pool, fc
+    return seq, pool, fc
+
+
+def _convs(layers):
+    return [l for l in main_path(layers)[0] if l.kind == "conv"]
 
 
 def random_weights(layers, rng, bound: int = 127) -> dict:
-    convs, pool, fc = main_path(layers)
-    w = {l.name: rng.integers(-bound, bound + 1, (l.c_o, l.c_i, l.f_w, l.f_w), dtype=np.int64) for l in convs}
+    _, _, fc = main_path(layers)
+    w = {l.name: rng.integers(-bound, bound + 1, (l.c_o, l.c_i, l.f_w, l.f_w), dtype=np.int64)
+         for l in _convs(layers)}
     w["fc"] = rng.integers(-bound, bound + 1, (fc.c_o, fc.c_i), dtype=np.int64)
     return w
 
@@ -51,63 +57,89 @@ def _conv_same(a: np.ndarray, w: np.ndarray) -> np.ndarray:
 
 
 def plain_forward(layers, x: np.ndarray, weights: dict, p: int, frac_bits: int = 0) -> np.ndarray:
-    """Integer model mod p: conv, stride subsample, a² + a·2^f, window sum, FC."""
-    convs, pool, fc = main_path(layers)
+    """Integer model mod p: conv, stride subsample, a² + a·2^f, window sums
+    (pools: sum of each k x k block), FC."""
+    seq, pool, fc = main_path(layers)
     a = np.asarray(x, dtype=np.int64) % p
-    for l in convs:
-        a = _conv_same(a, weights[l.name]) % p
-        a = a[:, :: l.stride, :: l.stride]
-        a = (a * a + a * (1 << frac_bits)) % p
-    pooled = a.reshape(a.shape[0], -1).sum(axis=1) % p
-    return (weights["fc"] @ pooled) % p
+    for l in seq:
+        if l.kind == "conv":
+            a = _conv_same(a, weights[l.name]) % p
+            a = a[:, :: l.stride, :: l.stride]
+            a = (a * a + a * (1 << frac_bits)) % p
+        elif l.kind == "pool":
+            k = l.f_w
+            c, h, w = a.shape
+            a = a.reshape(c, h // k, k, w // k, k).sum(axis=(2, 4)) % p
+    return (weights["fc"] @ a.reshape(a.shape[0])) % p
 
 
 def layer_specs(layers, weights: dict) -> dict:
     """ConvLayerSpec per main-path conv (they cache their K1 plans: build once, reuse)."""
-    convs, _, _ = main_path(layers)
-    return {l.name: conv.ConvLayerSpec(l.H, l.W, l.f_w, l.c_i, l.c_o, weights[l.name]) for l in convs}
+    return {l.name: conv.ConvLayerSpec(l.H, l.W, l.f_w, l.c_i, l.c_o, weights[l.name]) for l in _convs(layers)}
 
 
 def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, params: RingParams,
                frac_bits: int = 0, timings: dict | None = None, specs: dict | None = None) -> np.ndarray:
-    """The encrypted chain on the device; returns the decrypted logits mod p."""
+    """The encrypted chain on the device; returns the decrypted logits mod p.
+
+    conv -> x²+x layer exchange repacking into the next operation's layout
+    (the next conv's input layout, or a pad-1 layout for a pool); a pool
+    between convs (config 5) is evaluated by the server and its stride applied
+    by a masked repack round (act2pc.run_repack_round) before the next conv."""
     import time
 
     import torch
 
     P = params
-    convs, pool, fc = main_path(layers)
+    seq, pool, fc = main_path(layers)
     specs = specs if specs is not None else layer_specs(layers, weights)
-    t_conv = t_act = t_off = 0.0
-    cur = conv.pack_input(x, P, convs[0].f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
-    for i, l in enumerate(convs):
-        spec = specs[l.name]
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        y = conv.conv_proposed(cur, spec, P)
-        torch.cuda.synchronize()
-        t_conv += time.perf_counter() - t0
-        if l.stride > 1:  # subsampled by the client's repack below
-            y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
-        h = l.H // l.stride
-        nxt = convs[i + 1].f_w if i + 1 < len(convs) else 3
-        t0 = time.perf_counter()
-        plan = act2pc.RepackPlan(y.layout, l.c_o, conv.layout_direct(P, h, h, nxt), P)
-        sess = act2pc.offline_prepare_layer(plan, P, rng, frac_bits=frac_bits)
-        zeros = bfv.precompute_zero_rows(sk, rng, 3 * plan.k_dst)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        cur = act2pc.run_layer_activation(y, sess, sk, zeros, P)
-        torch.cuda.synchronize()
-        t_off += t1 - t0
-        t_act += time.perf_counter() - t1
+    t = dict(conv_s=0.0, act_s=0.0, offline_s=0.0, repack_s=0.0)
+    first = seq[0]
+    cur = conv.pack_input(x, P, first.f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
+
+    def next_layout(i, h):
+        nxt = seq[i + 1]
+        return conv.layout_direct(P, h, h, nxt.f_w if nxt.kind == "conv" else 3)
+
+    for i, l in enumerate(seq):
+        if l.kind == "conv":
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            y = conv.conv_proposed(cur, specs[l.name], P)
+            torch.cuda.synchronize()
+            t["conv_s"] += time.perf_counter() - t0
+            if l.stride > 1:  # subsampled by the client's repack below
+                y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
+            t0 = time.perf_counter()
+            plan = act2pc.RepackPlan(y.layout, l.c_o, next_layout(i, l.H // l.stride), P)
+            sess = act2pc.offline_prepare_layer(plan, P, rng, frac_bits=frac_bits)
+            zeros = bfv.precompute_zero_rows(sk, rng, 3 * plan.k_dst)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            cur = act2pc.run_layer_activation(y, sess, sk, zeros, P)
+            torch.cuda.synchronize()
+            t["offline_s"] += t1 - t0
+            t["act_s"] += time.perf_counter() - t1
+        elif l.kind == "pool" and l is not pool:
+            t0 = time.perf_counter()
+            pooled = conv.avg_pool(cur, l.f_w, P)
+            h = cur.layout.height // l.f_w
+            plan = act2pc.RepackPlan(pooled.layout, l.c_o, next_layout(i, h), P)
+            rs = act2pc.offline_prepare_repack(plan, P, rng)
+            zeros = bfv.precompute_zero_rows(sk, rng, plan.k_dst)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            cur = act2pc.run_repack_round(pooled, rs, sk, zeros, P)
+            torch.cuda.synchronize()
+            t["offline_s"] += t1 - t0
+            t["repack_s"] += time.perf_counter() - t1
     t0 = time.perf_counter()
     pooled = conv.avg_pool(cur, pool.f_w, P)
     logits = conv.fully_connected(pooled, weights["fc"], P)
     out = bfv.centered(conv.read_scalar_outputs(logits, sk), P.p) % P.p
-    t_tail = time.perf_counter() - t0
+    t["tail_s"] = time.perf_counter() - t0
     if timings is not None:
-        timings.update(conv_s=t_conv, act_s=t_act, offline_s=t_off, tail_s=t_tail)
+        timings.update(t)
     return out
 
 

@@ -1,6 +1,6 @@
-"""Configs 3 and 4 end to end on the device (inference.py): conv -> x²+x
-(shares, client repack, stride) -> ... -> avg_pool -> FC, decrypted logits
-equal to the integer model mod p."""
+"""Configs 3, 4 and 5 end to end on the device (inference.py): conv -> x²+x
+(shares, client repack, stride) -> ... [-> 2x2 pool -> masked repack round]
+-> ... -> avg_pool -> FC, decrypted logits equal to the integer model mod p."""
 
 import numpy as np
 import pytest
@@ -8,17 +8,17 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["config3", "config4"])
+@pytest.mark.parametrize("name", ["config3", "config4", "config5"])
 def test_chain_matches_integer_model(name):
     from paper_2401_16732_b200 import bfv, inference, params
 
     P = params.default_params()
     rng = np.random.default_rng(2024 + len(name))
     layers = inference.config_layers(name)
-    convs, pool, fc = inference.main_path(layers)
+    seq, pool, fc = inference.main_path(layers)
     weights = inference.random_weights(layers, rng)
     sk = bfv.keygen(P, rng)
-    x = rng.integers(0, 8, (convs[0].c_i, convs[0].H, convs[0].W), dtype=np.int64)
+    x = rng.integers(0, 8, (seq[0].c_i, seq[0].H, seq[0].W), dtype=np.int64)
     got = inference.he_forward(layers, x, weights, sk, rng, P)
     want = inference.plain_forward(layers, x, weights, P.p)
     assert got.shape == (fc.c_o,)

@@ -285,19 +285,21 @@ __global__ void act_server_kernel(ModDesc mp, uint64_t two_f, const uint64_t* __
 // One thread per (position x, limb l, batch chunk): the 2*ndig key words of x
 // stay in registers and are reused by every ciphertext of the chunk (the key
 // is read from HBM once per chunk, not once per ciphertext).
-template <int MAXD>
-__global__ void keyswitch_kernel(const ModSet ms, int logn, int L, int B, int bchunk, int ndig,
-                                 uint64_t gpow, const uint64_t* __restrict__ ct,
-                                 const uint64_t* __restrict__ dig, const uint64_t* __restrict__ keys,
-                                 uint64_t* __restrict__ out) {
+template <int MAXD, int BCH>
+__global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int logn, int L, int B, int ndig,
+                                                        uint64_t gpow, const uint64_t* __restrict__ ct,
+                                                        const uint64_t* __restrict__ dig,
+                                                        const uint64_t* __restrict__ keys,
+                                                        uint64_t* __restrict__ out) {
   const int n = 1 << logn;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   const int l = blockIdx.y;
-  const int b0 = blockIdx.z * bchunk;
-  const int b1 = min(B, b0 + bchunk);
+  const int b0 = blockIdx.z * BCH;
   const ModDesc m = ms.m[l];
-  // eval_perm (ring.py:199-202): exp_at_index[x] = 2 bitrev(x) + 1
+  // eval_perm (ring.py:199-202): exp_at_index[x] = 2 bitrev(x) + 1. A warp's 32
+  // consecutive x gather from 32 distinct slots of two aligned 128-byte lines
+  // (the map permutes within blocks), so the gathers stay coalesced.
   const uint32_t e = 2u * brev_bits((uint32_t)x, logn) + 1u;
   const uint32_t e2 = (uint32_t)(((uint64_t)e * (gpow % (2ull * n))) % (2ull * n));
   const int src = (int)brev_bits((e2 - 1u) >> 1, logn);
@@ -309,22 +311,29 @@ __global__ void keyswitch_kernel(const ModSet ms, int logn, int L, int B, int bc
       k1[i] = keys[((size_t)(l * ndig + i) * 2 + 1) * n + x];
     }
   }
-  for (int b = b0; b < b1; ++b) {
-    const size_t crow = ((size_t)b * L + l) * 2;
-    const size_t drow = ((size_t)b * L + l) * ndig;
-    uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+  // BCH ciphertexts per thread, fully unrolled: every gather of the chunk can
+  // be issued before the first multiply (memory-level parallelism); the key
+  // words stay in registers for all of them
 #pragma unroll
-    for (int i = 0; i < MAXD; ++i) {
-      if (i < ndig) {
-        const uint64_t dv = dig[(drow + i) * n + src];
-        mac128(a0l, a0h, dv, k0[i]);
-        mac128(a1l, a1h, dv, k1[i]);
+  for (int bb = 0; bb < BCH; ++bb) {
+    const int b = b0 + bb;
+    if (b < B) {
+      const size_t crow = ((size_t)b * L + l) * 2;
+      const size_t drow = ((size_t)b * L + l) * ndig;
+      uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i) {
+        if (i < ndig) {
+          const uint64_t dv = __ldg(&dig[(drow + i) * n + src]);
+          mac128(a0l, a0h, dv, k0[i]);
+          mac128(a1l, a1h, dv, k1[i]);
+        }
       }
+      // Σ_i D_i swk_i < ndig q^2 < q 2^64 (ndig < 2^64/q): one REDC each
+      const uint64_t c0p = __ldg(&ct[crow * n + src]);
+      out[crow * n + x] = csub(redc(a0l, a0h, m) + c0p, m.q);
+      out[(crow + 1) * n + x] = redc(a1l, a1h, m);
     }
-    // Σ_i D_i swk_i < ndig q^2 < q 2^64 (ndig < 2^64/q): one REDC each
-    const uint64_t c0p = ct[crow * n + src];
-    out[crow * n + x] = csub(redc(a0l, a0h, m) + c0p, m.q);
-    out[(crow + 1) * n + x] = redc(a1l, a1h, m);
   }
 }
 
@@ -657,16 +666,19 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
     if ((u128_t)ndig * ms.m[l].q >= ((u128_t)1 << 64))
       return fail(FHE_ERR_PARAMETER, "too many digits for one lazy REDC");
   if (!B) return FHE_OK;
-  const int bchunk = 8;
+#ifndef FHE_KS_BCH
+#define FHE_KS_BCH 4
+#endif
+  constexpr int bchunk = FHE_KS_BCH;  // key words reused by bchunk ciphertexts; bchunk x ndig gathers in flight per thread
   dim3 grid((n + 127) / 128, L, (B + bchunk - 1) / bchunk);
   const int logn = log2i(n);
   cudaStream_t st = (cudaStream_t)stream;
   if (ndig <= 4)
-    keyswitch_kernel<4><<<grid, 128, 0, st>>>(ms, logn, L, B, bchunk, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<4, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else if (ndig <= 8)
-    keyswitch_kernel<8><<<grid, 128, 0, st>>>(ms, logn, L, B, bchunk, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<8, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else if (ndig <= 16)
-    keyswitch_kernel<16><<<grid, 128, 0, st>>>(ms, logn, L, B, bchunk, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<16, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else
     return fail(FHE_ERR_VALUE, "more than 16 digits unsupported");
   FHE_CHECK_LAUNCH("keyswitch_kernel");

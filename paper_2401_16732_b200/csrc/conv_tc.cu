@@ -45,7 +45,11 @@ namespace fhe {
 namespace tc {
 
 constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant
-constexpr int kRelWarps = 6;  // dedicated relayout warps (run ahead of the GEMM)
+#ifndef FHE_REL_WARPS
+#define FHE_REL_WARPS 4
+#endif
+constexpr int kRelWarps = FHE_REL_WARPS;  // dedicated relayout warps (run ahead of the GEMM); 4 measured
+                                           // best of 2..10 (fewer warps leave more registers per thread)
 constexpr int kWarps = 2 + kEpiWarps + kRelWarps;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kMaxTaps = 64;

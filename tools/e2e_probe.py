@@ -54,3 +54,32 @@ if len(sys.argv) > 1 and sys.argv[1] == "profile":
         outs = conv.conv_proposed_stream(js, P)
         pr.disable()
     pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+if len(sys.argv) > 1 and sys.argv[1] == "pieces":
+    import collections
+
+    acc = collections.defaultdict(float)
+    comp = torch.cuda.current_stream()
+    up, down = conv._streams()
+    for it in range(5):
+        js = jobs()
+        torch.cuda.synchronize()
+        for x, layer in js:
+            t0 = time.perf_counter()
+            plan = conv._proposed_plan(x, layer, P)
+            t1 = time.perf_counter()
+            inp, ready = x.cts.rows.upload_on(up)
+            t2 = time.perf_counter()
+            inp = inp.reshape(-1, 2, P.n)
+            out = torch.empty((plan.n_out, 2, P.n), dtype=torch.int64, device=inp.device)
+            t3 = time.perf_counter()
+            (ev,) = conv.issue_k1([(plan, inp, ready, out)])
+            t4 = time.perf_counter()
+            down.wait_event(ev)
+            rows = conv.device.DeviceRows.download_on(out, down)
+            t5 = time.perf_counter()
+            if it:
+                for k, v in zip(("plan", "upload", "empty", "issue_k1", "download"), (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4)):
+                    acc[k] += v
+        down.synchronize()
+    print({k: round(v / 4 / 20 * 1e6, 1) for k, v in acc.items()}, "us per job")

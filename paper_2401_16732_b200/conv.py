@@ -296,7 +296,7 @@ class ConvTcPlan:
     @staticmethod
     def _fits(pos_tile: int, h: int, taps: int) -> bool:
         win = -(-(pos_tile + 2 * h) * 256 // 1024) * 1024
-        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 212 * 1024  # >= 2 pipeline stages
+        return 2 * (win + taps * ConvTcPlan.OC_TILE * 32) <= 218 * 1024  # >= 2 pipeline stages (csrc kRingBudget)
 
     @staticmethod
     def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int, c_i: int = 32) -> int:

@@ -59,7 +59,9 @@ constexpr int kEpilogue = 32 * kEpiWarps;
 constexpr int kOcTile = 128;         // output channels per tile (MMA M)
 constexpr int kWTap = kOcTile * 32;  // packed weight bytes per (tap, 32 channels)
 constexpr int kStg = 2048;           // relayout staging bytes per warp (16 positions x 128 B)
-constexpr int kRingBudget = 212 * 1024;
+// stage ring: what 227 KB leaves after the relayout staging (kRelWarps x 2 KB) and the
+// barriers — 4 stages of the 16x16-map layers (54 KB each) fit, 3 did at 212 KB
+constexpr int kRingBudget = 227 * 1024 - kRelWarps * kStg - 1024;
 constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
 #ifndef FHE_RELAYOUT_STATIC
 #define FHE_RELAYOUT_STATIC 1

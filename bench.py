@@ -313,6 +313,7 @@ def sub_benchmarks(steps, warmup, hbm):
     res["rotation_sweep"] = {"gbs": round(gbs, 1), "ms": round(avg * 1e3, 3), "frac_hbm": round(gbs / hbm, 3),
                              "rotations": len(rsteps) * B, "rot_per_s": round(len(rsteps) * B / avg, 1),
                              "N": N, "L": L, "B": B, "T": T}
+    res["config2_sweep"] = config2_sweep()
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
     res["pool_fc_tail"] = pool_fc_tail(steps, warmup)
@@ -432,6 +433,89 @@ def act2pc_layer(steps, warmup):
     return {"workload": "config4 stem activations: 64 ch x 64x64, 192 cts in / 192 out (repacked)",
             "ms": round(ms, 3), "activations_per_s": round(acts / ms * 1e3, 1), "cts": plan.k_src,
             "timing": "wall clock per layer round trip incl. host issue and the client's noise-budget checks"}
+
+
+def config2_sweep():
+    """BASELINE config 2 as a table: N in {4096, 8192, 16384} x B in {1, 8, 64}
+    ciphertexts (2 polys) x L = 4 limbs: forward / inverse NTT, pmult, hadd and
+    one hoisted rotation (digits + key switch, T = 16): device time per call
+    (20 calls in one CUDA graph, CUDA events, median of 5 replays; operands
+    resident, L2 not flushed) and GB/s of algorithmic bytes."""
+    import torch
+
+    from paper_2401_16732_b200 import _native, device, params
+
+    rng = np.random.default_rng(21)
+    out = []
+    st = device.stream()
+
+    reps = 20
+
+    def med(fn):
+        """Device time per call: `reps` calls captured in one CUDA graph (no
+        host/ctypes overhead in the timed span), median of 5 replays."""
+        fn()
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+            s2 = device.stream()
+            for _ in range(reps):
+                fn(s2)
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / reps)
+        return sorted(ts)[2]
+
+    for N in (4096, 8192, 16384):
+        p = params.find_plaintext_modulus(N)
+        L = 4
+        limbs = params.limb_primes(N, p, L)
+        mods = _native.u64_array(limbs)
+        plans = device.plan_array(N, limbs)
+        T, l = 16, 4
+        for B in (1, 8, 64):
+            x = torch.from_numpy(np.stack([rng.integers(0, q, (B, 2, N), dtype=np.int64) for q in limbs], axis=1)).cuda()
+            y = torch.from_numpy(np.stack([rng.integers(0, q, (B, 2, N), dtype=np.int64) for q in limbs], axis=1)).cuda()
+            pt = torch.from_numpy(np.stack([rng.integers(0, q, (1, 1, N), dtype=np.int64) for q in limbs], axis=1)).cuda()
+            keys = torch.from_numpy(np.stack([rng.integers(0, q, (l, 2, N), dtype=np.int64) for q in limbs])).cuda()
+            o = torch.empty_like(x)
+            c1 = x[:, :, 1].contiguous()
+            coeff = torch.empty_like(c1)
+            dig = torch.empty((B, L, l, N), dtype=torch.int64, device="cuda")
+            rows = B * L * 2
+            r = {"N": N, "B": B, "L": L}
+            ms = med(lambda st=st: _native.call("fhe_ntt_forward", plans, L, B, 2, x.data_ptr(), o.data_ptr(), st))
+            r["ntt_fwd_us"], r["ntt_fwd_gbs"] = round(ms * 1e3, 2), round(rows * N * 16 / ms / 1e6, 1)
+            ms = med(lambda st=st: _native.call("fhe_ntt_inverse", plans, L, B, 2, x.data_ptr(), o.data_ptr(), st))
+            r["ntt_inv_us"], r["ntt_inv_gbs"] = round(ms * 1e3, 2), round(rows * N * 16 / ms / 1e6, 1)
+            ptp = torch.empty_like(pt)  # pmult as bfv.pmult runs it: Shoup with the plaintext's companions
+            _native.call("fhe_shoup_companions", mods, L, 1, 1, N, pt.data_ptr(), ptp.data_ptr(), st)
+            ms = med(lambda st=st: _native.call("fhe_poly_mul_shoup", mods, L, B, 2, N, x.data_ptr(), pt.data_ptr(),
+                                                ptp.data_ptr(), 1, 1, o.data_ptr(), st))
+            r["pmult_us"], r["pmult_gbs"] = round(ms * 1e3, 2), round((2 * rows + B * L) * N * 8 / ms / 1e6, 1)
+            ms = med(lambda st=st: _native.call("fhe_poly_binary", _native.OP_ADD, mods, L, B, 2, N, x.data_ptr(),
+                                                y.data_ptr(), B, 2, o.data_ptr(), st))
+            r["hadd_us"], r["hadd_gbs"] = round(ms * 1e3, 2), round(3 * rows * N * 8 / ms / 1e6, 1)
+
+            def rot(st=st):
+                _native.call("fhe_ntt_inverse", plans, L, B, 1, c1.data_ptr(), coeff.data_ptr(), st)
+                _native.call("fhe_ntt_forward_digits", plans, L, B, coeff.data_ptr(), dig.data_ptr(), T, l, st)
+                _native.call("fhe_keyswitch_apply", mods, L, B, N, x.data_ptr(), dig.data_ptr(), keys.data_ptr(), l,
+                             3, o.data_ptr(), st)
+
+            ms = med(rot)
+            alg = B * L * 8 * N * (2 + 2 * l) + B * L * 8 * N * (1 + l + 2) + L * 2 * l * 8 * N
+            r["rotation_us"], r["rotation_gbs"] = round(ms * 1e3, 2), round(alg / ms / 1e6, 1)
+            out.append(r)
+    return out
 
 
 def conventional_vs_proposed(steps, warmup):

@@ -111,6 +111,15 @@ int fhe_ntt_forward_digits(const fhe_plan* const* plans, int L, int B,
 int fhe_poly_binary(int op, const uint64_t* moduli, int L, int B, int P, int n,
                     const uint64_t* a, const uint64_t* b, int Bb, int Pb,
                     uint64_t* out, void* stream);
+/* bfv.pmult with a prepared plaintext (bfv.py:359-372): out = a ⊙ w mod q_l by
+ * Shoup multiplication, w_shoup = fhe_shoup_companions(w) (floor(w 2^64 / q_l),
+ * once per prepared plaintext). Same broadcast rules as fhe_poly_binary; the
+ * result equals FHE_OP_MUL bit for bit. q_l < 2^63. */
+int fhe_poly_mul_shoup(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a,
+                       const uint64_t* w, const uint64_t* w_shoup, int Bb, int Pb, uint64_t* out,
+                       void* stream);
+int fhe_shoup_companions(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* w,
+                         uint64_t* w_shoup, void* stream);
 /* ring.poly_neg (ring.py:233-235) */
 int fhe_poly_neg(const uint64_t* moduli, int L, int B, int P, int n,
                  const uint64_t* a, uint64_t* out, void* stream);

@@ -57,6 +57,8 @@ SIGNATURES = {
     "fhe_ntt_forward_digits": (_int, [_PP, _int, _int, _vp, _vp, _int, _int, _vp]),
     "fhe_poly_binary": (_int, [_int, _vp, _int, _int, _int, _int, _vp, _vp, _int, _int, _vp, _vp]),
     "fhe_poly_neg": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
+    "fhe_poly_mul_shoup": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp, _int, _int, _vp, _vp]),
+    "fhe_shoup_companions": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_poly_scalar_mul": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "fhe_poly_monomial": (_int, [_vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp]),
     "fhe_poly_automorphism": (_int, [_vp, _int, _int, _int, _int, _vp, _u64, _vp, _vp]),

@@ -67,6 +67,39 @@ __global__ void binary_kernel(int op, const ModSet ms, RowGeom g, int B, int Bb,
   *reinterpret_cast<ulonglong2*>(out + idx) = z;
 }
 
+// pmult with a prepared plaintext: Shoup multiplication by the plaintext word
+// and its companion w' = floor(w 2^64 / q) — 2 high/low products per element
+// instead of the generic 128-bit Barrett reduction; identical canonical result.
+__global__ void mul_shoup_kernel(const ModSet ms, RowGeom g, int Bb, int Pb, const uint64_t* __restrict__ a,
+                                 const uint64_t* __restrict__ w, const uint64_t* __restrict__ wp,
+                                 uint64_t* __restrict__ out, int64_t total2) {
+  const int64_t i2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pair index
+  if (i2 >= total2) return;
+  const int64_t idx = 2 * i2;
+  const int r = (int)(idx >> g.logn);  // rows < 2^31 (checked on the host)
+  const int col = (int)(idx & ((1 << g.logn) - 1));
+  const int p = r % g.P, t = r / g.P, l = t % g.L, bb = t / g.L;
+  const int64_t rb = ((int64_t)(bb % Bb) * g.L + l) * Pb + (p % Pb);
+  const uint64_t q = ms.m[l].q;
+  const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(a + idx);
+  const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(w + (rb << g.logn) + col);
+  const ulonglong2 yp = *reinterpret_cast<const ulonglong2*>(wp + (rb << g.logn) + col);
+  ulonglong2 z;
+  z.x = csub(shoup_lazy(x.x, y.x, yp.x, q), q);
+  z.y = csub(shoup_lazy(x.y, y.y, yp.y, q), q);
+  *reinterpret_cast<ulonglong2*>(out + idx) = z;
+}
+
+// w' = floor(w 2^64 / q_l) per word (one-time, when a plaintext is prepared)
+__global__ void shoup_companion_kernel(const ModSet ms, RowGeom g, const uint64_t* __restrict__ w,
+                                       uint64_t* __restrict__ wp, int64_t total) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int r = (int)(idx >> g.logn);
+  const int l = (r / g.P) % g.L;
+  wp[idx] = (uint64_t)(((unsigned __int128)w[idx] << 64) / ms.m[l].q);
+}
+
 __global__ void neg_kernel(const ModSet ms, RowGeom g, const uint64_t* __restrict__ a,
                            uint64_t* __restrict__ out, int64_t total) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,6 +496,37 @@ int fhe_poly_binary(int op, const uint64_t* moduli, int L, int B, int P, int n, 
   RowGeom g{L, P, log2i(n)};
   binary_kernel<<<grid_for(total2), kThreads, 0, (cudaStream_t)stream>>>(op, ms, g, B, Bb, Pb, a, b, out, total2);
   FHE_CHECK_LAUNCH("binary_kernel");
+  return FHE_OK;
+}
+
+int fhe_poly_mul_shoup(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* a, const uint64_t* w,
+                       const uint64_t* w_shoup, int Bb, int Pb, uint64_t* out, void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  if (!(Bb == 1 || Bb == B) || !(Pb == 1 || Pb == P) || Bb < 1) return fail(FHE_ERR_VALUE, "bad broadcast");
+  if ((int64_t)B * L * P >= ((int64_t)1 << 31)) return fail(FHE_ERR_VALUE, "too many rows");
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  for (int l = 0; l < L; ++l)
+    if (ms.m[l].q >= (1ull << 63)) return fail(FHE_ERR_PARAMETER, "Shoup multiply needs q < 2^63");
+  const int64_t total2 = (int64_t)B * L * P * n / 2;
+  if (!total2) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  mul_shoup_kernel<<<grid_for(total2), kThreads, 0, (cudaStream_t)stream>>>(ms, g, Bb, Pb, a, w, w_shoup, out,
+                                                                             total2);
+  FHE_CHECK_LAUNCH("mul_shoup_kernel");
+  return FHE_OK;
+}
+
+int fhe_shoup_companions(const uint64_t* moduli, int L, int B, int P, int n, const uint64_t* w, uint64_t* w_shoup,
+                         void* stream) {
+  if (int rc = check_rows(L, B, P, n)) return rc;
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  const int64_t total = (int64_t)B * L * P * n;
+  if (!total) return FHE_OK;
+  RowGeom g{L, P, log2i(n)};
+  shoup_companion_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, w, w_shoup, total);
+  FHE_CHECK_LAUNCH("shoup_companion_kernel");
   return FHE_OK;
 }
 

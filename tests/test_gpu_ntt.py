@@ -119,6 +119,32 @@ def test_config2_pmult_add(golden, N):
     for l, e in enumerate(ent["limb"]):
         assert sha(mul[l]) == e["h:pmul"]
         assert sha(add[l]) == e["h:add"]
+    # the Shoup form bfv.pmult uses gives the same words (golden), also broadcast
+    # over a batch of 3 ciphertexts x 2 polys
+    import torch
+
+    from paper_2401_16732_b200 import device
+
+    L = len(limbs)
+    mods = _native.u64_array(limbs)
+    bd = _dev(b)
+    bp = torch.empty_like(bd)
+    _native.call("fhe_shoup_companions", mods, L, 1, 1, N, bd.data_ptr(), bp.data_ptr(), device.stream())
+    ad = _dev(a)
+    out = torch.empty_like(ad)
+    _native.call("fhe_poly_mul_shoup", mods, L, 1, 1, N, ad.data_ptr(), bd.data_ptr(), bp.data_ptr(), 1, 1,
+                 out.data_ptr(), device.stream())
+    got = out.cpu().numpy()
+    for l, e in enumerate(ent["limb"]):
+        assert sha(got[l]) == e["h:pmul"]
+    rng = np.random.default_rng(N)
+    xs = np.stack([rng.integers(0, q, (3, 2, N), dtype=np.int64) for q in limbs], axis=1)  # [3][L][2][N]
+    xd = _dev(xs)
+    o2 = torch.empty_like(xd)
+    _native.call("fhe_poly_mul_shoup", mods, L, 3, 2, N, xd.data_ptr(), bd.data_ptr(), bp.data_ptr(), 1, 1,
+                 o2.data_ptr(), device.stream())
+    ref = ring.binary_rows(_native.OP_MUL, xd, bd, N, limbs, P=2, Bb=1, Pb=1).cpu().numpy()
+    assert np.array_equal(o2.cpu().numpy(), ref)
 
 
 def test_digit_ntt_vs_oracle():

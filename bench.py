@@ -337,9 +337,9 @@ def inference_chain(name):
     rng = np.random.default_rng(77)
     weights = inference.random_weights(layers, rng)
     specs = inference.layer_specs(layers, weights)  # K1 plans cached on the specs after the first run
+    sk = bfv.keygen(P, np.random.default_rng(78))  # the client's key, fixed across inferences
     for it in range(2):
         rng = np.random.default_rng(78 + it)
-        sk = bfv.keygen(P, rng)
         x = rng.integers(0, 8, (convs[0].c_i, convs[0].H, convs[0].W), dtype=np.int64)
         t = {}
         got = inference.he_forward(layers, x, weights, sk, rng, P, timings=t, specs=specs)

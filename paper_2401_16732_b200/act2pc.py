@@ -216,6 +216,19 @@ class RepackPlan:
         return np.where(self.idx_host >= 0, flat[np.maximum(self.idx_host, 0)], 0)
 
 
+_repack_plans: dict = {}
+
+
+def repack_plan(src, channels: int, dst, params: RingParams) -> RepackPlan:
+    """RepackPlan cached per geometry (its device maps and the layer graph that
+    replays its exchange are reused by every inference through that layer)."""
+    key = (src, channels, dst, params.fingerprint())
+    plan = _repack_plans.get(key)
+    if plan is None:
+        plan = _repack_plans[key] = RepackPlan(src, channels, dst, params)
+    return plan
+
+
 def _gather(idx: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
     src_c = src.contiguous()
     out = torch.empty(idx.shape, dtype=torch.int64, device=idx.device)
@@ -376,9 +389,108 @@ def server_finalize_layer(ct1: torch.Tensor, ct2: torch.Tensor, session: LayerSe
     return conv.PackedTensor(cts, plan.dst, plan.channels, scale)
 
 
+class _StaticKey:
+    """Stands in for a SecretKey inside a captured exchange: s_eval from a
+    static device buffer (refilled per replay), so one graph serves any key."""
+
+    def __init__(self, params: RingParams, s_eval: torch.Tensor):
+        self.params, self._s = params, s_eval
+
+    def s_eval_dev(self) -> torch.Tensor:
+        return self._s
+
+
+class _LayerGraph:
+    """One layer's whole exchange (both parties, ~20 kernels) captured once per
+    (RepackPlan, fraction bits) into a CUDA graph over static operand buffers:
+    a replay costs one launch instead of ~20 Python/ctypes launches. The
+    kernels and data are the eager path's, so the ciphertexts are identical."""
+
+    def __init__(self, plan: RepackPlan, params: RingParams, f: int):
+        n, ks, kd = params.n, plan.k_src, plan.k_dst
+        dev = device.require_cuda()
+        z = lambda *shape: torch.zeros(shape, dtype=torch.int64, device=dev)  # noqa: E731
+        self.inp, self.zeros = z(ks, 2, n), z(3 * kd, 2, n)
+        self.r, self.two_r, self.v_eval, self.const = z(ks, n), z(kd, n), z(kd, n), z(kd, n)
+        self.s_eval = z(n)
+        key = _StaticKey(params, self.s_eval)
+
+        def body():
+            pending: list = []
+            m1 = _encrypt_rows(self.inp, self.r, params)
+            w = _decrypt_rows_checked(m1, Domain.COEFF, key, pending)
+            ct_sq = _encrypt_rows(self.zeros[:kd], _gather(plan.idx, w), params, square=True, f=f)
+            ct_w = _encrypt_rows(self.zeros[kd : 2 * kd], _batch_coeffs(_gather(plan.idx_eval, w), params), params)
+            w_eval = ring.ntt_rows(ct_w.reshape(-1, n), n, [params.q])
+            m2 = torch.empty_like(ct_w)
+            _native.call("fhe_ct_pmult_add", params.q, kd, n, w_eval.data_ptr(), self.two_r.data_ptr(),
+                         self.v_eval.data_ptr(), m2.data_ptr(), device.stream())
+            mm = _decrypt_rows_checked(m2, Domain.EVAL, key, pending)
+            evals = ring.ntt_rows(mm, n, [params.p])
+            back = _encrypt_rows(self.zeros[2 * kd :], evals, params, perm=plan.slot)
+            out = torch.empty_like(ct_sq)
+            _native.call("fhe_act_finalize", params.q, params.p, params.delta, kd, n, ct_sq.data_ptr(),
+                         back.data_ptr(), self.const.data_ptr(), out.data_ptr(), device.stream())
+            return out, torch.cat(pending)
+
+        body()  # plans, tables and kernels initialised outside the capture
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side), torch.cuda.graph(self.graph, stream=side):
+            self.out, self.maxw = body()
+        torch.cuda.current_stream().wait_stream(side)
+
+    def run(self, conv_rows: torch.Tensor, session: "LayerSession", sk: bfv.SecretKey, zero_rows: torch.Tensor):
+        self.inp.copy_(conv_rows)
+        self.zeros.copy_(zero_rows)
+        self.r.copy_(session.r)
+        self.two_r.copy_(session.two_r_eval)
+        self.v_eval.copy_(session.v_eval)
+        self.const.copy_(session.const)
+        self.s_eval.copy_(sk.s_eval_dev())
+        self.graph.replay()
+        return self.out.clone(), self.maxw.clone()
+
+
+_layer_graphs: dict = {}
+
+
+def _graph_for(plan: RepackPlan, params: RingParams, f: int) -> _LayerGraph:
+    key = (id(plan), params.fingerprint(), f)
+    hit = _layer_graphs.get(key)
+    if hit is None or hit[0] is not plan:
+        hit = _layer_graphs[key] = (plan, _LayerGraph(plan, params, f))
+    return hit[1]
+
+
 def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
-                         params: RingParams):
-    """Both parties in-process: one layer's full two-round exchange."""
+                         params: RingParams, graph: bool | None = None):
+    """Both parties in-process: one layer's full two-round exchange. With
+    `graph` (default: FLASHHE_ACT_GRAPH != 0) the exchange replays a CUDA graph
+    captured per RepackPlan (identical ciphertexts, one launch)."""
+    import os
+
+    if graph is None:
+        graph = os.environ.get("FLASHHE_ACT_GRAPH", "1") != "0"
+    if graph:
+        from . import conv
+
+        plan = session.plan
+        _expect(session, Round.INIT)
+        cts = conv_out.cts if hasattr(conv_out, "cts") else conv_out
+        if len(cts) != plan.k_src:
+            raise EncodingError("conv output does not match the session's layout")
+        if cts[0].encoding != Encoding.DIRECT:
+            raise EncodingError("activation input must be direct-encoded")
+        zero_rows = zeros.take_rows(3 * plan.k_dst)  # rounds 1 (2 k) and 2 (k), in the eager order
+        f = session.codec.frac_bits if session.codec else 0
+        out, maxw = _graph_for(plan, params, f).run(bfv.cts_rows(cts), session, sk, zero_rows)
+        session.round = Round.DONE
+        _check_budget_rows(params, maxw)
+        res = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+        return conv.PackedTensor(res, plan.dst, plan.channels, getattr(conv_out, "scale", 0))
     plan = session.plan
     pending: list = []  # the client's noise-budget checks, run once after the exchange (one host sync)
     m1 = server_round1_layer(conv_out, session, params)

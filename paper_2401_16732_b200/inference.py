@@ -95,7 +95,15 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
     specs = specs if specs is not None else layer_specs(layers, weights)
     t = dict(conv_s=0.0, act_s=0.0, offline_s=0.0, repack_s=0.0)
     first = seq[0]
+    t0 = time.perf_counter()
     cur = conv.pack_input(x, P, first.f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
+    # the client's ciphertexts as one device stack (seeded c1 halves are host
+    # arrays until uploaded): the upload is the input transfer, not the conv
+    rows = bfv.cts_rows(cur.cts).contiguous()
+    cur = conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), cur.layout,
+                            cur.channels, cur.scale)
+    torch.cuda.synchronize()
+    t["input_s"] = time.perf_counter() - t0
 
     def next_layout(i, h):
         nxt = seq[i + 1]
@@ -111,7 +119,7 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
             if l.stride > 1:  # subsampled by the client's repack below
                 y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
             t0 = time.perf_counter()
-            plan = act2pc.RepackPlan(y.layout, l.c_o, next_layout(i, l.H // l.stride), P)
+            plan = act2pc.repack_plan(y.layout, l.c_o, next_layout(i, l.H // l.stride), P)
             sess = act2pc.offline_prepare_layer(plan, P, rng, frac_bits=frac_bits)
             zeros = bfv.precompute_zero_rows(sk, rng, 3 * plan.k_dst)
             torch.cuda.synchronize()
@@ -124,7 +132,7 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
             t0 = time.perf_counter()
             pooled = conv.avg_pool(cur, l.f_w, P)
             h = cur.layout.height // l.f_w
-            plan = act2pc.RepackPlan(pooled.layout, l.c_o, next_layout(i, h), P)
+            plan = act2pc.repack_plan(pooled.layout, l.c_o, next_layout(i, h), P)
             rs = act2pc.offline_prepare_repack(plan, P, rng)
             zeros = bfv.precompute_zero_rows(sk, rng, plan.k_dst)
             torch.cuda.synchronize()

@@ -162,3 +162,22 @@ def test_layer_protocol_errors():
     m2 = act2pc.server_round2_layer((sq, w), sess, P)
     with pytest.raises(ProtocolError):
         act2pc.client_round2_layer(m2, plan, sk, zeros)  # pool exhausted: never reuse a zero
+
+
+def test_layer_graph_matches_eager():
+    """The CUDA-graph replay of the layer exchange gives the eager path's
+    ciphertexts bit for bit (same masks, same zero rows)."""
+    from paper_2401_16732_b200 import act2pc, bfv, conv, params
+
+    P = params.default_params()
+    rng = np.random.default_rng(99)
+    sk = bfv.keygen(P, rng)
+    y = _conv_output(P, rng, sk, 16, 8, 3, 2)
+    plan = act2pc.repack_plan(y.layout, 8, conv.layout_direct(P, 8, 8, 3), P)
+    outs = []
+    for graph in (False, True, True):
+        r2 = np.random.default_rng(5)
+        sess = act2pc.offline_prepare_layer(plan, P, r2)
+        zeros = bfv.precompute_zero_rows(sk, r2, 3 * plan.k_dst)
+        outs.append(bfv.cts_rows(act2pc.run_layer_activation(y, sess, sk, zeros, P, graph=graph).cts).cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])

@@ -333,17 +333,20 @@ class ConvTcPlan:
     def __init__(self, q: int, n: int, weights3d: np.ndarray, steps: np.ndarray, layout: TileLayout | None,
                  bias, mask, chan: np.ndarray | None = None):
         """`chan` ([c_i, 2]: source ciphertext, slot offset) replaces the
-        layout's channel placement — fully_connected's per-input DRot slots."""
+        layout's channel placement — fully_connected's per-input DRot slots,
+        or a tap-folded conv's (channel, tap) pairs (fragment f then reads
+        source + f when the layout is fragmented)."""
         self.q, self.n = int(q), int(n)
         self.c_o, self.c_i, self.taps = weights3d.shape
         self.h = int(np.abs(steps).max(initial=0))
-        self.frags = 1 if chan is not None else layout.frags
+        self.frags = layout.frags if layout is not None else 1
         self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps, self.c_i)
         N = self.OC_TILE
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
         j = np.arange(self.c_i)
         if chan is not None:
-            chan, self.fstride = np.asarray(chan, dtype=np.int64).reshape(self.c_i, 2), 0
+            chan = np.asarray(chan, dtype=np.int64).reshape(self.c_i, 2)
+            self.fstride = 1 if layout is not None and layout.fragmented else 0
         elif layout.fragmented:
             chan, self.fstride = np.stack([j * layout.frags, np.zeros_like(j)], 1), 1
         else:
@@ -481,7 +484,23 @@ def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> C
     plan = ConvPlan(params.q, params.n, layer.weights.reshape(layer.c_o, -1), src, step,
                     frags=layout.frags, fstride=fstride, bias_delta=bias_delta, bias_mask=bias_mask)
     h = int(np.abs(steps).max(initial=0))
-    if ConvTcPlan.eligible(layer.weights, params.q, params.n, h, taps):
+    c_i = layer.c_i
+    if taps > 1 and -(-(c_i * taps) // 32) < -(-c_i // 32) * taps:
+        # Few input channels (the stems): fold the taps into the contraction —
+        # virtual channel (j, t) = channel j read at its tap's DRot offset, one
+        # tap with no halo. ceil(c_i·taps/32) MMAs per tile instead of
+        # ceil(c_i/32)·taps, and 7x7 stems fit the tensor-core path at all.
+        w3 = layer.weights.reshape(layer.c_o, c_i * taps, 1)
+        jj = np.repeat(np.arange(c_i), taps)
+        tt = np.tile(np.arange(taps), c_i)
+        if layout.fragmented:
+            chan = np.stack([jj * layout.frags, steps[tt]], 1)
+        else:
+            chan = np.stack([jj // layout.c_n, layout.tile * (jj % layout.c_n) + steps[tt]], 1)
+        if ConvTcPlan.eligible(w3, params.q, params.n, 0, 1):
+            plan.tc = ConvTcPlan(params.q, params.n, w3, np.zeros(1, dtype=np.int64), layout, plan.bias, plan.mask,
+                                 chan=chan)
+    elif ConvTcPlan.eligible(layer.weights, params.q, params.n, h, taps):
         plan.tc = ConvTcPlan(params.q, params.n, layer.weights, steps, layout, plan.bias, plan.mask)
     cache[key] = plan
     return plan

@@ -230,6 +230,15 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
  * mod q, so identical to the k^2-tap contraction). (k-1)(w_p+1) < n, n <= 8192. */
 int fhe_avg_pool(uint64_t q, int n, int rows, int k, int w_p, const uint64_t* in, uint64_t* out,
                  void* stream);
+/* The serving path's per-job step in one call (conv.conv_proposed_stream):
+ * host_in (PINNED, in_bytes) -> layer->in on stream `up`, event ev_up; `comp`
+ * waits for it and runs the layer (fhe_conv_tc_stack, nl = 1), event ev_comp;
+ * `down` waits for that and copies layer->out to host_out (PINNED, out_bytes).
+ * Streams and events are cudaStream_t / cudaEvent_t; the two events may be
+ * reused for every job (waits bind to the latest record). */
+int fhe_conv_stream_job(uint64_t q, int n, const fhe_conv_tc_layer* layer, const void* host_in,
+                        size_t in_bytes, void* host_out, size_t out_bytes, uint8_t* X, size_t x_stride,
+                        uint64_t* sync, void* up, void* comp, void* down, void* ev_up, void* ev_comp);
 /* Host-only budget guard (conv._check_budget conv.py:314-319, ring.py:366-372):
  * FHE_ERR_BUDGET if max_o Σ_k |w[o][k]| >= 2^32. weights: HOST int64 [c_o][K]. */
 int fhe_conv_check_budget(const int64_t* weights_host, int c_o, int K);

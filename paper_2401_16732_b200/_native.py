@@ -77,6 +77,11 @@ SIGNATURES = {
     "fhe_conv_check_budget": (_int, [_vp, _int, _int]),
     "fhe_avg_pool": (_int, [_u64, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_conv_tc_stack": (_int, [_u64, _int, _vp, _int, _vp, ctypes.c_size_t, _vp, _vp]),
+    "fhe_conv_stream_job": (
+        _int,
+        [_u64, _int, _vp, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp,
+         _vp, _vp],
+    ),
     "fhe_to_montgomery": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_keyswitch_apply": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _int, _u64, _vp, _vp]),
     "fhe_pmac": (_int, [_u64, _int, _vp, _vp, _vp, _vp, _int, _vp, _vp]),

@@ -389,6 +389,15 @@ MAX_STACK = 24
 _stack_sync: dict[tuple, torch.Tensor] = {}
 
 
+def _stack_sync_for(tcs) -> torch.Tensor:
+    """The counter buffer of one layer sequence (see run_tc_stack)."""
+    key = (torch.cuda.current_device(),) + tuple(id(tc) for tc in tcs)
+    sync = _stack_sync.get(key)
+    if sync is None:
+        sync = _stack_sync[key] = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=device.require_cuda())
+    return sync
+
+
 def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
     """One fhe_conv_tc_stack launch for [(ConvTcPlan, inp, out)] (≤ 24 layers
     sharing q and n) on the current stream. `sync` defaults to a counter
@@ -398,10 +407,7 @@ def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
     if len(jobs) > MAX_STACK:
         raise ValueError(f"at most {MAX_STACK} layers per tensor-core launch")
     if sync is None:
-        key = (torch.cuda.current_device(),) + tuple(id(tc) for tc, *_ in jobs)
-        sync = _stack_sync.get(key)
-        if sync is None:
-            sync = _stack_sync[key] = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=device.require_cuda())
+        sync = _stack_sync_for([tc for tc, *_ in jobs])
     need = -(-max(tc.x_bytes for tc, *_ in jobs) // 256) * 256
     X = device.scratch("conv_tc_x", need * (3 if len(jobs) > 1 else 1))
     arr = (_native.ConvTcLayer * len(jobs))(*[tc.layer(inp, out) for tc, inp, out in jobs])
@@ -565,8 +571,34 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     host_all = torch.empty(sum(sizes), dtype=torch.int64, pin_memory=True)
     views = torch.split(host_all, sizes)
     outs = []
+    fast = _native.fn("fhe_conv_stream_job")
+    ev_up, ev_comp = torch.cuda.Event(), torch.cuda.Event()
+    ev_up.record(comp)  # create the cudaEvent handles (torch makes them on first record)
+    ev_comp.record(comp)
+    X = device.scratch("conv_tc_x", -(-need // 256) * 256) if need else 0
     for (x, layer, plan), hv in zip(meta, views):  # one pass: job i's download is enqueued before job i+1's upload
         ready = None
+        rows_in = x.cts.rows if isinstance(x.cts, bfv.CtStack) else None
+        if plan.path == "tc" and rows_in is not None and rows_in._dev is None and rows_in._pinned is not None:
+            # host-resident pinned input: upload, K1 and download in one C call (one
+            # ctypes crossing per job instead of ~10 torch/ctypes calls)
+            pin = rows_in._pinned
+            inp = torch.empty((pin.numel() // (2 * params.n), 2, params.n), dtype=torch.int64, device=comp.device)
+            out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=comp.device)
+            lay = (_native.ConvTcLayer * 1)(plan.tc.layer(inp, out))
+            sync = _stack_sync_for([plan.tc])
+            rc = fast(params.q, params.n, lay, pin.data_ptr(), pin.numel() * 8, hv.data_ptr(), hv.numel() * 8, X,
+                      -(-need // 256) * 256, sync.data_ptr(), up.cuda_stream, comp.cuda_stream, down.cuda_stream,
+                      ev_up.cuda_event, ev_comp.cuda_event)
+            if rc:
+                _native.check(rc)
+            rows_in._dev = inp.reshape(-1, params.n)
+            h = hv.view(out.shape[0] * 2, params.n).numpy()
+            h.flags.writeable = False
+            rows = device.DeviceRows(dev=out.reshape(-1, params.n), host=h, pinned=hv)
+            cts = bfv.CtStack(rows, params.q, Encoding.DIRECT, Domain.COEFF)
+            outs.append(PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale))
+            continue
         if isinstance(x.cts, bfv.CtStack):
             inp, ready = x.cts.rows.upload_on(up)
         else:

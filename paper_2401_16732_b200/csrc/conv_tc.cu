@@ -961,4 +961,20 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   return FHE_OK;
 }
 
+int fhe_conv_stream_job(uint64_t q, int n, const fhe_conv_tc_layer* layer, const void* host_in, size_t in_bytes,
+                        void* host_out, size_t out_bytes, uint8_t* X, size_t x_stride, uint64_t* sync, void* up,
+                        void* comp, void* down, void* ev_up, void* ev_comp) {
+  if (!layer || !host_in || !host_out || !ev_up || !ev_comp)  // streams may be 0 (the legacy default stream)
+    return fail(FHE_ERR_VALUE, "null stream-job operand");
+  cudaStream_t su = (cudaStream_t)up, sc = (cudaStream_t)comp, sd = (cudaStream_t)down;
+  FHE_CUDA(cudaMemcpyAsync((void*)layer->in, host_in, in_bytes, cudaMemcpyHostToDevice, su));
+  FHE_CUDA(cudaEventRecord((cudaEvent_t)ev_up, su));
+  FHE_CUDA(cudaStreamWaitEvent(sc, (cudaEvent_t)ev_up, 0));
+  if (int rc = fhe_conv_tc_stack(q, n, layer, 1, X, x_stride, sync, comp)) return rc;
+  FHE_CUDA(cudaEventRecord((cudaEvent_t)ev_comp, sc));
+  FHE_CUDA(cudaStreamWaitEvent(sd, (cudaEvent_t)ev_comp, 0));
+  FHE_CUDA(cudaMemcpyAsync(host_out, layer->out, out_bytes, cudaMemcpyDeviceToHost, sd));
+  return FHE_OK;
+}
+
 }  // extern "C"

@@ -170,3 +170,39 @@ def test_conventional_steps_and_storage():
     steps = conv.vgg16_step_set(P)
     mb = len(steps) * P.decomp_count * 2 * P.n * 8 / 1e6
     assert abs(mb - 11.67) < 0.05
+
+
+def test_wire_format_frames():
+    """bfv.py:525-561 wire frames: header <BBB> (encoding, domain, seeded), c0
+    as little-endian u64, then the 32-byte c1 seed or c1; batched stacks are
+    consecutive unseeded frames."""
+    import struct
+
+    from paper_2401_16732_b200 import bfv, params
+    from paper_2401_16732_b200.ring import Domain, ModPoly
+
+    P = params.default_params()
+    rng = np.random.default_rng(12)
+    seed = bytes(range(32))
+    c0 = rng.integers(0, P.q, P.n, dtype=np.int64)
+    c1 = bfv.expand_seed(seed, P)
+    fresh = bfv.Ciphertext(ModPoly(c0, P.q), ModPoly(c1, P.q), bfv.Encoding.DIRECT, Domain.COEFF, fresh=True, seed=seed)
+    wire = bfv.ct_to_bytes(fresh)
+    assert wire == struct.pack("<BBB", 1, 0, 1) + c0.astype("<u8").tobytes() + seed
+    assert len(wire) == bfv.ct_wire_size(P, True)
+    back = bfv.ct_from_bytes(wire, P)
+    assert np.array_equal(back.c0.coeffs, c0) and np.array_equal(back.c1.coeffs, c1) and back.seed == seed
+    full = bfv.ct_to_bytes(fresh, seed_compress=False)
+    assert full == struct.pack("<BBB", 1, 0, 0) + c0.astype("<u8").tobytes() + c1.astype("<u8").tobytes()
+    assert len(full) == bfv.ct_wire_size(P, False)
+    ev = bfv.Ciphertext(ModPoly(c1, P.q, Domain.EVAL), ModPoly(c0, P.q, Domain.EVAL), bfv.Encoding.BATCH, Domain.EVAL)
+    assert bfv.ct_to_bytes(ev)[:3] == struct.pack("<BBB", 0, 1, 0)  # EVAL never seed-compressed
+    cts = [bfv.Ciphertext(ModPoly(rng.integers(0, P.q, P.n, dtype=np.int64), P.q),
+                          ModPoly(rng.integers(0, P.q, P.n, dtype=np.int64), P.q), bfv.Encoding.DIRECT, Domain.COEFF)
+           for _ in range(3)]
+    blob = bfv.cts_to_bytes(cts, bfv.Encoding.DIRECT, Domain.COEFF)
+    assert blob == b"".join(bfv.ct_to_bytes(c, seed_compress=False) for c in cts)
+    stack = bfv.cts_from_bytes(blob, 3, P, pin=False)
+    got = stack.host_stack()
+    for i, c in enumerate(cts):
+        assert np.array_equal(got[i, 0], c.c0.coeffs) and np.array_equal(got[i, 1], c.c1.coeffs)

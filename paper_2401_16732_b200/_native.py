@@ -11,22 +11,15 @@ import ctypes
 import threading
 from pathlib import Path
 
-from .errors import AccumulatorBudgetError, EncodingError, ParameterError, ProtocolError
+import os
 
-import os  # noqa: E402
+from .errors import BY_STATUS
 
 # FLASHHE_LIB: an alternative build of the same library (development probes only)
 LIB_PATH = Path(os.environ.get("FLASHHE_LIB") or Path(__file__).resolve().parent / "libflashhe.so")
 
 FHE_OK = 0
-_ERRORS = {
-    1: ParameterError,
-    2: EncodingError,
-    3: AccumulatorBudgetError,
-    4: ProtocolError,
-    5: ValueError,
-    6: RuntimeError,
-}
+_ERRORS = {**BY_STATUS, 5: ValueError, 6: RuntimeError}
 
 OP_ADD, OP_SUB, OP_MUL = 0, 1, 2
 MAX_LIMBS = 8

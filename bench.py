@@ -261,7 +261,7 @@ def cpu_baseline(P, layers, threads: int):
 # ------------------------------------------------------- config-2 sweep
 
 
-def sub_benchmarks(steps, warmup, hbm):
+def sub_benchmarks(steps, warmup, hbm, peaks=None):
     """Config 2 at N=16384, L=4 limbs, B=64 ciphertexts: NTT fwd/inv and the
     hoisted rotation sweep (steps 1,2,4..N/4) — GB/s of algorithmic bytes."""
     import torch
@@ -284,8 +284,11 @@ def sub_benchmarks(steps, warmup, hbm):
         ms = time_steps(lambda: _native.call(fn, plans, L, B, 2, t.data_ptr(), out.data_ptr(), st), steps, warmup, flush)
         avg = sum(ms) / len(ms) * 1e-3
         gbs = rows * N * 16 / avg / 1e9
+        bfly = rows * (N // 2) * (N.bit_length() - 1) / avg
         res[name] = {"gbs": round(gbs, 1), "ms": round(avg * 1e3, 4), "frac_hbm": round(gbs / hbm, 3),
-                     "rows": rows, "N": N}
+                     "rows": rows, "N": N, "bound": "integer (butterfly)", "bfly_per_s": round(bfly, 1)}
+        if peaks and peaks.get("butterfly"):
+            res[name]["frac_butterfly"] = round(bfly / peaks["butterfly"], 3)
     # rotation sweep: iNTT(c1) + l digit NTTs once (hoisted), then K4 per step
     T, l = 16, 4
     rsteps = [1 << i for i in range(N.bit_length() - 2)]  # 1 .. N/4
@@ -304,6 +307,13 @@ def sub_benchmarks(steps, warmup, hbm):
             _native.call("fhe_keyswitch_apply", mods, L, B, N, t.data_ptr(), dig.data_ptr(), keys[s].data_ptr(), l,
                          pow(3, s, 2 * N), rot.data_ptr(), st)
 
+    def switches():
+        for s in rsteps:
+            _native.call("fhe_keyswitch_apply", mods, L, B, N, t.data_ptr(), dig.data_ptr(), keys[s].data_ptr(), l,
+                         pow(3, s, 2 * N), rot.data_ptr(), st)
+
+    ms = time_steps(switches, max(2, steps // 2), warmup, flush)
+    avg_ks = sum(ms) / len(ms) * 1e-3
     ms = time_steps(sweep, max(2, steps // 2), warmup, flush)
     avg = sum(ms) / len(ms) * 1e-3
     ct_limbs = B * L
@@ -313,6 +323,10 @@ def sub_benchmarks(steps, warmup, hbm):
     res["rotation_sweep"] = {"gbs": round(gbs, 1), "ms": round(avg * 1e3, 3), "frac_hbm": round(gbs / hbm, 3),
                              "rotations": len(rsteps) * B, "rot_per_s": round(len(rsteps) * B / avg, 1),
                              "N": N, "L": L, "B": B, "T": T}
+    alg_ks = len(rsteps) * (ct_limbs * 8 * N * (1 + l + 2) + L * 2 * l * 8 * N)
+    res["keyswitch_only"] = {"gbs": round(alg_ks / avg_ks / 1e9, 1), "ms": round(avg_ks * 1e3, 3),
+                             "frac_hbm": round(alg_ks / avg_ks / 1e9 / hbm, 3), "launches": len(rsteps),
+                             "note": "the sweep's 13 key-switch launches alone (digits already in EVAL form)"}
     res["config2_sweep"] = config2_sweep()
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
@@ -739,7 +753,7 @@ def main():
         if rank == 0:
             result["e2e"] = e2e
     if rank == 0 and not args.no_sub:
-        result["sub"] = sub_benchmarks(max(4, args.steps // 2), args.warmup, hbm)
+        result["sub"] = sub_benchmarks(max(4, args.steps // 2), args.warmup, hbm, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         est_s, units = cpu_baseline(P, layers, threads)

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
   const int limb = (row / lm.G) % ls.L;
   const NttDesc d = ls.d[limb];
   const int n = d.n;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int tid = threadIdx.x;
   const uint64_t* srow;
   int shift = 0;
   if (from_src) {
@@ -381,17 +381,23 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
     return COLS ? (size_t)e * (1 << b) + part * kSplitW + v : (size_t)(part * kSplitW + v) * len + e;
   };
   auto sidx = [&](int e, int v) -> int { return COLS ? e * kSplitW + v : v * (len + len / 16) + spad(e); };
-  // load (pairs of consecutive elements: columns for COLS, positions for blocks)
-  for (int i = tid; i < (len * kSplitW) / 2; i += nthr) {
-    int e, v;
-    if (COLS) {
-      e = (2 * i) / kSplitW;
-      v = (2 * i) % kSplitW;
-    } else {
-      v = (2 * i) / len;
-      e = (2 * i) % len;
-    }
-    ulonglong2 x = *reinterpret_cast<const ulonglong2*>(srow + gidx(e, v));
+  // load (pairs of consecutive elements: columns for COLS, positions for blocks):
+  // the thread count is a compile-time constant (kSplitW sub-transforms x
+  // len / 2^LOGR items), so all NP pair loads are issued before the first
+  // shared-memory store
+  constexpr int NT = kSplitW * (len >> LOGR), NP = (len * kSplitW / 2) / NT;
+  ulonglong2 xin[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int i = tid + k * NT;
+    const int e = COLS ? (2 * i) / kSplitW : (2 * i) % len, v = COLS ? (2 * i) % kSplitW : (2 * i) / len;
+    xin[k] = *reinterpret_cast<const ulonglong2*>(srow + gidx(e, v));
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int i = tid + k * NT;
+    const int e = COLS ? (2 * i) / kSplitW : (2 * i) % len, v = COLS ? (2 * i) % kSplitW : (2 * i) / len;
+    ulonglong2 x = xin[k];
     if (from_src && lm.ndig > 0) {
       x.x = (x.x >> shift) & mask;
       x.y = (x.y >> shift) & mask;
@@ -411,17 +417,13 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
   const int item = COLS ? tid / kSplitW : tid % ipv;
   const uint32_t O = COLS ? (uint32_t)len : (uint32_t)((1 << a) + part * kSplitW + v) << b;
   split_sub<LOGR, INV, COLS, LG>(sm, v, item, d, O, INV && COLS);
-  // store
+  // store: all NP pairs read from shared memory, then written
   const uint64_t q = d.m.q, q2 = 2 * q;
-  for (int i = tid; i < (len * kSplitW) / 2; i += nthr) {
-    int e, vv;
-    if (COLS) {
-      e = (2 * i) / kSplitW;
-      vv = (2 * i) % kSplitW;
-    } else {
-      vv = (2 * i) / len;
-      e = (2 * i) % len;
-    }
+  ulonglong2 xo[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int i = tid + k * NT;
+    const int e = COLS ? (2 * i) / kSplitW : (2 * i) % len, vv = COLS ? (2 * i) % kSplitW : (2 * i) / len;
     uint64_t x = sm[sidx(e, vv)];
     uint64_t y = COLS ? sm[sidx(e, vv + 1)] : sm[sidx(e + 1, vv)];
     if (final_) {
@@ -432,7 +434,13 @@ __global__ void __launch_bounds__(256, MINB) ntt_split_kernel(const LimbSet ls, 
       x = csub(x, q);
       y = csub(y, q);
     }
-    *reinterpret_cast<ulonglong2*>(drow + gidx(e, vv)) = make_ulonglong2(x, y);
+    xo[k] = make_ulonglong2(x, y);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int i = tid + k * NT;
+    const int e = COLS ? (2 * i) / kSplitW : (2 * i) % len, vv = COLS ? (2 * i) % kSplitW : (2 * i) / len;
+    *reinterpret_cast<ulonglong2*>(drow + gidx(e, vv)) = xo[k];
   }
 }
 
@@ -445,8 +453,8 @@ static void launch_split_k(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, 
 // One CTA per row for 2^LOGN <= 4096 with the split kernels' compile-time
 // phase geometry (the whole row is one "block": O = n, v = 0): one item per
 // thread per phase, element slots and twiddle indices as base + constant.
-template <bool INV, int LOGN>
-__global__ void __launch_bounds__((1 << LOGN) / 16) ntt_row_kernel(const LimbSet ls, const LoadMap lm,
+template <bool INV, int LOGN, int LOGR>
+__global__ void __launch_bounds__((1 << LOGN) >> LOGR) ntt_row_kernel(const LimbSet ls, const LoadMap lm,
                                                                    uint64_t* __restrict__ dst) {
   extern __shared__ uint64_t sm[];
   constexpr int n = 1 << LOGN;
@@ -462,10 +470,14 @@ __global__ void __launch_bounds__((1 << LOGN) / 16) ntt_row_kernel(const LimbSet
     srow = lm.src + (size_t)row * n;
   }
   const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(srow);
+  constexpr int NT = n >> LOGR, NP = (n / 2) / NT;  // n/2 pairs over n/2^LOGR threads
+  ulonglong2 xin[NP];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {  // n/2 pairs over n/16 threads
-    const int i = tid + k * (n / 16);
-    ulonglong2 v = s2[i];
+  for (int k = 0; k < NP; ++k) xin[k] = s2[tid + k * NT];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int i = tid + k * NT;
+    ulonglong2 v = xin[k];
     if (lm.ndig > 0) {
       v.x = (v.x >> shift) & lm.mask;
       v.y = (v.y >> shift) & lm.mask;
@@ -474,18 +486,45 @@ __global__ void __launch_bounds__((1 << LOGN) / 16) ntt_row_kernel(const LimbSet
     sm[spad(2 * i + 1)] = v.y;
   }
   __syncthreads();
-  split_sub<4, INV, false, LOGN>(sm, 0, tid, d, (uint32_t)n, INV);
+  split_sub<LOGR, INV, false, LOGN>(sm, 0, tid, d, (uint32_t)n, INV);
   const uint64_t q = d.m.q, q2 = 2 * q;
   ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + (size_t)row * n);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int i = tid + k * (n / 16);
+  for (int k = 0; k < NP; ++k) {
+    const int i = tid + k * NT;
     uint64_t x = sm[spad(2 * i)], y = sm[spad(2 * i + 1)];
     if (!INV) {
       x = x >= q2 ? x - q2 : x;
       y = y >= q2 ? y - q2 : y;
     }
-    d2[i] = make_ulonglong2(csub(x, q), csub(y, q));
+    xin[k] = make_ulonglong2(csub(x, q), csub(y, q));
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) d2[tid + k * NT] = xin[k];
+}
+
+// Radix of the row kernels' register phases (2^LOGR elements per thread,
+// n / 2^LOGR threads per row). Measured on the B200 at 512 rows: n = 4096
+// radix 8 (512 threads) 32.8 us vs radix 16 34.8 us forward; n = 2048 equal
+// at 8/16 and slower at 4. FHE_NTT_ROW_LOGR overrides it for A/B checks.
+static int row_logr(int logn) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_NTT_ROW_LOGR");
+    v = e ? atoi(e) : 0;
+    if (v < 2 || v > 4) v = 0;
+  }
+  return v ? v : (logn == 12 ? 3 : 4);
+}
+
+template <bool INV, int LOGN>
+static void launch_row(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, cudaStream_t st) {
+  constexpr int n = 1 << LOGN;
+  const size_t smem = (size_t)(n + (n >> 4) + 1) * sizeof(uint64_t);
+  switch (row_logr(LOGN)) {
+    case 2: ntt_row_kernel<INV, LOGN, 2><<<rows, n >> 2, smem, st>>>(ls, lm, dst); break;
+    case 3: ntt_row_kernel<INV, LOGN, 3><<<rows, n >> 3, smem, st>>>(ls, lm, dst); break;
+    default: ntt_row_kernel<INV, LOGN, 4><<<rows, n >> 4, smem, st>>>(ls, lm, dst); break;
   }
 }
 
@@ -566,11 +605,10 @@ static int launch(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows,
   while ((1 << logn) < n) ++logn;
   if (logn >= kSplitMinLog && split_enabled()) return launch_split<INV>(ls, lm, dst, rows, logn, st);
   if ((logn == 11 || logn == 12) && split_enabled()) {  // FHE_NTT_SPLIT=0 also selects the generic row kernel
-    const size_t smem = (size_t)(n + (n >> 4) + 1) * sizeof(uint64_t);
     if (logn == 11)
-      ntt_row_kernel<INV, 11><<<rows, n / 16, smem, st>>>(ls, lm, dst);
+      launch_row<INV, 11>(ls, lm, dst, rows, st);
     else
-      ntt_row_kernel<INV, 12><<<rows, n / 16, smem, st>>>(ls, lm, dst);
+      launch_row<INV, 12>(ls, lm, dst, rows, st);
     FHE_CHECK_LAUNCH("ntt_row_kernel");
     return FHE_OK;
   }

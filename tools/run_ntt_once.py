@@ -10,7 +10,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_2401_16732_b200 import _native, device, params  # noqa: E402
 
-N, L, B = 16384, 4, 64
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+L, B = 4, 64
 p = params.find_plaintext_modulus(N)
 limbs = params.limb_primes(N, p, L)
 rng = np.random.default_rng(2)

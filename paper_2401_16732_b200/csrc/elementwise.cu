@@ -344,27 +344,35 @@ __global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int log
       k1[i] = keys[((size_t)(l * ndig + i) * 2 + 1) * n + x];
     }
   }
-  // BCH ciphertexts per thread, fully unrolled: every gather of the chunk can
-  // be issued before the first multiply (memory-level parallelism); the key
-  // words stay in registers for all of them
+  // BCH ciphertexts per thread: every gather of the chunk (BCH x (ndig + 1)
+  // words) is issued as a predicated load before the first multiply, so they
+  // are all in flight together (memory-level parallelism); the key words stay
+  // in registers for all of them
+  uint64_t dv[BCH][MAXD], c0v[BCH];
+#pragma unroll
+  for (int bb = 0; bb < BCH; ++bb) {
+    const bool ok = b0 + bb < B;
+    const size_t crow = ((size_t)(b0 + bb) * L + l) * 2;
+    const size_t drow = ((size_t)(b0 + bb) * L + l) * ndig;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) dv[bb][i] = (ok && i < ndig) ? __ldg(&dig[(drow + i) * n + src]) : 0;
+    c0v[bb] = ok ? __ldg(&ct[crow * n + src]) : 0;
+  }
 #pragma unroll
   for (int bb = 0; bb < BCH; ++bb) {
     const int b = b0 + bb;
     if (b < B) {
       const size_t crow = ((size_t)b * L + l) * 2;
-      const size_t drow = ((size_t)b * L + l) * ndig;
       uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
 #pragma unroll
       for (int i = 0; i < MAXD; ++i) {
         if (i < ndig) {
-          const uint64_t dv = __ldg(&dig[(drow + i) * n + src]);
-          mac128(a0l, a0h, dv, k0[i]);
-          mac128(a1l, a1h, dv, k1[i]);
+          mac128(a0l, a0h, dv[bb][i], k0[i]);
+          mac128(a1l, a1h, dv[bb][i], k1[i]);
         }
       }
       // Σ_i D_i swk_i < ndig q^2 < q 2^64 (ndig < 2^64/q): one REDC each
-      const uint64_t c0p = __ldg(&ct[crow * n + src]);
-      out[crow * n + x] = csub(redc(a0l, a0h, m) + c0p, m.q);
+      out[crow * n + x] = csub(redc(a0l, a0h, m) + c0v[bb], m.q);
       out[(crow + 1) * n + x] = redc(a1l, a1h, m);
     }
   }
@@ -731,18 +739,22 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
       return fail(FHE_ERR_PARAMETER, "too many digits for one lazy REDC");
   if (!B) return FHE_OK;
 #ifndef FHE_KS_BCH
-#define FHE_KS_BCH 4
+#define FHE_KS_BCH 3
 #endif
-  constexpr int bchunk = FHE_KS_BCH;  // key words reused by bchunk ciphertexts; bchunk x ndig gathers in flight per thread
-  dim3 grid((n + 127) / 128, L, (B + bchunk - 1) / bchunk);
+  // key words reused by bchunk ciphertexts; bchunk x (ndig + 1) gathers in flight
+  // per thread (chunk shrinks with the digit count to bound registers)
+  constexpr int bchunk = FHE_KS_BCH;
+  constexpr int bch8 = bchunk > 2 ? bchunk / 2 : 1, bch16 = bchunk > 4 ? bchunk / 4 : 1;
+  const int bch = ndig <= 4 ? bchunk : ndig <= 8 ? bch8 : bch16;
+  dim3 grid((n + 127) / 128, L, (B + bch - 1) / bch);
   const int logn = log2i(n);
   cudaStream_t st = (cudaStream_t)stream;
   if (ndig <= 4)
     keyswitch_kernel<4, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else if (ndig <= 8)
-    keyswitch_kernel<8, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<8, bch8><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else if (ndig <= 16)
-    keyswitch_kernel<16, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<16, bch16><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else
     return fail(FHE_ERR_VALUE, "more than 16 digits unsupported");
   FHE_CHECK_LAUNCH("keyswitch_kernel");

@@ -173,6 +173,34 @@ __device__ __forceinline__ void mac128(uint64_t& lo, uint64_t& hi, uint64_t a, u
   asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(pl), "l"(ph));
 }
 
+// Column-split 128-bit accumulator for sums of up to 8 products of 60-bit
+// operands (u, v < 2^60): the 32x32 partial products go to separate columns —
+// lo*lo into a 96-bit carry chain, both cross products into one 64-bit word
+// (16 terms < 2^60 each), hi*hi into another (< 2^56 each) — so no 128-bit
+// carry propagation per product; acc60_get combines the columns once.
+struct Acc60 {
+  uint32_t s0, s1, s2;
+  uint64_t x, h;
+};
+__device__ __forceinline__ void acc60_zero(Acc60& a) {
+  a.s0 = a.s1 = a.s2 = 0;
+  a.x = a.h = 0;
+}
+__device__ __forceinline__ void mac60(Acc60& a, uint64_t u, uint64_t v) {
+  const uint32_t ul = (uint32_t)u, uh = (uint32_t)(u >> 32), vl = (uint32_t)v, vh = (uint32_t)(v >> 32);
+  asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\tmadc.hi.cc.u32 %1, %3, %4, %1;\n\taddc.u32 %2, %2, 0;"
+      : "+r"(a.s0), "+r"(a.s1), "+r"(a.s2)
+      : "r"(ul), "r"(vl));
+  a.x += (uint64_t)ul * vh;
+  a.x += (uint64_t)uh * vl;
+  a.h += (uint64_t)uh * vh;
+}
+__device__ __forceinline__ void acc60_get(const Acc60& a, uint64_t& lo, uint64_t& hi) {
+  const uint64_t l = ((uint64_t)a.s1 << 32) | a.s0;
+  lo = l + (a.x << 32);
+  hi = a.h + a.s2 + (a.x >> 32) + (lo < l ? 1ull : 0ull);
+}
+
 // x mod q for any x < 2^64 (q < 2^63): quotient estimate off by at most 1
 __device__ __forceinline__ uint64_t reduce_u64(uint64_t x, const ModDesc& m) {
   uint64_t qt = __umul64hi(x, m.inv64);

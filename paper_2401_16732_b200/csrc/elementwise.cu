@@ -161,7 +161,8 @@ __global__ void automorphism_kernel(const ModSet ms, RowGeom g, uint64_t gpow,
   int64_t bb;
   int l, p;
   g.split(r, bb, l, p);
-  const uint64_t e = (i * (gpow % (2ull * n))) % (2ull * n);
+  const uint64_t mask2n = 2ull * n - 1;  // mod 2n as a mask (n is a power of two)
+  const uint64_t e = (i * (gpow & mask2n)) & mask2n;
   const uint64_t v = a[idx];
   const bool neg = e >= (uint64_t)n;
   out[(r << g.logn) + (e & (n - 1))] = (neg && v) ? ms.m[l].q - v : v;
@@ -318,7 +319,7 @@ __global__ void act_server_kernel(ModDesc mp, uint64_t two_f, const uint64_t* __
 // One thread per (position x, limb l, batch chunk): the 2*ndig key words of x
 // stay in registers and are reused by every ciphertext of the chunk (the key
 // is read from HBM once per chunk, not once per ciphertext).
-template <int MAXD, int BCH>
+template <int MAXD, int BCH, bool W60>
 __global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int logn, int L, int B, int ndig,
                                                         uint64_t gpow, const uint64_t* __restrict__ ct,
                                                         const uint64_t* __restrict__ dig,
@@ -334,7 +335,8 @@ __global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int log
   // consecutive x gather from 32 distinct slots of two aligned 128-byte lines
   // (the map permutes within blocks), so the gathers stay coalesced.
   const uint32_t e = 2u * brev_bits((uint32_t)x, logn) + 1u;
-  const uint32_t e2 = (uint32_t)(((uint64_t)e * (gpow % (2ull * n))) % (2ull * n));
+  const uint32_t mask2n = 2u * (uint32_t)n - 1u;  // 2n is a power of two: mod 2n is a mask
+  const uint32_t e2 = (uint32_t)(((uint64_t)e * (gpow & mask2n)) & mask2n);
   const int src = (int)brev_bits((e2 - 1u) >> 1, logn);
   uint64_t k0[MAXD], k1[MAXD];
 #pragma unroll
@@ -364,11 +366,26 @@ __global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int log
     if (b < B) {
       const size_t crow = ((size_t)b * L + l) * 2;
       uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+      if constexpr (W60) {  // q < 2^60, ndig <= 8: column-split accumulation
+        Acc60 s0, s1;
+        acc60_zero(s0);
+        acc60_zero(s1);
 #pragma unroll
-      for (int i = 0; i < MAXD; ++i) {
-        if (i < ndig) {
-          mac128(a0l, a0h, dv[bb][i], k0[i]);
-          mac128(a1l, a1h, dv[bb][i], k1[i]);
+        for (int i = 0; i < MAXD; ++i) {
+          if (i < ndig) {
+            mac60(s0, dv[bb][i], k0[i]);
+            mac60(s1, dv[bb][i], k1[i]);
+          }
+        }
+        acc60_get(s0, a0l, a0h);
+        acc60_get(s1, a1l, a1h);
+      } else {
+#pragma unroll
+        for (int i = 0; i < MAXD; ++i) {
+          if (i < ndig) {
+            mac128(a0l, a0h, dv[bb][i], k0[i]);
+            mac128(a1l, a1h, dv[bb][i], k1[i]);
+          }
         }
       }
       // Σ_i D_i swk_i < ndig q^2 < q 2^64 (ndig < 2^64/q): one REDC each
@@ -446,9 +463,10 @@ __global__ void __launch_bounds__(kRotX) rot_pmac_kernel(const ModDesc m, int lo
       r1 = c[n + x];
     } else {
       // eval_perm (ring.py:199-202): exp_at_index[x] = 2 bitrev(x) + 1
-      const uint64_t gp = __ldg(&gpow[g]) % (2ull * n);
+      const uint64_t mask2n = 2ull * n - 1;  // mod 2n as a mask (n is a power of two)
+      const uint64_t gp = __ldg(&gpow[g]) & mask2n;
       const uint32_t e = 2u * brev_bits((uint32_t)x, logn) + 1u;
-      const uint32_t e2 = (uint32_t)(((uint64_t)e * gp) % (2ull * n));
+      const uint32_t e2 = (uint32_t)(((uint64_t)e * gp) & mask2n);
       const int src = (int)brev_bits((e2 - 1u) >> 1, logn);
       const uint64_t* dg = D + (size_t)gi.x * ndig * n;
       const uint64_t* kk = K + (size_t)gi.y * ndig * 2 * n;
@@ -749,12 +767,18 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
   dim3 grid((n + 127) / 128, L, (B + bch - 1) / bch);
   const int logn = log2i(n);
   cudaStream_t st = (cudaStream_t)stream;
-  if (ndig <= 4)
-    keyswitch_kernel<4, bchunk><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+  bool w60 = ndig <= 8;  // column-split MACs need every modulus below 2^60
+  for (int l = 0; l < L; ++l) w60 = w60 && ms.m[l].q < (1ull << 60);
+  if (ndig <= 4 && w60)
+    keyswitch_kernel<4, bchunk, true><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+  else if (ndig <= 4)
+    keyswitch_kernel<4, bchunk, false><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+  else if (ndig <= 8 && w60)
+    keyswitch_kernel<8, bch8, true><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else if (ndig <= 8)
-    keyswitch_kernel<8, bch8><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<8, bch8, false><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else if (ndig <= 16)
-    keyswitch_kernel<16, bch16><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
+    keyswitch_kernel<16, bch16, false><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, gpow, ct, digits, keys_mont, out);
   else
     return fail(FHE_ERR_VALUE, "more than 16 digits unsupported");
   FHE_CHECK_LAUNCH("keyswitch_kernel");

@@ -757,7 +757,7 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
       return fail(FHE_ERR_PARAMETER, "too many digits for one lazy REDC");
   if (!B) return FHE_OK;
 #ifndef FHE_KS_BCH
-#define FHE_KS_BCH 3
+#define FHE_KS_BCH 2
 #endif
   // key words reused by bchunk ciphertexts; bchunk x (ndig + 1) gathers in flight
   // per thread (chunk shrinks with the digit count to bound registers)

@@ -150,22 +150,26 @@ def test_config2_hrot_sweep(golden, N):
             assert sha(np.stack([o.c0.coeffs, o.c1.coeffs])) == hr["h:out"][str(st)]
 
 
-def test_hrot_batch_kernel_vs_oracle():
-    """K4 over a batch of ciphertexts sharing one key (the hoisted form)."""
-    from paper_2401_16732_b200 import bfv, params
+@pytest.mark.parametrize("T,B", [(16, 5), (16, 1), (8, 3), (4, 2)])
+def test_hrot_batch_kernel_vs_oracle(T, B):
+    """K4 over a batch of ciphertexts sharing one key (the hoisted form). T=16
+    (4 digits) and T=8 (8 digits, the most the column-split Acc60 MACs take)
+    run the 60-bit path, T=4 (15 digits) the 128-bit MAC path; odd batches
+    leave a partial 2-ciphertext chunk."""
+    from paper_2401_16732_b200 import bfv
 
     P = _P()
-    rng = np.random.default_rng(21)
+    rng = np.random.default_rng(21 + T)
     sk = bfv.keygen(P, rng)
-    swk = bfv.gen_switching_keys(sk, [3], rng)
-    B = 5
+    swk = bfv.gen_switching_keys(sk, [3], rng, decomp_log=T)
+    ndig = -(-Q.bit_length() // T)
     cts = rng.integers(0, Q, (B, 2, P.n), dtype=np.int64)
     t = torch.from_numpy(cts).cuda()
-    dig = bfv.key_digits_rows(t[:, 1].contiguous(), P, 16, 4)
+    dig = bfv.key_digits_rows(t[:, 1].contiguous(), P, T, ndig)
     out = bfv.keyswitch_rows(t, dig, 3, swk).cpu().numpy()
     g = O.galois_element(3, P.n)
     for b in range(B):
-        o0, o1 = O.hrot(cts[b, 0], cts[b, 1], g, swk.keys[3], 16, Q)
+        o0, o1 = O.hrot(cts[b, 0], cts[b, 1], g, swk.keys[3], T, Q)
         assert np.array_equal(out[b, 0], o0) and np.array_equal(out[b, 1], o1)
 
 

@@ -90,6 +90,41 @@ __global__ void mul_shoup_kernel(const ModSet ms, RowGeom g, int Bb, int Pb, con
   *reinterpret_cast<ulonglong2*>(out + idx) = z;
 }
 
+// pmult with one plaintext broadcast over the batch (Bb = 1, the common
+// case): each thread keeps its plaintext pair and companions in registers and
+// applies them to BCH ciphertexts, whose loads are all issued first — the
+// plaintext is read once per chunk and the row decomposition is done once.
+template <int BCH>
+__global__ void mul_shoup_bcast_kernel(const ModSet ms, int logn, int L, int P, int Pb, int B,
+                                       const uint64_t* __restrict__ a, const uint64_t* __restrict__ w,
+                                       const uint64_t* __restrict__ wp, uint64_t* __restrict__ out, int64_t inner2) {
+  const int64_t j2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pair index inside one batch slice
+  if (j2 >= inner2) return;
+  const int64_t j = 2 * j2;
+  const int rr = (int)(j >> logn);  // l * P + p
+  const int col = (int)(j & ((1 << logn) - 1));
+  const int p = rr % P, l = rr / P;
+  const int64_t rb = (int64_t)l * Pb + (p % Pb);
+  const uint64_t q = ms.m[l].q;
+  const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(w + (rb << logn) + col);
+  const ulonglong2 yp = *reinterpret_cast<const ulonglong2*>(wp + (rb << logn) + col);
+  const int b0 = blockIdx.y * BCH;
+  const int64_t slice = (int64_t)L * P << logn;  // words per batch entry
+  ulonglong2 x[BCH];
+#pragma unroll
+  for (int k = 0; k < BCH; ++k)
+    if (b0 + k < B) x[k] = *reinterpret_cast<const ulonglong2*>(a + (b0 + k) * slice + j);
+#pragma unroll
+  for (int k = 0; k < BCH; ++k) {
+    if (b0 + k < B) {
+      ulonglong2 z;
+      z.x = csub(shoup_lazy(x[k].x, y.x, yp.x, q), q);
+      z.y = csub(shoup_lazy(x[k].y, y.y, yp.y, q), q);
+      *reinterpret_cast<ulonglong2*>(out + (b0 + k) * slice + j) = z;
+    }
+  }
+}
+
 // w' = floor(w 2^64 / q_l) per word (one-time, when a plaintext is prepared)
 __global__ void shoup_companion_kernel(const ModSet ms, RowGeom g, const uint64_t* __restrict__ w,
                                        uint64_t* __restrict__ wp, int64_t total) {
@@ -537,6 +572,15 @@ int fhe_poly_mul_shoup(const uint64_t* moduli, int L, int B, int P, int n, const
   const int64_t total2 = (int64_t)B * L * P * n / 2;
   if (!total2) return FHE_OK;
   RowGeom g{L, P, log2i(n)};
+  if (Bb == 1 && B > 1 && (B + 3) / 4 <= 65535) {
+    constexpr int bch = 4;
+    const int64_t inner2 = (int64_t)L * P * n / 2;
+    dim3 grid((unsigned)((inner2 + kThreads - 1) / kThreads), (unsigned)((B + bch - 1) / bch));
+    mul_shoup_bcast_kernel<bch><<<grid, kThreads, 0, (cudaStream_t)stream>>>(ms, g.logn, L, P, Pb, B, a, w, w_shoup,
+                                                                             out, inner2);
+    FHE_CHECK_LAUNCH("mul_shoup_bcast_kernel");
+    return FHE_OK;
+  }
   mul_shoup_kernel<<<grid_for(total2), kThreads, 0, (cudaStream_t)stream>>>(ms, g, Bb, Pb, a, w, w_shoup, out,
                                                                              total2);
   FHE_CHECK_LAUNCH("mul_shoup_kernel");

@@ -147,6 +147,31 @@ def test_config2_pmult_add(golden, N):
     assert np.array_equal(o2.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("B,Pb", [(2, 1), (9, 2), (64, 1)])
+def test_pmult_shoup_batch_broadcast(B, Pb):
+    """Shoup pmult with one plaintext broadcast over the batch (the chunked
+    kernel: full and partial 4-ciphertext chunks, per-poly or shared plaintext)
+    equals the generic Barrett multiply word for word."""
+    import torch
+
+    from paper_2401_16732_b200 import _native, device, params, ring
+
+    N, L = 4096, 3
+    limbs = params.limb_primes(N, params.find_plaintext_modulus(N), L)
+    mods = _native.u64_array(limbs)
+    rng = np.random.default_rng(B * 10 + Pb)
+    x = np.stack([rng.integers(0, q, (B, 2, N), dtype=np.int64) for q in limbs], axis=1)  # [B][L][2][N]
+    w = np.stack([rng.integers(0, q, (Pb, N), dtype=np.int64) for q in limbs])[None]  # [1][L][Pb][N]
+    xd, wd = _dev(x), _dev(w)
+    wp = torch.empty_like(wd)
+    _native.call("fhe_shoup_companions", mods, L, 1, Pb, N, wd.data_ptr(), wp.data_ptr(), device.stream())
+    out = torch.empty_like(xd)
+    _native.call("fhe_poly_mul_shoup", mods, L, B, 2, N, xd.data_ptr(), wd.data_ptr(), wp.data_ptr(), 1, Pb,
+                 out.data_ptr(), device.stream())
+    ref = ring.binary_rows(_native.OP_MUL, xd, wd, N, limbs, P=2, Bb=1, Pb=Pb).cpu().numpy()
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
 def test_digit_ntt_vs_oracle():
     from paper_2401_16732_b200 import _native, device
 

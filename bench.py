@@ -128,6 +128,36 @@ def build_stack(workload: str, seed: int = 4):
     return P, layers
 
 
+WORKLOAD_NAMES = {
+    "config1": "config1: one 3x3 16->16 HE conv on 32x32",
+    "config3": "config3: ResNet-20 32x32x3 server-side HE conv stack",
+    "config4": "config4: ResNet-18 64x64x3 server-side HE conv stack",
+    "config5": "config5: ResNet-18 224x224x3 server-side HE conv stack (7x7 s2 stem, 2x2 pool reading A)",
+}
+
+
+def stack_meta(workload: str):
+    """Host-only geometry of the workload's conv layers (both arms)."""
+    from paper_2401_16732_b200 import conv, params, stacks
+
+    P = params.default_params()
+    out = []
+    for l in stacks.conv_layers(stacks.CONFIGS[workload]()):
+        lay = conv.layout_direct(P, l.H, l.W, l.f_w)
+        n_out = l.c_o * lay.frags
+        out.append((l, lay, n_out, n_out * l.c_i * l.f_w * l.f_w * 2 * P.n))
+    return P, out
+
+
+def config_dict(workload: str, world: int) -> dict:
+    """The `config` object of the JSON line — identical in both arms."""
+    P, meta = stack_meta(workload)
+    return {"workload": WORKLOAD_NAMES[workload], "conv_layers": len(meta),
+            "output_ciphertexts": int(sum(m[2] for m in meta)), "macs_60x8": int(sum(m[3] for m in meta)),
+            "n": P.n, "q_bits": P.q.bit_length(), "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"replicas x{world}"}
+
+
 def _traffic(kernel: str):
     """DRAM bytes (read + write) per launch of `kernel` from the committed
     `ncu --set full` capture summarised in profiles/traffic.json (None if absent)."""
@@ -205,6 +235,20 @@ def run_peaks():
     return res
 
 
+def verify_outputs(layers) -> bool:
+    """The timed replays' outputs against the integer-pipe K1 kernel, which
+    shares no code with the tensor-core stack (outside the timed region)."""
+    import torch
+
+    ok = True
+    for L in layers:
+        want = L["plan"].run(L["dev"], torch.empty_like(L["out"]), path="int")
+        if not torch.equal(want, L["out"]):
+            print(f"bench: layer {L['layer'].name} output differs from the integer-pipe kernel", file=sys.stderr)
+            ok = False
+    return ok
+
+
 def time_steps(fn, steps, warmup, flush_buf=None):
     """Per-step CUDA-event timing on torch's current stream (the kernels' stream)."""
     import torch
@@ -225,37 +269,57 @@ def time_steps(fn, steps, warmup, flush_buf=None):
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def oracle_lib():
-    lib = ctypes.CDLL(str(ROOT / "oracle" / "liboracle.so"))
-    vp, i = ctypes.c_void_p, ctypes.c_int
-    lib.oracle_conv.restype = i
-    lib.oracle_conv.argtypes = [ctypes.c_uint64, i, vp, i, vp, i, i, vp, vp, i, i, vp, i, i]
-    return lib
+REF_SAMPLE_STRIDE = 8  # the CPU arms compute every 8th output ciphertext of every layer
 
 
-def cpu_baseline(P, layers, threads: int):
-    """C oracle (oracle/conv_oracle.c) on a bounded sample: per layer the
-    first `threads` output units, extrapolated to the full layer."""
-    lib = oracle_lib()
-    total = 0.0
-    sampled_units = 0
+def cpu_stack(workload: str, seed: int = 4):
+    """Seeded host inputs and the C oracle's contraction terms of every conv
+    layer (same draw order as build_stack, so both arms see the same data)."""
+    from oracle import c_oracle
+
+    P, meta = stack_meta(workload)
+    rng = np.random.default_rng(seed)
+    out = []
+    for l, lay, n_out, macs in meta:
+        w = rng.integers(-127, 128, (l.c_o, l.c_i, l.f_w, l.f_w), dtype=np.int64)
+        host = rng.integers(0, P.q, (lay.ct_count(l.c_i), 2, P.n), dtype=np.int64)
+        ld = {"w_p": lay.w_p, "tile": lay.tile, "c_n": lay.c_n, "frags": lay.frags}
+        src, step, fstride = c_oracle.conv_terms(ld, l.c_i, l.f_w)
+        out.append({"layer": l, "frags": lay.frags, "n_out": n_out, "w": w.reshape(l.c_o, -1), "host": host,
+                    "src": src, "step": step, "fstride": fstride,
+                    "sel": np.arange(0, n_out, REF_SAMPLE_STRIDE, dtype=np.int32)})
+    return P, out
+
+
+def cpu_step(P, layers, threads: int):
+    """One step of the reference algorithm on the host (oracle/conv_oracle.c,
+    `threads` POSIX threads): every layer's extension build (all inputs, as
+    privinfer's conv_proposed does per call) and every REF_SAMPLE_STRIDE-th
+    output ciphertext. Returns (seconds, layers' worth of work done)."""
+    from oracle import c_oracle
+
+    t0 = time.perf_counter()
     for L in layers:
-        plan = L["plan"]
-        w = plan.w.cpu().numpy().astype(np.int16)
-        src = plan.src.cpu().numpy().astype(np.int32)
-        step = plan.step.cpu().numpy().astype(np.int32)
-        host = np.ascontiguousarray(L["host"]).view(np.uint64)
-        units = min(plan.n_out, threads)
-        out = np.zeros((units, 2, P.n), dtype=np.uint64)
-        t0 = time.perf_counter()
-        rc = lib.oracle_conv(ctypes.c_uint64(P.q), P.n, host.ctypes.data, host.shape[0], w.ctypes.data, plan.c_o,
-                             plan.K, src.ctypes.data, step.ctypes.data, plan.frags, plan.fstride, out.ctypes.data,
-                             threads, units)
-        dt = time.perf_counter() - t0
-        assert rc == 0
-        total += dt * plan.n_out / units
-        sampled_units += units
-    return total, sampled_units
+        c_oracle.conv(P.q, P.n, L["host"], L["w"], L["src"], L["step"], L["frags"], L["fstride"], threads=threads,
+                      units=L["sel"])
+    dt = time.perf_counter() - t0
+    return dt, sum(len(L["sel"]) / L["n_out"] for L in layers)
+
+
+def cpu_sample_note(threads: int) -> str:
+    return (f"oracle/conv_oracle.c on {threads} host threads; one step = every {REF_SAMPLE_STRIDE}th output "
+            f"ciphertext of every conv layer (about 1/{REF_SAMPLE_STRIDE} of the stack, measured, not "
+            "extrapolated: value = layers' worth of outputs computed / measured seconds) plus every layer's full "
+            "input extension build")
+
+
+def cpu_baseline(workload: str, threads: int, steps: int = 2):
+    P, layers = cpu_stack(workload)
+    cpu_step(P, layers, threads)  # warm (page-in)
+    runs = [cpu_step(P, layers, threads) for _ in range(steps)]
+    t = sum(r[0] for r in runs)
+    work = sum(r[1] for r in runs)
+    return work / t, t / steps
 
 
 # ------------------------------------------------------- config-2 sweep
@@ -289,7 +353,10 @@ def sub_benchmarks(steps, warmup, hbm, peaks=None):
                      "rows": rows, "N": N, "bound": "integer (butterfly)", "bfly_per_s": round(bfly, 1)}
         if peaks and peaks.get("butterfly"):
             res[name]["frac_butterfly"] = round(bfly / peaks["butterfly"], 3)
-    # rotation sweep: iNTT(c1) + l digit NTTs once (hoisted), then K4 per step
+    # rotation sweep: iNTT(c1) + l digit NTTs once (hoisted), then ONE
+    # multi-step K4 launch writing every step's rotated ciphertexts
+    import ctypes
+
     T, l = 16, 4
     rsteps = [1 << i for i in range(N.bit_length() - 2)]  # 1 .. N/4
     keys = {s: torch.from_numpy(np.stack([rng.integers(0, q, (l, 2, N), dtype=np.int64) for q in limbs])).cuda()
@@ -297,36 +364,47 @@ def sub_benchmarks(steps, warmup, hbm, peaks=None):
     c1 = t[:, :, 1].contiguous()
     coeff = torch.empty_like(c1)
     dig = torch.empty((B, L, l, N), dtype=torch.int64, device="cuda")
-    rot = torch.empty((B, L, 2, N), dtype=torch.int64, device="cuda")
+    rots = {s: torch.empty((B, L, 2, N), dtype=torch.int64, device="cuda") for s in rsteps}
     mods = _native.u64_array(limbs)
+    S = len(rsteps)
+    kptr = (ctypes.c_void_p * S)(*[keys[s].data_ptr() for s in rsteps])
+    gp = (ctypes.c_uint64 * S)(*[pow(3, s, 2 * N) for s in rsteps])
+    optr = (ctypes.c_void_p * S)(*[rots[s].data_ptr() for s in rsteps])
+
+    def switches():
+        _native.call("fhe_keyswitch_multi", mods, L, B, N, t.data_ptr(), dig.data_ptr(), l, S, kptr, gp, optr, st)
 
     def sweep():
         _native.call("fhe_ntt_inverse", plans, L, B, 1, c1.data_ptr(), coeff.data_ptr(), st)
         _native.call("fhe_ntt_forward_digits", plans, L, B, coeff.data_ptr(), dig.data_ptr(), T, l, st)
-        for s in rsteps:
-            _native.call("fhe_keyswitch_apply", mods, L, B, N, t.data_ptr(), dig.data_ptr(), keys[s].data_ptr(), l,
-                         pow(3, s, 2 * N), rot.data_ptr(), st)
-
-    def switches():
-        for s in rsteps:
-            _native.call("fhe_keyswitch_apply", mods, L, B, N, t.data_ptr(), dig.data_ptr(), keys[s].data_ptr(), l,
-                         pow(3, s, 2 * N), rot.data_ptr(), st)
+        switches()
 
     ms = time_steps(switches, max(2, steps // 2), warmup, flush)
     avg_ks = sum(ms) / len(ms) * 1e-3
     ms = time_steps(sweep, max(2, steps // 2), warmup, flush)
     avg = sum(ms) / len(ms) * 1e-3
     ct_limbs = B * L
-    # per rotation: read c0 + l digit rows (gather) + write 2 rows; keys once per batch
-    alg = len(rsteps) * (ct_limbs * 8 * N * (1 + l + 2) + L * 2 * l * 8 * N) + ct_limbs * 8 * N * (2 + 2 * l)
-    gbs = alg / avg / 1e9
-    res["rotation_sweep"] = {"gbs": round(gbs, 1), "ms": round(avg * 1e3, 3), "frac_hbm": round(gbs / hbm, 3),
-                             "rotations": len(rsteps) * B, "rot_per_s": round(len(rsteps) * B / avg, 1),
-                             "N": N, "L": L, "B": B, "T": T}
-    alg_ks = len(rsteps) * (ct_limbs * 8 * N * (1 + l + 2) + L * 2 * l * 8 * N)
-    res["keyswitch_only"] = {"gbs": round(alg_ks / avg_ks / 1e9, 1), "ms": round(avg_ks * 1e3, 3),
-                             "frac_hbm": round(alg_ks / avg_ks / 1e9 / hbm, 3), "launches": len(rsteps),
-                             "note": "the sweep's 13 key-switch launches alone (digits already in EVAL form)"}
+    row = 8 * N
+    # SURVEY §8d K4 bytes per (ct-limb, step): 8N (2 in + 2 out) + 2l·8N/B
+    alg_ks = S * (ct_limbs * row * 4 + L * 2 * l * row)
+    # bytes the multi-step kernel must move: c0 + l digit rows once per
+    # ct-limb, every step's keys once, 2 output rows per (ct-limb, step)
+    moved_ks = ct_limbs * row * (1 + l) + S * L * 2 * l * row + S * ct_limbs * 2 * row
+    # hoisted part: iNTT of c1 (r+w) and l digit NTTs (read c1 coeffs, write l rows)
+    hoist = ct_limbs * row * 2 + ct_limbs * row * (1 + l)
+    res["rotation_sweep"] = {"ms": round(avg * 1e3, 3), "rotations": S * B, "rot_per_s": round(S * B / avg, 1),
+                             "gbs_alg": round((alg_ks + hoist) / avg / 1e9, 1),
+                             "gbs_moved": round((moved_ks + hoist) / avg / 1e9, 1),
+                             "frac_hbm_moved": round((moved_ks + hoist) / avg / 1e9 / hbm, 3),
+                             "N": N, "L": L, "B": B, "T": T, "steps": S,
+                             "note": "iNTT(c1) + digit NTTs once, then one fhe_keyswitch_multi launch"}
+    res["keyswitch_only"] = {"ms": round(avg_ks * 1e3, 3), "launches": 1,
+                             "gbs_alg_s8d": round(alg_ks / avg_ks / 1e9, 1),
+                             "frac_hbm_alg_s8d": round(alg_ks / avg_ks / 1e9 / hbm, 3),
+                             "gbs_moved": round(moved_ks / avg_ks / 1e9, 1),
+                             "frac_hbm_moved": round(moved_ks / avg_ks / 1e9 / hbm, 3),
+                             "note": "keyswitch_multi_kernel over the 13-step sweep (digits already in EVAL form); "
+                                     "alg = SURVEY §8d bytes, moved = c0 + digits once, keys once, outputs"}
     res["config2_sweep"] = config2_sweep()
     res["conv_vs_conventional"] = conventional_vs_proposed(steps, warmup)
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
@@ -358,8 +436,10 @@ def inference_chain(name):
         t = {}
         got = inference.he_forward(layers, x, weights, sk, rng, P, timings=t, specs=specs)
         ok = bool(np.array_equal(got, inference.plain_forward(layers, x, weights, P.p)))
+        per_conv = t.pop("per_conv_s")
         out = {"convs": len(convs), "logits": int(fc.c_o), "bit_exact_vs_integer_model": ok,
                **{k: round(v * 1e3, 2) for k, v in t.items()}}
+        out["per_conv_ms"] = [round(v * 1e3, 3) for v in per_conv]
         out = {k.replace("_s", "_ms") if k.endswith("_s") else k: v for k, v in out.items()}
     out["online_ms"] = round(out["conv_ms"] + out["act_ms"] + out["repack_ms"] + out["tail_ms"], 2)
     return out
@@ -583,7 +663,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config4", choices=["config1", "config3", "config4", "config5"])
+    ap.add_argument("--workload", default="config5", choices=["config1", "config3", "config4", "config5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sub", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -688,6 +768,7 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
+    verified = verify_outputs(layers)
     launches = launches_per_step * args.steps
     per_step = [a.elapsed_time(b) for a, b in step_ms]
     total_ms = sum(per_step)
@@ -713,10 +794,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 mod q (60-bit) x s8",
             "data": "synthetic: seeded uniform ciphertexts mod q, seeded int weights in [-127,127]",
-            "config": {"workload": f"{args.workload}: ResNet-18 64x64x3 server-side HE conv stack"
-                       if args.workload == "config4" else args.workload,
-                       "conv_layers": n_layers, "macs_60x8": macs, "n": P.n, "q_bits": P.q.bit_length(),
-                       "l2": "flushed (256 MiB write) before every timed step", "parallelism": f"replicas x{world}"},
+            "config": config_dict(args.workload, world),
             "roofline": {"bound": "tensor", "kernel": "conv_tc_stack_kernel (K1-TC, tcgen05.mma.kind::i8)",
                          "achieved": round(achieved_tops, 2), "peak": round(peak_tops, 2), "unit": "TOPS (int8)",
                          "frac": round(achieved_tops / peak_tops, 4) if peak_tops else None,
@@ -731,6 +809,10 @@ def main():
                          "stack_vs_int_pipe_peak": round(macs / step_s / 1e12 / peak_tmac, 3),
                          "hbm_achieved_gbs": round(alg_bytes / step_s / 1e9, 1), "hbm_peak_gbs": hbm,
                          "hbm_peak_source": hbm_kind},
+            "verified": verified,
+            "verification": "after the timed loop: every layer's output of the last timed replay equals the "
+                            "integer-pipe K1 kernel (conv_flash_kernel, an independent implementation) on the "
+                            "same inputs, full arrays compared on the device",
             "gpu_launches": int(launches),
             "clocks": clocks,
             "peaks_measured": {k: v for k, v in peaks.items()},
@@ -758,12 +840,9 @@ def main():
         result["sub"] = sub_benchmarks(max(4, args.steps // 2), args.warmup, hbm, peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        est_s, units = cpu_baseline(P, layers, threads)
-        result["cpu_baseline"] = {
-            "value": round(n_layers / est_s, 5), "unit": "conv layers/s", "cores": threads, "kind": "port",
-            "sample": f"oracle/conv_oracle.c, first {threads} output ciphertexts of each layer "
-                      f"({units} units total), extrapolated per layer to the full stack",
-        }
+        v, step_s = cpu_baseline(args.workload, threads)
+        result["cpu_baseline"] = {"value": round(v, 5), "unit": "conv layers/s", "cores": threads, "kind": "port",
+                                  "sample": cpu_sample_note(threads), "ms_per_sample_step": round(step_s * 1e3, 1)}
     if rank == 0:
         print(json.dumps(result))
     if world > 1:
@@ -852,57 +931,23 @@ def e2e_arm(P, layers, steps, n_layers):
 
 def reference_arm(args, world):
     """The reference's CPU path (oracle/conv_oracle.c restatement, all host
-    threads) on a bounded sample of the same stack, same metric."""
-    import torch  # noqa: F401  (only for the ConvPlan host arrays, built on CPU below)
-
-    from paper_2401_16732_b200 import conv, params, stacks
-
-    P = params.default_params()
-    rng = np.random.default_rng(4)
-    lib = oracle_lib()
+    threads) on the same workload, metric and config: each step a bounded
+    sample of the stack (cpu_step)."""
     threads = os.cpu_count() or 1
-    layers = []
-    for l in stacks.conv_layers(stacks.CONFIGS[args.workload]()):
-        lay = conv.layout_direct(P, l.H, l.W, l.f_w)
-        w = rng.integers(-127, 128, (l.c_o, l.c_i, l.f_w, l.f_w), dtype=np.int64)
-        host = rng.integers(0, P.q, (lay.ct_count(l.c_i), 2, P.n), dtype=np.int64).view(np.uint64)
-        taps = l.f_w * l.f_w
-        j = np.repeat(np.arange(l.c_i), taps)
-        t = np.tile(np.arange(taps), l.c_i)
-        steps = conv._tap_steps(lay, l.f_w)
-        if lay.fragmented:
-            src, fs, st = j * lay.frags, 1, steps[t]
-        else:
-            src, fs, st = j // lay.c_n, 0, steps[t] + lay.tile * (j % lay.c_n)
-        layers.append((l, lay, w.reshape(l.c_o, -1).astype(np.int16), src.astype(np.int32), st.astype(np.int32),
-                       fs, host))
-
-    def one_step():
-        est = 0.0
-        for l, lay, w, src, st, fs, host in layers:
-            n_out = l.c_o * lay.frags
-            units = min(n_out, threads)
-            out = np.zeros((units, 2, P.n), dtype=np.uint64)
-            t0 = time.perf_counter()
-            lib.oracle_conv(ctypes.c_uint64(P.q), P.n, host.ctypes.data, host.shape[0], w.ctypes.data, l.c_o,
-                            w.shape[1], src.ctypes.data, st.ctypes.data, lay.frags, fs, out.ctypes.data, threads,
-                            units)
-            est += (time.perf_counter() - t0) * n_out / units
-        return est
-
+    P, layers = cpu_stack(args.workload)
     for _ in range(args.warmup):
-        one_step()
-    ests = [one_step() for _ in range(max(1, args.steps))]
-    est = sum(ests) / len(ests)
-    value = len(layers) / est
+        cpu_step(P, layers, threads)
+    runs = [cpu_step(P, layers, threads) for _ in range(max(1, args.steps))]
+    t = sum(r[0] for r in runs)
+    value = sum(r[1] for r in runs) / t
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "conv layers/s", "n_gpus": world,
-        "steps": len(ests), "warmup": args.warmup, "ms_per_step": round(est * 1e3, 2),
+        "steps": len(runs), "warmup": args.warmup, "ms_per_step": round(t / len(runs) * 1e3, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 mod q (60-bit) x s8",
-        "data": "synthetic: seeded uniform ciphertexts mod q, seeded int weights",
-        "config": {"workload": args.workload, "conv_layers": len(layers)},
+        "data": "synthetic: seeded uniform ciphertexts mod q, seeded int weights in [-127,127]",
+        "config": config_dict(args.workload, world),
         "cpu_baseline": {"value": round(value, 5), "unit": "conv layers/s", "cores": threads, "kind": "port",
-                         "sample": f"first {threads} output ciphertexts per layer, extrapolated to full layers"},
+                         "sample": cpu_sample_note(threads)},
         "e2e": {"value": round(value, 5), "unit": "conv layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

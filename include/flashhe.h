@@ -218,10 +218,11 @@ typedef struct fhe_conv_tc_layer {
  * X: DEVICE scratch of 3 operand buffers x_stride bytes apart (x_stride >= the
  *   largest layer's X; one buffer when nl == 1). Layer l uses buffer l % 3:
  *   layer l+1 is relaid out while layer l's GEMM runs.
- * sync: DEVICE uint64[3 + 24], zeroed once before first use: launch,
- *   relayout-done, GEMM-done and per-layer work counters. They only grow (graph-replay safe); reuse one
- *   sync buffer only for stacks with the same number of layers and never for
- *   launches that may run concurrently. */
+ * sync: DEVICE uint64[3 + 3*24], zeroed once before first use: the launch
+ *   counter and, per layer, work / relayout-done / GEMM-done counters. They
+ *   only grow (graph-replay safe); reuse one sync buffer only for stacks with
+ *   the same number of layers and never for launches that may run
+ *   concurrently. */
 int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl,
                       uint8_t* X, size_t x_stride, uint64_t* sync, void* stream);
 /* conv.avg_pool (conv.py:604-623): every row (polynomial) of in [rows][n]
@@ -257,6 +258,16 @@ int fhe_to_montgomery(const uint64_t* moduli, int L, int B, int P, int n,
 int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct,
                         const uint64_t* digits, const uint64_t* keys_mont, int ndig,
                         uint64_t gpow, uint64_t* out, void* stream);
+
+/* A whole rotation sweep in one launch (bfv.hrot for S steps of the same
+ * ciphertexts, bfv.py:467-500; the digit NTTs of bfv.py:485-497 do not depend
+ * on the step and are computed once): for every step s, exactly
+ * fhe_keyswitch_apply(..., keys_mont[s], gpows[s], outs[s]). keys_mont / outs:
+ * HOST arrays of S DEVICE pointers ([L][ndig][2][n] keys, [B][L][2][n]
+ * outputs); gpows: HOST [S] Galois elements. ndig <= 8. */
+int fhe_keyswitch_multi(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct, const uint64_t* digits,
+                        int ndig, int S, const uint64_t* const* keys_mont, const uint64_t* gpows,
+                        uint64_t* const* outs, void* stream);
 
 /* Fused PMult-accumulate of the conventional convolution (conv.py:457-564:
  * the pmult + hadd chain per output ciphertext), EVAL domain, one launch:

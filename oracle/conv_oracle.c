@@ -31,6 +31,7 @@ typedef struct {
   uint64_t* out;
   int64_t* ext_lo; /* [n_in][2][3n] */
   int64_t* ext_hi;
+  const int32_t* sel; /* optional list of output units to compute (NULL: 0..total-1) */
   int next, total;
   pthread_mutex_t mu;
 } job_t;
@@ -51,7 +52,7 @@ static void build_ext(job_t* J, int r) {
   }
 }
 
-static void do_unit(job_t* J, int u, int64_t* alo, int64_t* ahi) {
+static void do_unit(job_t* J, int u, int row, int64_t* alo, int64_t* ahi) {
   const int n = J->n, o = u / J->frags, f = u % J->frags;
   for (int p = 0; p < 2; ++p) {
     memset(alo, 0, sizeof(int64_t) * n);
@@ -67,7 +68,7 @@ static void do_unit(job_t* J, int u, int64_t* alo, int64_t* ahi) {
         ahi[s] += hi[s] * w;
       }
     }
-    uint64_t* dst = J->out + ((size_t)u * 2 + p) * n;
+    uint64_t* dst = J->out + ((size_t)row * 2 + p) * n;
     for (int s = 0; s < n; ++s) {
       __int128 t = ((__int128)ahi[s] << LIMB) + alo[s];
       __int128 r = t % (__int128)J->q;
@@ -86,18 +87,16 @@ static void* worker(void* arg) {
     int u = J->next++;
     pthread_mutex_unlock(&J->mu);
     if (u >= J->total) break;
-    do_unit(J, u, alo, ahi);
+    do_unit(J, J->sel ? J->sel[u] : u, u, alo, ahi); /* row u of `out` */
   }
   free(alo);
   free(ahi);
   return NULL;
 }
 
-/* Returns 0 on success. `units` limits the computation to the first `units`
- * output units (a bounded sample for the CPU baseline); pass c_o*frags for all. */
-int oracle_conv(uint64_t q, int n, const uint64_t* in, int n_in, const int16_t* w, int c_o, int K,
-                const int32_t* src, const int32_t* step, int frags, int fstride, uint64_t* out,
-                int threads, int units) {
+static int run(uint64_t q, int n, const uint64_t* in, int n_in, const int16_t* w, int c_o, int K,
+               const int32_t* src, const int32_t* step, int frags, int fstride, uint64_t* out, int threads,
+               int total, const int32_t* sel) {
   job_t J;
   J.q = q;
   J.n = n;
@@ -111,16 +110,21 @@ int oracle_conv(uint64_t q, int n, const uint64_t* in, int n_in, const int16_t* 
   J.src = src;
   J.step = step;
   J.out = out;
+  J.sel = sel;
   J.next = 0;
+  J.total = total;
   for (int k = 0; k < K; ++k)
     if (step[k] <= -n || step[k] >= n) return 1;
+  for (int k = 0; k < K; ++k)
+    if (src[k] < 0 || src[k] + (frags - 1) * fstride >= n_in) return 3;
+  if (sel)
+    for (int i = 0; i < total; ++i)
+      if (sel[i] < 0 || sel[i] >= c_o * frags) return 4;
   J.ext_lo = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_in * 2 * 3 * n);
   J.ext_hi = (int64_t*)malloc(sizeof(int64_t) * (size_t)n_in * 2 * 3 * n);
   if (!J.ext_lo || !J.ext_hi) return 2;
   for (int r = 0; r < n_in; ++r) build_ext(&J, r);
   pthread_mutex_init(&J.mu, NULL);
-  J.total = c_o * frags;
-  if (units >= 0 && units < J.total) J.total = units; /* bounded sample: first `units` units */
   if (threads < 1) threads = 1;
   pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * threads);
   for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, worker, &J);
@@ -130,4 +134,24 @@ int oracle_conv(uint64_t q, int n, const uint64_t* in, int n_in, const int16_t* 
   free(J.ext_lo);
   free(J.ext_hi);
   return 0;
+}
+
+/* Returns 0 on success. `units` limits the computation to the first `units`
+ * output units (a bounded sample); pass c_o*frags (or -1) for all. */
+int oracle_conv(uint64_t q, int n, const uint64_t* in, int n_in, const int16_t* w, int c_o, int K,
+                const int32_t* src, const int32_t* step, int frags, int fstride, uint64_t* out,
+                int threads, int units) {
+  int total = c_o * frags;
+  if (units >= 0 && units < total) total = units;
+  return run(q, n, in, n_in, w, c_o, K, src, step, frags, fstride, out, threads, total, NULL);
+}
+
+/* The output units listed in `sel` (n_sel of them, any order): unit sel[i]
+ * is written to row i of `out` ([n_sel][2][n]). Used by the stacked-launch
+ * parity tests and the strided CPU-baseline sample. */
+int oracle_conv_units(uint64_t q, int n, const uint64_t* in, int n_in, const int16_t* w, int c_o, int K,
+                      const int32_t* src, const int32_t* step, int frags, int fstride, uint64_t* out,
+                      int threads, const int32_t* sel, int n_sel) {
+  if (!sel || n_sel < 0) return 4;
+  return run(q, n, in, n_in, w, c_o, K, src, step, frags, fstride, out, threads, n_sel, sel);
 }

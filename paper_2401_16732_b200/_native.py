@@ -77,6 +77,7 @@ SIGNATURES = {
     ),
     "fhe_to_montgomery": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_keyswitch_apply": (_int, [_vp, _int, _int, _int, _vp, _vp, _vp, _int, _u64, _vp, _vp]),
+    "fhe_keyswitch_multi": (_int, [_vp, _int, _int, _int, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
     "fhe_pmac": (_int, [_u64, _int, _vp, _vp, _vp, _vp, _int, _vp, _vp]),
     "fhe_rot_pmac": (
         _int,

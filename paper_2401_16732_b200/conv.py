@@ -261,12 +261,16 @@ class ConvPlan:
     def path(self) -> str:
         return "tc" if self.tc is not None and _conv_path() != "int" else "int"
 
-    def run(self, inp: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """inp: device [n_in, 2, n] -> out [c_o*frags, 2, n]."""
+    def run(self, inp: torch.Tensor, out: torch.Tensor | None = None, path: str | None = None) -> torch.Tensor:
+        """inp: device [n_in, 2, n] -> out [c_o*frags, 2, n]. `path` ("tc" |
+        "int") overrides the variant choice (both give identical results)."""
         inp = inp.contiguous()
         if out is None:
             out = torch.empty((self.n_out, 2, self.n), dtype=torch.int64, device=inp.device)
-        if self.path == "tc":
+        path = path or self.path
+        if path == "tc" and self.tc is None:
+            raise ParameterError("this layer has no tensor-core plan")
+        if path == "tc":
             return self.tc.run(inp, out)
         _native.call(
             "fhe_conv_flash", self.q, self.n, inp.data_ptr(), inp.shape[0], self.w.data_ptr(), self.c_o, self.K,
@@ -384,7 +388,7 @@ class ConvTcPlan:
         return out
 
 
-SYNC_WORDS = 3 + 24  # fhe_conv_tc_stack: launch, relayout, GEMM and per-layer work counters
+SYNC_WORDS = 3 + 3 * 24  # fhe_conv_tc_stack: launch counter + per-layer work / relayout-done / GEMM-done counters
 MAX_STACK = 24
 _stack_sync: dict[tuple, torch.Tensor] = {}
 
@@ -490,26 +494,49 @@ def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> C
     plan = ConvPlan(params.q, params.n, layer.weights.reshape(layer.c_o, -1), src, step,
                     frags=layout.frags, fstride=fstride, bias_delta=bias_delta, bias_mask=bias_mask)
     h = int(np.abs(steps).max(initial=0))
-    c_i = layer.c_i
-    if taps > 1 and -(-(c_i * taps) // 32) < -(-c_i // 32) * taps:
-        # Few input channels (the stems): fold the taps into the contraction —
-        # virtual channel (j, t) = channel j read at its tap's DRot offset, one
-        # tap with no halo. ceil(c_i·taps/32) MMAs per tile instead of
-        # ceil(c_i/32)·taps, and 7x7 stems fit the tensor-core path at all.
-        w3 = layer.weights.reshape(layer.c_o, c_i * taps, 1)
-        jj = np.repeat(np.arange(c_i), taps)
-        tt = np.tile(np.arange(taps), c_i)
-        if layout.fragmented:
-            chan = np.stack([jj * layout.frags, steps[tt]], 1)
+    fold = _tap_fold(layer.c_i, layer.f_w)
+    if fold == "none":
+        if ConvTcPlan.eligible(layer.weights, params.q, params.n, h, taps):
+            plan.tc = ConvTcPlan(params.q, params.n, layer.weights, steps, layout, plan.bias, plan.mask)
+    else:
+        # Few input channels (the stems): move taps into the contraction.
+        # "full": virtual channel (j, t) = channel j read at tap t's DRot
+        #   offset; one tap, no halo (3x3 stems: 27 channels, one MMA per stage).
+        # "rows": virtual channel (j, dy) = channel j read at row dy's offset
+        #   (dy - pad)·W_p; the f_w column taps stay descriptor offsets (halo
+        #   pad). The 7x7 stem folds 21 channels into ONE 32-channel block
+        #   instead of 147 into five: the digit-plane operand X is 5x smaller.
+        c_i, f, pad = layer.c_i, layer.f_w, layer.f_w // 2
+        if fold == "full":
+            v_steps, t_steps = steps, np.zeros(1, dtype=np.int64)
+            w3 = layer.weights.reshape(layer.c_o, c_i * taps, 1)
         else:
-            chan = np.stack([jj // layout.c_n, layout.tile * (jj % layout.c_n) + steps[tt]], 1)
-        if ConvTcPlan.eligible(w3, params.q, params.n, 0, 1):
-            plan.tc = ConvTcPlan(params.q, params.n, w3, np.zeros(1, dtype=np.int64), layout, plan.bias, plan.mask,
-                                 chan=chan)
-    elif ConvTcPlan.eligible(layer.weights, params.q, params.n, h, taps):
-        plan.tc = ConvTcPlan(params.q, params.n, layer.weights, steps, layout, plan.bias, plan.mask)
+            v_steps, t_steps = (np.arange(f) - pad) * layout.w_p, np.arange(f) - pad
+            w3 = layer.weights.reshape(layer.c_o, c_i * f, f)
+        nv = len(v_steps)
+        jj, tt = np.repeat(np.arange(c_i), nv), np.tile(np.arange(nv), c_i)
+        if layout.fragmented:
+            chan = np.stack([jj * layout.frags, v_steps[tt]], 1)
+        else:
+            chan = np.stack([jj // layout.c_n, layout.tile * (jj % layout.c_n) + v_steps[tt]], 1)
+        th = int(np.abs(t_steps).max(initial=0))
+        if ConvTcPlan.eligible(w3, params.q, params.n, th, len(t_steps)):
+            plan.tc = ConvTcPlan(params.q, params.n, w3, t_steps, layout, plan.bias, plan.mask, chan=chan)
     cache[key] = plan
     return plan
+
+
+def _tap_fold(c_i: int, f_w: int) -> str:
+    """How K1-TC lays out a layer's taps: "none" (channels in 32-wide blocks,
+    all taps as DRot descriptor offsets), "rows" or "full" (taps folded into
+    virtual channels). Fewest 32-channel blocks first (each block is one
+    digit-plane slab of X, written once and streamed by the GEMM), then the
+    fewest MMAs per tile (blocks x remaining taps)."""
+    taps = f_w * f_w
+    if taps == 1:
+        return "none"
+    cand = {"none": (-(-c_i // 32), taps), "rows": (-(-(c_i * f_w) // 32), f_w), "full": (-(-(c_i * taps) // 32), 1)}
+    return min(cand, key=lambda k: (cand[k][0], cand[k][0] * cand[k][1]))
 
 
 def _bias_mask(layout: TileLayout, frag: int) -> np.ndarray:
@@ -563,9 +590,9 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     up, down = _streams()
     up.wait_stream(comp)
     meta = [(x, layer, _proposed_plan(x, layer, params)) for x, layer in jobs]  # validate before enqueueing
-    need = max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0)
-    if need:
-        device.scratch("conv_tc_x", -(-need // 256) * 256)
+    need = -(-max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0) // 256) * 256
+    if need:  # issue_k1 (the non-fast jobs below) sizes the buffer 3x: do it once, before any job is enqueued
+        device.scratch("conv_tc_x", 3 * need)
     # all of the call's host outputs in one pinned allocation (one allocator call, not one per job)
     sizes = [plan.n_out * 2 * params.n for *_, plan in meta]
     host_all = torch.empty(sum(sizes), dtype=torch.int64, pin_memory=True)
@@ -575,7 +602,6 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     ev_up, ev_comp = torch.cuda.Event(), torch.cuda.Event()
     ev_up.record(comp)  # create the cudaEvent handles (torch makes them on first record)
     ev_comp.record(comp)
-    X = device.scratch("conv_tc_x", -(-need // 256) * 256) if need else 0
     for (x, layer, plan), hv in zip(meta, views):  # one pass: job i's download is enqueued before job i+1's upload
         ready = None
         rows_in = x.cts.rows if isinstance(x.cts, bfv.CtStack) else None
@@ -583,12 +609,19 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
             # host-resident pinned input: upload, K1 and download in one C call (one
             # ctypes crossing per job instead of ~10 torch/ctypes calls)
             pin = rows_in._pinned
-            inp = torch.empty((pin.numel() // (2 * params.n), 2, params.n), dtype=torch.int64, device=comp.device)
+            # inp is written by the upload stream: allocate it there (its block is
+            # then never handed out while a pending copy on `up` could still write
+            # it) and tell the allocator the compute stream reads it
+            with torch.cuda.stream(up):
+                inp = torch.empty((pin.numel() // (2 * params.n), 2, params.n), dtype=torch.int64,
+                                  device=comp.device)
+            inp.record_stream(comp)
             out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=comp.device)
             lay = (_native.ConvTcLayer * 1)(plan.tc.layer(inp, out))
             sync = _stack_sync_for([plan.tc])
+            X = device.scratch("conv_tc_x", 3 * need)  # already sized: never reallocated here
             rc = fast(params.q, params.n, lay, pin.data_ptr(), pin.numel() * 8, hv.data_ptr(), hv.numel() * 8, X,
-                      -(-need // 256) * 256, sync.data_ptr(), up.cuda_stream, comp.cuda_stream, down.cuda_stream,
+                      need, sync.data_ptr(), up.cuda_stream, comp.cuda_stream, down.cuda_stream,
                       ev_up.cuda_event, ev_comp.cuda_event)
             if rc:
                 _native.check(rc)

@@ -87,9 +87,12 @@ struct LayerDesc {
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
 
+constexpr int kRdy = 3 + kMaxLayers;      // sync index of layer 0's relayout-done counter
+constexpr int kGem = 3 + 2 * kMaxLayers;  // sync index of layer 0's GEMM-done counter
+
 struct StackArgs {
   LayerDesc L[kMaxLayers];
-  unsigned long long* sync;  // [0] launches, [1] relayout done, [2] GEMM done, [3 + l] unit counters
+  unsigned long long* sync;  // 3 + 3 * kMaxLayers counters (see the protocol note below)
   uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
   int n, nl;
 };
@@ -380,16 +383,19 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
 // resident) and all spins are bounded (a protocol bug traps, never hangs).
 // P(l) = warps per CTA that relayout layer l: epilogue + relayout warps for
 // layer 0 (nothing else to do yet), the kRelWarps relayout warps afterwards.
-//   sync[0]      launch arrivals: epoch e = arrivals / gridDim.x + 1
-//   sync[1]      relayout completions (one per participating warp): layer
-//                l's X is ready when it reaches
-//                (e-1)·G·(P(0) + kRelWarps·(nl-1)) + G·(P(0) + kRelWarps·l)
-//   sync[2]      GEMM completions (one per CTA per layer): layer l's X has
-//                been fully consumed at (e-1)·G·nl + G·(l+1)
-//   sync[3 + l]  layer l's relayout work counter, taken g = kUnitsPerGrab
-//                units at a time: launch e starts at
-//                (e-1)·(g·ceil(units/g) + g·G·P(l)) (each participating warp
-//                overshoots it exactly once)
+//   sync[0]             launch arrivals: epoch e = arrivals / gridDim.x + 1
+//   sync[3 + l]         layer l's relayout work counter (dynamic relayout
+//                       mode only), taken g = kUnitsPerGrab units at a time:
+//                       launch e starts at (e-1)·(g·ceil(units/g) + g·G·P(l))
+//                       (each participating warp overshoots it exactly once)
+//   sync[kRdy + l]      layer l's relayout completions (one per participating
+//                       warp): its X is complete at e·G·P(l)
+//   sync[kGem + l]      layer l's GEMM completions (one per CTA): its X has
+//                       been fully consumed at e·G
+// Every layer has its OWN completion counters: warps and CTAs run ahead by
+// up to three layers, so a shared running count can reach "layer l done"
+// while a slow CTA is still on layer l (the config-5 stack, whose 80-fragment
+// stem is relaid out next to two small layers, showed exactly that).
 // The relayout warps run up to three layers ahead of the GEMM: layer l's X
 // buffer (three rotate) is overwritten only after every CTA finished the
 // GEMM of layer l-3. The loader waits for "X ready" before layer l's first
@@ -482,10 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   const unsigned long long e1 = slot[1];  // epoch - 1
   constexpr int P0 = kEpiWarps + kRelWarps;  // warps per CTA relaying out layer 0
   const unsigned long long Gu = (unsigned long long)G;
-  auto ready_target = [&](int l) {
-    return e1 * Gu * (P0 + kRelWarps * (nl - 1)) + Gu * (P0 + kRelWarps * l);
-  };
-  auto gemm_target = [&](int l) { return e1 * Gu * nl + Gu * (l + 1); };
+  auto ready_target = [&](int l) { return (e1 + 1) * Gu * (l == 0 ? P0 : kRelWarps); };
+  auto gemm_target = [&](int) { return (e1 + 1) * Gu; };
   // relayout units of layer l until none is left, then publish this warp's completion
   // relayout units of layer l until none is left, then publish this warp's
   // completion. The next grab's atomic is issued before the current unit is
@@ -510,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
       asm volatile("fence.proxy.async.shared::cta;");
       __threadfence();
       __syncwarp();
-      if (lane == 0) atomicAdd(A.sync + 1, 1ull);
+      if (lane == 0) atomicAdd(A.sync + kRdy + l, 1ull);
       return;
     }
 #endif
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
     asm volatile("fence.proxy.async.shared::cta;");  // (epilogue warps) ring staging before later bulk copies
     __threadfence();  // this warp's X stores before its completion count
     __syncwarp();
-    if (lane == 0) atomicAdd(A.sync + 1, 1ull);
+    if (lane == 0) atomicAdd(A.sync + kRdy + l, 1ull);
   };
 
   if (warp == 0) {
@@ -644,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
           s_ld = 0;
           prev_sb = d.stage_bytes;
         }
-        wait_count(A.sync + 1, ready_target(l));    // layer l's X is complete
+        wait_count(A.sync + kRdy + l, ready_target(l));  // layer l's X is complete
         TC_TRACE(7, l);
         asm volatile("fence.proxy.async.global;");  // generic-proxy X stores -> cp.async.bulk reads
         const uint32_t wstage = (uint32_t)d.taps * kWTap;
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         if (l + 1 < nl) prefetch_l2(A.L[l + 1].in, A.L[l + 1].in_bytes);
         prefetch_l2(A.L[l].W, A.L[l].w_bytes);
       }
-      if (l >= 3) wait_count(A.sync + 2, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
+      if (l >= 3) wait_count(A.sync + kGem + l - 3, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
       relayout_layer(l, kRelWarps);
       if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(3, l);
     }
@@ -785,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
       }
       // this CTA consumed all of layer l's X (every tile's MMAs completed)
       asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue));
-      if (tid == 64) atomicAdd(A.sync + 2, 1ull);
+      if (tid == 64) atomicAdd(A.sync + kGem + l, 1ull);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

@@ -3,6 +3,8 @@
 // All HBM-bound single passes: 128-bit coalesced rows where the access is
 // affine, scalar 64-bit gathers where it is a permutation (DRot, automorphism,
 // eval-domain Galois map).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fhe {
@@ -430,6 +432,110 @@ __global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int log
   }
 }
 
+// K4 over a whole rotation sweep (bfv.hrot over several steps, bfv.py:467-500,
+// with the step-independent digit NTTs of :485-497 hoisted): one launch writes
+// every step's rotated ciphertexts. A thread owns one coefficient x of one limb
+// for BCH ciphertexts and walks the steps; its ciphertexts' c0 and digit rows
+// are fetched from HBM by the first step and re-gathered from L2 by the others
+// (blocks are ordered x-fastest, then chunk, then limb, so the resident CTAs
+// work on a few chunks of ONE limb: their digit rows and that limb's keys stay
+// L2-resident). Step s+1's key words and gathers are issued before step s's
+// multiply-accumulates (software pipelining keeps two steps of loads in flight).
+constexpr int kKsMaxSteps = 32;
+struct KsSteps {
+  const uint64_t* keys[kKsMaxSteps];  // [L][ndig][2][n] Montgomery form, per step
+  uint64_t* out[kKsMaxSteps];         // [B][L][2][n] per step
+  uint32_t gpow[kKsMaxSteps];         // Galois element mod 2n per step
+  int S;
+};
+
+template <int MAXD, int BCH>
+struct KsLoads {
+  uint64_t k0[MAXD], k1[MAXD], dv[BCH][MAXD], c0[BCH];
+};
+
+template <int MAXD, int BCH>
+__device__ __forceinline__ void ks_issue(KsLoads<MAXD, BCH>& v, const KsSteps& A, int s, int logn, int L, int B,
+                                         int ndig, int l, int b0, int x, uint32_t e,
+                                         const uint64_t* __restrict__ ct, const uint64_t* __restrict__ dig) {
+  const int n = 1 << logn;
+  const uint32_t mask2n = 2u * (uint32_t)n - 1u;
+  const uint32_t e2 = (e * A.gpow[s]) & mask2n;
+  const int src = (int)brev_bits((e2 - 1u) >> 1, logn);
+  const uint64_t* keys = A.keys[s];
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    v.k0[i] = i < ndig ? __ldg(&keys[((size_t)(l * ndig + i) * 2 + 0) * n + x]) : 0;
+    v.k1[i] = i < ndig ? __ldg(&keys[((size_t)(l * ndig + i) * 2 + 1) * n + x]) : 0;
+  }
+#pragma unroll
+  for (int bb = 0; bb < BCH; ++bb) {
+    const bool ok = b0 + bb < B;
+    const size_t drow = ((size_t)(b0 + bb) * L + l) * ndig;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) v.dv[bb][i] = (ok && i < ndig) ? __ldg(&dig[(drow + i) * n + src]) : 0;
+    v.c0[bb] = ok ? __ldg(&ct[((size_t)(b0 + bb) * L + l) * 2 * n + src]) : 0;
+  }
+}
+
+template <int MAXD, int BCH, bool W60>
+__device__ __forceinline__ void ks_finish(const KsLoads<MAXD, BCH>& v, uint64_t* __restrict__ out, int logn, int L,
+                                          int B, int ndig, int l, int b0, int x, const ModDesc& m) {
+  const int n = 1 << logn;
+#pragma unroll
+  for (int bb = 0; bb < BCH; ++bb) {
+    const int b = b0 + bb;
+    if (b >= B) continue;
+    uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+    if constexpr (W60) {
+      Acc60 s0, s1;
+      acc60_zero(s0);
+      acc60_zero(s1);
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i) {
+        if (i < ndig) {
+          mac60(s0, v.dv[bb][i], v.k0[i]);
+          mac60(s1, v.dv[bb][i], v.k1[i]);
+        }
+      }
+      acc60_get(s0, a0l, a0h);
+      acc60_get(s1, a1l, a1h);
+    } else {
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i) {
+        if (i < ndig) {
+          mac128(a0l, a0h, v.dv[bb][i], v.k0[i]);
+          mac128(a1l, a1h, v.dv[bb][i], v.k1[i]);
+        }
+      }
+    }
+    const size_t crow = ((size_t)b * L + l) * 2;
+    out[crow * n + x] = csub(redc(a0l, a0h, m) + v.c0[bb], m.q);
+    out[(crow + 1) * n + x] = redc(a1l, a1h, m);
+  }
+}
+
+template <int MAXD, int BCH, bool W60>
+__global__ void __launch_bounds__(128) keyswitch_multi_kernel(const ModSet ms, int logn, int L, int B, int ndig,
+                                                              const __grid_constant__ KsSteps A,
+                                                              const uint64_t* __restrict__ ct,
+                                                              const uint64_t* __restrict__ dig) {
+  const int n = 1 << logn;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int b0 = blockIdx.y * BCH;
+  const int l = blockIdx.z;
+  const ModDesc m = ms.m[l];
+  const uint32_t e = 2u * brev_bits((uint32_t)x, logn) + 1u;  // exp_at_index[x] (ring.py:114-116)
+  KsLoads<MAXD, BCH> cur, nxt;
+  ks_issue<MAXD, BCH>(cur, A, 0, logn, L, B, ndig, l, b0, x, e, ct, dig);
+  for (int s = 0; s < A.S; ++s) {
+    if (s + 1 < A.S) ks_issue<MAXD, BCH>(nxt, A, s + 1, logn, L, B, ndig, l, b0, x, e, ct, dig);
+    ks_finish<MAXD, BCH, W60>(cur, A.out[s], logn, L, B, ndig, l, b0, x, m);
+    cur = nxt;
+  }
+}
+
 // ---------------------------------------------------------------- K4b
 // Fused PMult-accumulate of the conventional convolution (conv.py:457-564):
 // out[o][p] = Σ_{(r, w) in terms(o)} R[r][p] ⊙ PT[w]   (mod q, EVAL domain)
@@ -826,6 +932,55 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
   else
     return fail(FHE_ERR_VALUE, "more than 16 digits unsupported");
   FHE_CHECK_LAUNCH("keyswitch_kernel");
+  return FHE_OK;
+}
+
+int fhe_keyswitch_multi(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct, const uint64_t* digits,
+                        int ndig, int S, const uint64_t* const* keys_mont, const uint64_t* gpows,
+                        uint64_t* const* outs, void* stream) {
+  if (int rc = check_rows(L, B, 2, n)) return rc;
+  if (ndig < 1 || ndig > 8) return fail(FHE_ERR_VALUE, "multi-step key switch takes 1..8 digits, got %d", ndig);
+  if (S < 0 || (S && (!keys_mont || !gpows || !outs))) return fail(FHE_ERR_VALUE, "bad step list");
+  ModSet ms;
+  if (int rc = make_modset(moduli, L, &ms)) return rc;
+  for (int l = 0; l < L; ++l)
+    if ((u128_t)ndig * ms.m[l].q >= ((u128_t)1 << 64))
+      return fail(FHE_ERR_PARAMETER, "too many digits for one lazy REDC");
+  for (int s = 0; s < S; ++s) {
+    if (!(gpows[s] & 1)) return fail(FHE_ERR_PARAMETER, "Galois element must be odd");
+    if (!keys_mont[s] || !outs[s]) return fail(FHE_ERR_VALUE, "null key or output of step %d", s);
+    if (outs[s] == ct) return fail(FHE_ERR_VALUE, "keyswitch cannot run in place");
+  }
+  if (!B || !S) return FHE_OK;
+  bool w60 = true;  // column-split MACs need every modulus below 2^60
+  for (int l = 0; l < L; ++l) w60 = w60 && ms.m[l].q < (1ull << 60);
+  const int logn = log2i(n);
+  cudaStream_t st = (cudaStream_t)stream;
+#ifndef FHE_KSM_BCH
+#define FHE_KSM_BCH 2
+#endif
+  constexpr int bch = FHE_KSM_BCH;
+  const dim3 grid((n + 127) / 128, (B + bch - 1) / bch, L);
+  for (int s0 = 0; s0 < S; s0 += kKsMaxSteps) {
+    KsSteps A;
+    A.S = std::min(kKsMaxSteps, S - s0);
+    for (int s = 0; s < A.S; ++s) {
+      A.keys[s] = keys_mont[s0 + s];
+      A.out[s] = outs[s0 + s];
+      A.gpow[s] = (uint32_t)(gpows[s0 + s] & (2ull * n - 1));
+    }
+    if (ndig <= 4 && w60)
+      keyswitch_multi_kernel<4, bch, true><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, A, ct, digits);
+    else if (ndig <= 4)
+      keyswitch_multi_kernel<4, bch, false><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, A, ct, digits);
+    else if (w60)
+      keyswitch_multi_kernel<8, 1, true><<<dim3((n + 127) / 128, B, L), 128, 0, st>>>(ms, logn, L, B, ndig, A, ct,
+                                                                                       digits);
+    else
+      keyswitch_multi_kernel<8, 1, false><<<dim3((n + 127) / 128, B, L), 128, 0, st>>>(ms, logn, L, B, ndig, A, ct,
+                                                                                        digits);
+    FHE_CHECK_LAUNCH("keyswitch_multi_kernel");
+  }
   return FHE_OK;
 }
 

@@ -79,9 +79,11 @@ _scratch: dict[tuple[int, str], torch.Tensor] = {}
 
 def scratch(name: str, nbytes: int) -> int:
     """Device pointer to a named per-device scratch buffer of >= nbytes.
-    Reuse is stream-ordered (every kernel runs on torch's current stream); the
-    buffer only grows, so pointers baked into a captured CUDA graph stay valid
-    once the largest user has run eagerly."""
+    Reuse is stream-ordered (every kernel runs on torch's current stream).
+    Growth replaces the buffer: pointers returned earlier (and CUDA graphs
+    that captured them) are then invalid. Callers size the buffer for their
+    largest use before they take pointers or capture, and growth is refused
+    during capture."""
     key = (torch.cuda.current_device(), name)
     t = _scratch.get(key)
     if t is None or t.numel() < nbytes:

@@ -94,6 +94,7 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
     seq, pool, fc = main_path(layers)
     specs = specs if specs is not None else layer_specs(layers, weights)
     t = dict(conv_s=0.0, act_s=0.0, offline_s=0.0, repack_s=0.0)
+    per_conv = []
     first = seq[0]
     t0 = time.perf_counter()
     cur = conv.pack_input(x, P, first.f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
@@ -116,6 +117,7 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
             y = conv.conv_proposed(cur, specs[l.name], P)
             torch.cuda.synchronize()
             t["conv_s"] += time.perf_counter() - t0
+            per_conv.append(time.perf_counter() - t0)
             if l.stride > 1:  # subsampled by the client's repack below
                 y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
             t0 = time.perf_counter()
@@ -148,6 +150,7 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
     t["tail_s"] = time.perf_counter() - t0
     if timings is not None:
         timings.update(t)
+        timings["per_conv_s"] = per_conv
     return out
 
 

@@ -206,3 +206,40 @@ def test_act2pc_end_to_end():
     assert np.array_equal(out.c1.coeffs, exp1)
     with pytest.raises(bfv.ProtocolError):
         act2pc.server_finalize(out, out, sess, P)  # session already DONE
+
+
+@pytest.mark.parametrize("N,L,B,ndig,S", [(4096, 4, 5, 4, 40), (16384, 2, 3, 4, 13), (2048, 1, 2, 8, 11),
+                                          (8192, 3, 1, 3, 7)])
+def test_keyswitch_multi_equals_per_step(N, L, B, ndig, S):
+    """fhe_keyswitch_multi (one launch for a whole rotation sweep, the digit
+    rows read once) equals S separate fhe_keyswitch_apply launches bit for
+    bit: several limbs, partial 2-ciphertext chunks, 3..8 digits (both MAC
+    widths: 60-bit limbs take the column-split path), and S > 32 steps
+    (split into launches of 32)."""
+    from paper_2401_16732_b200 import _native, device, params
+
+    p = params.find_plaintext_modulus(N)
+    limbs = params.limb_primes(N, p, L)
+    rng = np.random.default_rng(N + S)
+    cts = torch.from_numpy(np.stack([rng.integers(0, q, (B, 2, N), dtype=np.int64) for q in limbs], 1)).cuda()
+    dig = torch.from_numpy(np.stack([rng.integers(0, q, (B, ndig, N), dtype=np.int64) for q in limbs], 1)).cuda()
+    keys = [torch.from_numpy(np.stack([rng.integers(0, q, (ndig, 2, N), dtype=np.int64) for q in limbs])).cuda()
+            for _ in range(S)]
+    gp = [int(g) for g in (2 * rng.integers(0, N, S) + 1)]
+    mods = _native.u64_array(limbs)
+    st = device.stream()
+    want = []
+    for s in range(S):
+        o = torch.empty_like(cts)
+        _native.call("fhe_keyswitch_apply", mods, L, B, N, cts.data_ptr(), dig.data_ptr(), keys[s].data_ptr(), ndig,
+                     gp[s], o.data_ptr(), st)
+        want.append(o)
+    got = [torch.full_like(cts, -1) for _ in range(S)]
+    import ctypes
+
+    _native.call("fhe_keyswitch_multi", mods, L, B, N, cts.data_ptr(), dig.data_ptr(), ndig, S,
+                 (ctypes.c_void_p * S)(*[k.data_ptr() for k in keys]), (ctypes.c_uint64 * S)(*gp),
+                 (ctypes.c_void_p * S)(*[o.data_ptr() for o in got]), st)
+    torch.cuda.synchronize()
+    for s in range(S):
+        assert torch.equal(got[s], want[s]), f"step {s} (gpow {gp[s]}) differs"

@@ -1,0 +1,100 @@
+"""Parity of the STACKED tensor-core launch — the path bench.py times.
+
+conv.issue_k1 runs up to 24 independent conv layers as ONE
+conv_tc_stack_kernel launch: three rotating digit-plane buffers, relayout
+running up to three layers ahead of the GEMM, launch epochs on monotonic
+counters and tiles dealt round-robin over the whole stack. Every layer's
+output must equal (i) the same layer launched alone (nl = 1, the path the
+reference goldens pin in test_gpu_conv.py), (ii) the integer-pipe kernel
+(conv_flash_kernel, an independent implementation) and (iii) the C oracle
+(oracle/conv_oracle.c, pinned against the reference in
+test_oracle_golden.py) on sampled output units — eagerly, on repeated
+launches (epochs 1, 2, ...) and as CUDA-graph replays.
+Reference: privinfer conv.conv_proposed (conv.py:355-411).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import bench
+from oracle import c_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _layout_dict(lay):
+    return {"n": lay.n, "w_p": lay.w_p, "tile": lay.tile, "c_n": lay.c_n, "frags": lay.frags}
+
+
+def _oracle_check(P, L, out, rng, k=3):
+    lay, spec = L["layout"], L["spec"]
+    n_out = L["plan"].n_out
+    sel = np.unique(np.concatenate([[0, n_out - 1], rng.integers(0, n_out, k)]))
+    src, step, fstride = c_oracle.conv_terms(_layout_dict(lay), spec.c_i, spec.f_w)
+    want = c_oracle.conv(P.q, P.n, L["host"], spec.weights.reshape(spec.c_o, -1), src, step, lay.frags, fstride,
+                         threads=8, units=sel)
+    got = out[torch.from_numpy(sel).cuda()].cpu().numpy()
+    assert np.array_equal(got, want), f"{L['layer'].name}: stacked output differs from the C oracle"
+
+
+def _compare(layers, refs, tag):
+    for L, r in zip(layers, refs):
+        assert torch.equal(L["out"], r), f"{tag}: layer {L['layer'].name} differs from its single-layer launch"
+
+
+@pytest.mark.parametrize("workload", ["config4", "config5", "config3"])
+def test_stacked_launch_bit_exact(workload):
+    from paper_2401_16732_b200 import conv
+
+    P, layers = bench.build_stack(workload, seed=31)
+    assert all(L["plan"].path == "tc" for L in layers)
+    refs, ints = [], []
+    for L in layers:
+        refs.append(L["plan"].run(L["dev"], torch.empty_like(L["out"])))  # nl = 1
+        ints.append(L["plan"].run(L["dev"], torch.empty_like(L["out"]), path="int"))
+    torch.cuda.synchronize()
+    for L, r, i in zip(layers, refs, ints):
+        assert torch.equal(r, i), f"{L['layer'].name}: tensor-core and integer-pipe K1 differ"
+    items = [(L["plan"], L["dev"], None, L["out"]) for L in layers]
+    for rep in range(2):  # launch epochs 1 and 2 of this stack's counters
+        for L in layers:
+            L["out"].fill_(-1)
+        conv.issue_k1(items)
+        torch.cuda.synchronize()
+        _compare(layers, refs, f"eager launch {rep}")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+        conv.issue_k1(items)
+    torch.cuda.current_stream().wait_stream(side)
+    for rep in range(2):
+        for L in layers:
+            L["out"].fill_(-1)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        _compare(layers, refs, f"graph replay {rep}")
+    rng = np.random.default_rng(5)
+    for L in layers:
+        _oracle_check(P, L, L["out"], rng)
+
+
+def test_two_stacks_beyond_24_layers():
+    """More than MAX_STACK jobs: issue_k1 splits them into consecutive
+    launches (config 4's 20 layers + config 3's 21 = 41 jobs, 2 launches)
+    that share the digit-plane scratch."""
+    from paper_2401_16732_b200 import conv
+
+    _, a = bench.build_stack("config4", seed=41)
+    _, b = bench.build_stack("config3", seed=42)
+    layers = a + b
+    refs = [L["plan"].run(L["dev"], torch.empty_like(L["out"])) for L in layers]
+    for rep in range(2):
+        for L in layers:
+            L["out"].fill_(-1)
+        ev = conv.issue_k1([(L["plan"], L["dev"], None, L["out"]) for L in layers])
+        assert len(set(map(id, ev))) == 2
+        torch.cuda.synchronize()
+        _compare(layers, refs, f"split launch {rep}")

@@ -202,3 +202,24 @@ def test_x2x_algebra():
     ct2 = (2 * a * r + 2 * r * r + v) % P
     c = O.x2x_server_const(r, r * r % P, v, P)
     assert np.array_equal((ct1 - ct2 + c) % P, (a * a + a) % P)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "r20_stem", "r20_s2", "r20_s3", "proj1x1", "frag64", "r18_8x8_512",
+                                  "vgg4x4", "stem7x7_224"])
+def test_c_oracle_matches_reference_conv(golden, name):
+    """oracle/conv_oracle.c (the CPU baseline and the --impl reference arm)
+    reproduces the reference's conv_proposed outputs (golden sha256)."""
+    from oracle import c_oracle
+
+    g = golden["conv"][name]
+    r = np.random.default_rng(g["seed"])
+    arr = r.integers(0, Q, (g["n_in"], 2, N), dtype=np.int64)
+    w = r.integers(-127, 128, (g["c_o"], g["c_i"], g["f_w"], g["f_w"]), dtype=np.int64)
+    src, step, fstride = c_oracle.conv_terms(g["layout"], g["c_i"], g["f_w"])
+    out = c_oracle.conv(Q, N, arr, w.reshape(g["c_o"], -1), src, step, g["layout"]["frags"], fstride, threads=4)
+    assert out.shape[0] == g["n_out"]
+    assert sha(out) == g["h:out"]
+    # a strided unit selection lands each unit in its own row
+    sel = np.arange(g["n_out"])[::-3][:5]
+    assert np.array_equal(c_oracle.conv(Q, N, arr, w.reshape(g["c_o"], -1), src, step, g["layout"]["frags"],
+                                        fstride, threads=2, units=sel), out[sel])

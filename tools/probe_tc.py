@@ -1,7 +1,7 @@
-"""Per-layer timing of K1 (tensor-core or integer path) on the config-4 layers.
+"""Per-layer timing of K1 (tensor-core or integer path) on a config's conv layers.
 
 Development probe (not part of the product or the bench contract):
-    python tools/probe_tc.py [--layer NAME] [--once]
+    python tools/probe_tc.py [--workload config4] [--layer NAME] [--once]
 """
 
 import argparse
@@ -20,11 +20,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layer", default=None, help="only this config-4 layer name")
     ap.add_argument("--once", action="store_true", help="one launch per layer (for ncu)")
+    ap.add_argument("--workload", default="config4")
     args = ap.parse_args()
     P = params.default_params()
     rng = np.random.default_rng(0)
     seen = set()
-    for l in stacks.conv_layers(stacks.config4()):
+    for l in stacks.conv_layers(stacks.CONFIGS[args.workload]()):
         key = (l.H, l.f_w, l.c_i, l.c_o)
         if key in seen or (args.layer and l.name != args.layer):
             continue

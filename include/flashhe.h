@@ -213,6 +213,11 @@ typedef struct fhe_conv_tc_layer {
   const uint64_t* bias_delta; /* DEVICE [c_o] or NULL (conv._bias_plaintext) */
   const uint8_t* bias_mask;   /* DEVICE [frags][n] slots that receive the bias */
   uint64_t* out;          /* DEVICE [c_o*frags][2][n] */
+  int rep;                /* 1 (or 0), 2 or 4: position groups stacked in the 128 accumulator
+                             rows for c_o <= 128/rep (pos_tile 32): a tile covers 32 rep
+                             positions; w then holds taps*rep tap blocks, block r*taps + t
+                             carrying tap t's weights in rows [r*128/rep, r*128/rep + c_o)
+                             (zero elsewhere) — group r reads the window 32 r positions on */
 } fhe_conv_tc_layer;
 /* layers: HOST array of nl (<= 24) layers sharing (q, n), 2^56 <= q < 2^62.
  * X: DEVICE scratch of 3 operand buffers x_stride bytes apart (x_stride >= the

@@ -322,6 +322,32 @@ class ConvTcPlan:
         return 32
 
     @staticmethod
+    def rep_for(c_o: int, JB: int, taps: int, h: int) -> int:
+        """Position groups stacked in the 128 accumulator rows (csrc/conv_tc.cu
+        LayerDesc.rep). A layer with c_o <= 64 fills only c_o TMEM lanes, so
+        only the warps of c_o/32 lane quadrants (SM sub-partitions) can read
+        its accumulators: short contractions (JB·taps <= 16 MMAs per tile —
+        the stems) are then bound by the epilogue's TMEM reads, not the MMAs.
+        With rep groups, rows r·128/rep + o compute channel o at positions
+        32 r.. of the tile (the same window, tap offsets + 32 r): every
+        quadrant's warps run the epilogue, for the same MMA work per position.
+        FLASHHE_TC_REP (1 | 2 | 4) forces a value where it is valid."""
+        import os
+
+        def ok(r):
+            if r == 1:
+                return True
+            stage = -(-(32 * r + 2 * h) * 256 // 1024) * 1024 + taps * r * 32 * ConvTcPlan.OC_TILE
+            return c_o <= ConvTcPlan.OC_TILE // r and taps * r <= 64 and 2 * stage <= 218 * 1024
+
+        forced = os.environ.get("FLASHHE_TC_REP")
+        if forced:
+            return int(forced) if ok(int(forced)) else 1
+        if JB * taps > 16:
+            return 1
+        return next(r for r in (4, 2, 1) if ok(r))
+
+    @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
         c_o, c_i, _ = weights3d.shape
         if n < 64 or n % 64 or taps > 64 or 2 * h >= n:
@@ -347,6 +373,7 @@ class ConvTcPlan:
         self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps, self.c_i)
         N = self.OC_TILE
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
+        self.rep = self.rep_for(self.c_o, JB, self.taps, self.h) if self.pos_tile == 32 else 1
         j = np.arange(self.c_i)
         if chan is not None:
             chan = np.asarray(chan, dtype=np.int64).reshape(self.c_i, 2)
@@ -355,10 +382,13 @@ class ConvTcPlan:
             chan, self.fstride = np.stack([j * layout.frags, np.zeros_like(j)], 1), 1
         else:
             chan, self.fstride = np.stack([j // layout.c_n, layout.tile * (j % layout.c_n)], 1), 0
-        wp = np.zeros((OB * N, JB * 32, self.taps), dtype=np.int8)
-        wp[: self.c_o, : self.c_i] = weights3d
+        T = self.taps * self.rep
+        wp = np.zeros((OB * N, JB * 32, T), dtype=np.int8)
+        rows = N // self.rep
+        for r in range(self.rep):  # position group r: rows [r·rows, r·rows + c_o), tap blocks [r·taps, (r+1)·taps)
+            wp[r * rows : r * rows + self.c_o, : self.c_i, r * self.taps : (r + 1) * self.taps] = weights3d
         # [ob][jb][tap][g][kh][r][jj] with o = ob*128 + g*8 + r, j = jb*32 + kh*16 + jj
-        wp = wp.reshape(OB, N // 8, 8, JB, 2, 16, self.taps).transpose(0, 3, 6, 1, 4, 2, 5)
+        wp = wp.reshape(OB, N // 8, 8, JB, 2, 16, T).transpose(0, 3, 6, 1, 4, 2, 5)
         dev = device.require_cuda()
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
         self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
@@ -376,7 +406,7 @@ class ConvTcPlan:
         return _native.ConvTcLayer(
             inp.data_ptr(), inp.numel() // (2 * self.n), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
             self.c_o, self.taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
-            device.ptr(self.mask), out.data_ptr())
+            device.ptr(self.mask), out.data_ptr(), self.rep)
 
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
         """One cooperative persistent launch of this layer alone (relayout,

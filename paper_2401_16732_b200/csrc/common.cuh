@@ -201,6 +201,42 @@ __device__ __forceinline__ void acc60_get(const Acc60& a, uint64_t& lo, uint64_t
   hi = a.h + a.s2 + (a.x >> 32) + (lo < l ? 1ull : 0ull);
 }
 
+// Karatsuba accumulator for sums of up to 4 products of operands below 2^60:
+// u = u0 + 2^30 u1 with 30-bit limbs, u0 v0 and u1 v1 accumulate directly and
+// the cross term through (u0 + u1)(v0 + v1) (< 2^62 each, four sum below 2^64),
+// so a product costs three 32x32 -> 64 multiply-accumulates (IMAD.WIDE.U32
+// with a 64-bit addend) and no carry handling; acc30_get recombines once.
+struct Split30 {
+  uint32_t l, h, s;  // low 30 bits, high 30 bits, their sum (< 2^31)
+};
+__device__ __forceinline__ Split30 split30(uint64_t u) {
+  Split30 r;
+  r.l = (uint32_t)u & 0x3fffffffu;
+  r.h = (uint32_t)(u >> 30);
+  r.s = r.l + r.h;
+  return r;
+}
+struct Acc30 {
+  uint64_t s00, smid, s11;
+};
+__device__ __forceinline__ void acc30_zero(Acc30& a) { a.s00 = a.smid = a.s11 = 0; }
+__device__ __forceinline__ void mac30(Acc30& a, const Split30& u, const Split30& v) {
+  a.s00 += (uint64_t)u.l * v.l;
+  a.s11 += (uint64_t)u.h * v.h;
+  a.smid += (uint64_t)u.s * v.s;
+}
+// T = s00 + 2^30 (smid - s00 - s11) + 2^60 s11 as hi:lo
+__device__ __forceinline__ void acc30_get(const Acc30& a, uint64_t& lo, uint64_t& hi) {
+  const uint64_t m = a.smid - a.s00 - a.s11;
+  const uint64_t x = m << 30, y = a.s11 << 60;
+  asm("add.cc.u64 %0, %2, %3;\n\t"
+      "addc.u64 %1, %4, %5;\n\t"
+      "add.cc.u64 %0, %0, %6;\n\t"
+      "addc.u64 %1, %1, 0;"
+      : "=l"(lo), "=l"(hi)
+      : "l"(a.s00), "l"(x), "l"(m >> 34), "l"(a.s11 >> 4), "l"(y));
+}
+
 // x mod q for any x < 2^64 (q < 2^63): quotient estimate off by at most 1
 __device__ __forceinline__ uint64_t reduce_u64(uint64_t x, const ModDesc& m) {
   uint64_t qt = __umul64hi(x, m.inv64);

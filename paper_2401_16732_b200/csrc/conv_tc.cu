@@ -83,7 +83,8 @@ struct LayerDesc {
   int Y, JB, F, c_i, fstride, c_o, OB, taps, h, npos, nst, stage_bytes, win_bytes, tiles, units;
   int toff;  // tiles of the previous layers mod gridDim.x: tiles are dealt round-robin over the whole stack
   int nacc;  // accumulators per tile: 1, or 2 (a 64-position tile: weights reused by both, TMEM single-buffered)
-  int tpos;  // positions per tile = npos * nacc
+  int tpos;  // positions per tile = npos * nacc, or npos * rep
+  int rep;   // 32-position groups stacked in the 128 accumulator rows (c_o <= 128 / rep): 1, 2 or 4
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
 
@@ -571,9 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         const uint32_t idesc = idesc_i8(8 * d.npos);
         const uint32_t sstep = (uint32_t)(stage_bytes >> 4), wdesc = (uint32_t)(d.win_bytes >> 4);
         const uint32_t adelta = (uint32_t)(d.npos * 256 >> 4);  // second accumulator's positions
-        uint32_t off16[9];  // this layer's DRot offsets in 16-byte descriptor units (taps <= 9 fast path)
+        uint32_t off16[16];  // this layer's DRot offsets in 16-byte descriptor units (fast paths)
 #pragma unroll
-        for (int tp = 0; tp < 9; ++tp) off16[tp] = tp < taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
+        for (int tp = 0; tp < 16; ++tp) off16[tp] = tp < taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
         for (int t = t0; t < tiles; t += G, ++tl) {
           int b0 = 0, b1 = 1;
           if (nacc == 1) {
@@ -599,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
               if (jb == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
                 mbar_wait(tempty_bar(b), ((use >> b) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+                if (a == 0 && lane == 0) TC_TRACE(4, tl);
               }
               const uint32_t acc = tmem + b * kAccCols;
               const uint32_t blo = blo0 + (uint32_t)a * adelta;
@@ -613,6 +615,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
                 issue_taps<9>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
               } else if (taps == 1) {
                 issue_taps<1>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+              } else if (taps == 14) {  // 7 column taps x 2 stacked position groups (the 7x7 stem)
+                issue_taps<14>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+              } else if (taps == 7) {
+                issue_taps<7>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
               } else {
                 for (int tp = 0; tp < taps; ++tp) {
                   if (tp == taps - 1) wait_next();
@@ -712,13 +718,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
       // fields read through `d` in the chunk loop were re-fetched from the
       // parameter bank every chunk)
       const int c_o = d.c_o, F = d.F, npos = d.npos, nacc = d.nacc;
+      // rows of the accumulator: rep groups of rows_per output channels, group
+      // r holding positions [32 r, 32 r + 32) of the tile
+      const int rows_per = kOcTile / d.rep;
+      const int grp = (quad * 32 + lane) / rows_per, orow = (quad * 32 + lane) % rows_per;
       uint64_t* const dout = d.out;
       const uint8_t* const bmask = d.bmask;
       const uint64_t* const bias = d.bias;
       for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
         const Tile T = tile_of(t, d, n);
-        const int o = T.ob * kOcTile + quad * 32 + lane;
-        const bool active = T.ob * kOcTile + quad * 32 < c_o;  // warp-uniform
+        const int o = T.ob * kOcTile + orow;
+        const bool active = T.ob * kOcTile + (quad * 32) % rows_per < c_o;  // warp-uniform (rows_per >= 32)
         const uint64_t bd = (active && T.p == 0 && bias && o < c_o) ? bias[o] : 0;
         for (int a = 0; a < nacc; ++a) {
           int buf;
@@ -728,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
           } else {
             buf = a;
           }
-          const int s0 = T.s0 + a * npos;
+          const int s0 = T.s0 + (a + grp) * npos;
           mbar_wait_sleep(tfull_bar(buf), (use >> buf) & 1, 64);
           use ^= 1u << buf;
           if (lane == 0 && warp == 2) TC_TRACE(5, tl);
@@ -898,6 +908,11 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     if (s.bias_delta && !s.bias_mask) return fail(FHE_ERR_VALUE, "tc layer %d: bias needs a mask", l);
     if (s.pos_tile != 16 && s.pos_tile != 32 && s.pos_tile != 64)
       return fail(FHE_ERR_VALUE, "tc layer %d: pos_tile must be 16, 32 or 64", l);
+    const int rep = s.rep < 1 ? 1 : s.rep;
+    if (rep != 1 && rep != 2 && rep != 4) return fail(FHE_ERR_VALUE, "tc layer %d: rep must be 1, 2 or 4", l);
+    if (rep > 1 && (s.pos_tile != 32 || s.c_o > tc::kOcTile / rep))
+      return fail(FHE_ERR_VALUE, "tc layer %d: rep %d needs pos_tile 32 and c_o <= %d", l, rep, tc::kOcTile / rep);
+    if (s.taps * rep > tc::kMaxTaps) return fail(FHE_ERR_VALUE, "tc layer %d: taps x rep above %d", l, tc::kMaxTaps);
     if (127ll * 255 * ((s.c_i + 31) / 32 * 32) * s.taps >= (1ll << 31))
       return fail(FHE_ERR_VALUE, "tc layer %d: plane sums would exceed s32", l);
     d.in = s.in;
@@ -914,17 +929,18 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.fstride = s.fstride;
     d.c_o = s.c_o;
     d.OB = (s.c_o + tc::kOcTile - 1) / tc::kOcTile;
-    d.taps = s.taps;
+    d.taps = s.taps * rep;  // MMAs per stage: every tap for every stacked position group
+    d.rep = rep;
     d.h = s.h;
     d.npos = std::min(s.pos_tile, 32);  // positions per MMA (N = 8 npos <= 256)
     d.nacc = s.pos_tile / d.npos;       // 64-position tiles use both TMEM buffers
-    d.tpos = s.pos_tile;
+    d.tpos = s.pos_tile * rep;
     d.in_bytes = (size_t)s.n_in * 2 * n * 8;
     d.w_bytes = (size_t)d.OB * d.JB * d.taps * tc::kWTap;
     for (int t = 0; t < s.taps; ++t) {
       const int off = s.tap_steps[t] + s.h;
       if (off < 0 || off > 2 * s.h) return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
-      d.tap_off[t] = (int16_t)off;
+      for (int r = 0; r < rep; ++r) d.tap_off[r * s.taps + t] = (int16_t)(off + r * d.npos);  // group r: +32 r
     }
     d.win_bytes = ((d.tpos + 2 * d.h) * 256 + 1023) / 1024 * 1024;
     d.stage_bytes = d.win_bytes + d.taps * tc::kWTap;

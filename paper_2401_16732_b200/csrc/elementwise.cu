@@ -397,13 +397,36 @@ __global__ void __launch_bounds__(128) keyswitch_kernel(const ModSet ms, int log
     for (int i = 0; i < MAXD; ++i) dv[bb][i] = (ok && i < ndig) ? __ldg(&dig[(drow + i) * n + src]) : 0;
     c0v[bb] = ok ? __ldg(&ct[crow * n + src]) : 0;
   }
+  constexpr bool KARA = W60 && MAXD <= 4;  // q < 2^60, <= 4 digits: Karatsuba 30-bit limbs
+  Split30 sk0[KARA ? MAXD : 1], sk1[KARA ? MAXD : 1];
+  if constexpr (KARA) {
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      sk0[i] = split30(k0[i]);
+      sk1[i] = split30(k1[i]);
+    }
+  }
 #pragma unroll
   for (int bb = 0; bb < BCH; ++bb) {
     const int b = b0 + bb;
     if (b < B) {
       const size_t crow = ((size_t)b * L + l) * 2;
       uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
-      if constexpr (W60) {  // q < 2^60, ndig <= 8: column-split accumulation
+      if constexpr (KARA) {
+        Acc30 s0, s1;
+        acc30_zero(s0);
+        acc30_zero(s1);
+#pragma unroll
+        for (int i = 0; i < MAXD; ++i) {
+          if (i < ndig) {
+            const Split30 u = split30(dv[bb][i]);
+            mac30(s0, u, sk0[i]);
+            mac30(s1, u, sk1[i]);
+          }
+        }
+        acc30_get(s0, a0l, a0h);
+        acc30_get(s1, a1l, a1h);
+      } else if constexpr (W60) {  // q < 2^60, ndig <= 8: column-split accumulation
         Acc60 s0, s1;
         acc60_zero(s0);
         acc60_zero(s1);
@@ -487,7 +510,21 @@ __device__ __forceinline__ void ks_finish(const KsLoads<MAXD, BCH>& v, uint64_t*
     const int b = b0 + bb;
     if (b >= B) continue;
     uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
-    if constexpr (W60) {
+    if constexpr (W60 && MAXD <= 4) {  // Karatsuba 30-bit limbs (see Acc30)
+      Acc30 s0, s1;
+      acc30_zero(s0);
+      acc30_zero(s1);
+#pragma unroll
+      for (int i = 0; i < MAXD; ++i) {
+        if (i < ndig) {
+          const Split30 u = split30(v.dv[bb][i]);
+          mac30(s0, u, split30(v.k0[i]));
+          mac30(s1, u, split30(v.k1[i]));
+        }
+      }
+      acc30_get(s0, a0l, a0h);
+      acc30_get(s1, a1l, a1h);
+    } else if constexpr (W60) {
       Acc60 s0, s1;
       acc60_zero(s0);
       acc60_zero(s1);

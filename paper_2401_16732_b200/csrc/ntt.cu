@@ -503,6 +503,155 @@ __global__ void __launch_bounds__((1 << LOGN) >> LOGR) ntt_row_kernel(const Limb
   for (int k = 0; k < NP; ++k) d2[tid + k * NT] = xin[k];
 }
 
+// Butterflies of one phase on register-resident elements (the math of
+// split_phase without its shared-memory load / store).
+template <int LOGR, int R, bool INV, int TL>
+__device__ __forceinline__ void phase_math(uint64_t (&e)[1 << LOGR], const NttDesc& d, uint32_t tb, bool fold_ninv) {
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  if constexpr (!INV) {
+    static_for<0, R>([&](auto ai) {
+      constexpr int a = R - 1 - decltype(ai)::value;  // largest stride first
+      constexpr int dd = 1 << a;
+      const uint32_t t0 = tb >> (TL + a + 1);
+#pragma unroll
+      for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+        const ulonglong2 tw = __ldg(&d.psi[t0 + (g >> (a + 1))]);
+#pragma unroll
+        for (int u = 0; u < dd; ++u) {
+          uint64_t X = e[g + u];
+          X = X >= q2 ? X - q2 : X;
+          const uint64_t T = shoup_lazy(e[g + u + dd], tw.x, tw.y, q);
+          e[g + u] = X + T;
+          e[g + u + dd] = X - T + q2;
+        }
+      }
+    });
+  } else {
+    static_for<0, R>([&](auto ai) {
+      constexpr int a = decltype(ai)::value;  // smallest stride first
+      constexpr int dd = 1 << a;
+      if (fold_ninv && a == R - 1) {  // global stage 0: fold n^-1 (ring.py:162)
+#pragma unroll
+        for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+#pragma unroll
+          for (int u = 0; u < dd; ++u) {
+            const uint64_t X = e[g + u], Y = e[g + u + dd];
+            e[g + u] = shoup_lazy(X + Y, d.ninv.x, d.ninv.y, q);
+            e[g + u + dd] = shoup_lazy(X - Y + q2, d.ninv_w1.x, d.ninv_w1.y, q);
+          }
+        }
+      } else {
+        const uint32_t t0 = tb >> (TL + a + 1);
+#pragma unroll
+        for (int g = 0; g < (1 << LOGR); g += 2 * dd) {
+          const ulonglong2 tw = __ldg(&d.ipsi[t0 + (g >> (a + 1))]);
+#pragma unroll
+          for (int u = 0; u < dd; ++u) {
+            const uint64_t X = e[g + u], Y = e[g + u + dd];
+            const uint64_t S = X + Y;
+            e[g + u] = S >= q2 ? S - q2 : S;
+            e[g + u + dd] = shoup_lazy(X - Y + q2, tw.x, tw.y, q);
+          }
+        }
+      }
+    });
+  }
+}
+
+// Phase K of a LOGN-point transform in execution order: forward runs the
+// stage groups [0, LOGR), [LOGR, 2 LOGR), ..., [nfull LOGR, LOGN); the inverse
+// runs them in reverse.
+template <int LOGN, int LOGR, bool INV, int K>
+struct RowPhase {
+  static constexpr int nfull = LOGN / LOGR, rem = LOGN - nfull * LOGR, count = nfull + (rem > 0);
+  static constexpr int fk = INV ? count - 1 - K : K;
+  static constexpr int S = fk * LOGR;
+  static constexpr int R = fk < nfull ? LOGR : rem;
+  static constexpr int TL = LOGN - (S + R);
+};
+
+// One CTA per row, the first phase's elements loaded straight from global
+// memory into registers (a warp's load i reads 32 consecutive words, or each
+// thread's 2^LOGR contiguous words as 128-bit loads when the phase's stride is
+// 1) and the last phase's results stored straight from registers: two
+// shared-memory passes and two barriers fewer than staging the row through
+// shared memory at both ends. n = 2048: 3 phases, 2 shared-memory exchanges.
+template <bool INV, int LOGN, int LOGR>
+__global__ void __launch_bounds__((1 << LOGN) >> LOGR) ntt_row_direct_kernel(const LimbSet ls, const LoadMap lm,
+                                                                          uint64_t* __restrict__ dst) {
+  extern __shared__ uint64_t sm[];
+  constexpr int n = 1 << LOGN, E = 1 << LOGR;
+  constexpr int NPH = RowPhase<LOGN, LOGR, INV, 0>::count;
+  const int row = blockIdx.x;
+  const NttDesc d = ls.d[(row / lm.G) % ls.L];
+  const int item = threadIdx.x;
+  const uint64_t* srow;
+  int shift = 0;
+  uint64_t mask = ~0ull;
+  if (lm.ndig > 0) {
+    srow = lm.src + (size_t)(row / lm.ndig) * n;
+    shift = lm.T * (row % lm.ndig);
+    mask = lm.mask;
+  } else {
+    srow = lm.src + (size_t)row * n;
+  }
+  uint64_t* drow = dst + (size_t)row * n;
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  static_for<0, NPH>([&](auto kc) {
+    constexpr int K = decltype(kc)::value;
+    using Ph = RowPhase<LOGN, LOGR, INV, K>;
+    constexpr int TL = Ph::TL;
+    const int B = ((item >> TL) << (TL + LOGR)) + (item & ((1 << TL) - 1));
+    uint64_t e[E];
+    if constexpr (K == 0) {
+      if constexpr (TL == 0) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(srow + B + i);
+          e[i] = (v.x >> shift) & mask;
+          e[i + 1] = (v.y >> shift) & mask;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) e[i] = (srow[B + (i << TL)] >> shift) & mask;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) e[i] = sm[spad(B) + (i << TL) + ((i << TL) >> 4)];
+    }
+    phase_math<LOGR, Ph::R, INV, TL>(e, d, (uint32_t)(n + B), INV && Ph::S == 0);
+    if constexpr (K == NPH - 1) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        uint64_t x = e[i];
+        if (!INV) x = x >= q2 ? x - q2 : x;
+        e[i] = csub(x, q);
+      }
+      if constexpr (TL == 0) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2)
+          *reinterpret_cast<ulonglong2*>(drow + B + i) = make_ulonglong2(e[i], e[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) drow[B + (i << TL)] = e[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) sm[spad(B) + (i << TL) + ((i << TL) >> 4)] = e[i];
+      __syncthreads();
+    }
+  });
+}
+
+static bool row_direct_enabled() {  // FHE_NTT_ROW_DIRECT=0 selects the staged row kernel (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_NTT_ROW_DIRECT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // Radix of the row kernels' register phases (2^LOGR elements per thread,
 // n / 2^LOGR threads per row). Measured on the B200 at 512 rows: n = 4096
 // radix 8 (512 threads) 32.8 us vs radix 16 34.8 us forward; n = 2048 equal
@@ -521,6 +670,14 @@ template <bool INV, int LOGN>
 static void launch_row(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, cudaStream_t st) {
   constexpr int n = 1 << LOGN;
   const size_t smem = (size_t)(n + (n >> 4) + 1) * sizeof(uint64_t);
+  if (row_direct_enabled()) {
+    switch (row_logr(LOGN)) {
+      case 2: ntt_row_direct_kernel<INV, LOGN, 2><<<rows, n >> 2, smem, st>>>(ls, lm, dst); break;
+      case 3: ntt_row_direct_kernel<INV, LOGN, 3><<<rows, n >> 3, smem, st>>>(ls, lm, dst); break;
+      default: ntt_row_direct_kernel<INV, LOGN, 4><<<rows, n >> 4, smem, st>>>(ls, lm, dst); break;
+    }
+    return;
+  }
   switch (row_logr(LOGN)) {
     case 2: ntt_row_kernel<INV, LOGN, 2><<<rows, n >> 2, smem, st>>>(ls, lm, dst); break;
     case 3: ntt_row_kernel<INV, LOGN, 3><<<rows, n >> 3, smem, st>>>(ls, lm, dst); break;

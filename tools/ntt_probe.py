@@ -28,15 +28,15 @@ def main():
     plans = device.plan_array(n, [q])
     x = torch.from_numpy(np.random.default_rng(1).integers(0, q, (rows, n), dtype=np.int64)).cuda()
     y = torch.empty_like(x)
-    st = device.stream()
     for name in ("fhe_ntt_forward", "fhe_ntt_inverse"):
-        fn = lambda: _native.call(name, plans, 1, rows, 1, x.data_ptr(), y.data_ptr(), st)  # noqa: E731
+        fn = lambda: _native.call(name, plans, 1, rows, 1, x.data_ptr(), y.data_ptr(), device.stream())  # noqa: E731
         fn()
         torch.cuda.synchronize()
         if args.once:
             continue
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
             for _ in range(20):
                 fn()
         g.replay()

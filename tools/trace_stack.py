@@ -38,17 +38,19 @@ def main():
     tl = 0
     toff = 0
     print(f"{'layer':10s} {'rel_done':>9s} {'x_ready':>9s} {'mma0':>9s} {'mma_end':>9s} {'epi_end':>9s} tiles(CTA0)"
-          f" {'mma/tile':>9s} {'epi/tile':>9s}")
+          f" {'mma/tile':>9s} {'wait/tile':>9s} {'epi/tile':>9s} {'commit->epi':>11s}")
     for l, L in enumerate(layers):
         d = L["plan"].tc
-        tiles = (P.n // d.pos_tile) * -(-d.c_o // 128) * 2 * d.frags
+        tiles = (P.n // (d.pos_tile * d.rep)) * -(-d.c_o // 128) * 2 * d.frags
         mine = len(range((0 - toff) % 148, tiles, 148))
         toff = (toff + tiles) % 148
         first, last = tl, tl + mine - 1
         print(f"{L['layer'].name:10s} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
               f"{rel(t[1][last]) if mine else -1:9d} {rel(t[6][last]) if mine else -1:9d} {mine:11d}"
               f" {int(np.mean([t[1][i] - t[0][i] for i in range(first, last + 1)])) if mine else -1:9d}"
-              f" {int(np.mean([t[6][i] - t[5][i] for i in range(first, last + 1)])) if mine else -1:9d}")
+              f" {int(np.mean([t[4][i] - t[0][i] for i in range(first, last + 1)])) if mine else -1:9d}"
+              f" {int(np.mean([t[6][i] - t[5][i] for i in range(first, last + 1)])) if mine else -1:9d}"
+              f" {int(np.mean([t[5][i] - t[1][i] for i in range(first, last + 1)])) if mine else -1:11d}")
         tl += mine
 
 

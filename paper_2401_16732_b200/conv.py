@@ -487,7 +487,12 @@ def issue_k1(items, on_gemm=None) -> list:
         if items[i][0].path == "tc":
             if on_gemm:
                 on_gemm(i, "start")
-            run_tc_stack([(plan.tc, inp, out) for plan, inp, _, out in items[i:j]])
+            # Jobs of one launch are independent, so their order is free: the
+            # first job's relayout is exposed (nothing runs beside it) while a
+            # later job's is overlapped with the GEMMs of the jobs before it,
+            # so jobs with a small digit-plane operand go first (stable).
+            run = sorted(items[i:j], key=lambda it: it[0].tc.x_bytes) if _stack_order() else items[i:j]
+            run_tc_stack([(plan.tc, inp, out) for plan, inp, _, out in run])
             if on_gemm:
                 on_gemm(i, "end")
         else:
@@ -498,6 +503,13 @@ def issue_k1(items, on_gemm=None) -> list:
         done[i:j] = [ev] * (j - i)
         i = j
     return done
+
+
+def _stack_order() -> bool:
+    """FLASHHE_STACK_ORDER = x (default: small digit-plane operands first) | given."""
+    import os
+
+    return os.environ.get("FLASHHE_STACK_ORDER", "x") != "given"
 
 
 def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> ConvPlan:

@@ -757,11 +757,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             // each warp of the quadrant takes a contiguous half of the chunks: a
             // lane then writes whole 128-byte lines of its channel row
             const int kper = npos / 4 / (kEpiWarps / 4);
-#pragma unroll 1
-            for (int k = sub * kper; k < (sub + 1) * kper; ++k) {
-              uint32_t v[32];
-              TMEM_LD32(acc + k * 32, v);
-              asm volatile("tcgen05.wait::ld.sync.aligned;");
+            // recombine the 4 positions of one 32-column chunk and store them
+            auto finish = [&](const uint32_t* v, int k) {
               uint64_t r[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -790,6 +787,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
                              "l"(r[2]), "l"(r[3])
                              : "memory");
 #endif
+            };
+            if (kper % 2 == 0) {
+              // two chunks per TMEM round trip: both loads in flight before the
+              // one wait (tcgen05.wait::ld covers every outstanding load)
+#pragma unroll 1
+              for (int k = sub * kper; k < (sub + 1) * kper; k += 2) {
+                uint32_t va[32], vb[32];
+                TMEM_LD32(acc + k * 32, va);
+                TMEM_LD32(acc + (k + 1) * 32, vb);
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+                finish(va, k);
+                finish(vb, k + 1);
+              }
+            } else {
+#pragma unroll 1
+              for (int k = sub * kper; k < (sub + 1) * kper; ++k) {
+                uint32_t v[32];
+                TMEM_LD32(acc + k * 32, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+                finish(v, k);
+              }
             }
           }
           asm volatile("tcgen05.fence::before_thread_sync;");

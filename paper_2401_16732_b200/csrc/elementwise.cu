@@ -4,6 +4,7 @@
 // affine, scalar 64-bit gathers where it is a permutation (DRot, automorphism,
 // eval-domain Galois map).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -573,6 +574,78 @@ __global__ void __launch_bounds__(128) keyswitch_multi_kernel(const ModSet ms, i
   }
 }
 
+// The default configuration (T = 16: four digits, every modulus below 2^60)
+// of keyswitch_multi_kernel with the digit count and the Karatsuba MAC form
+// fixed at compile time: no per-digit predicates, no load-buffer copies
+// between steps (the generic kernel spent most of its issue slots on those),
+// occupancy instead of software pipelining for the gather latency.
+template <int BCH>
+__global__ void __launch_bounds__(128) keyswitch_multi4_kernel(const ModSet ms, int logn, int L, int B,
+                                                               const __grid_constant__ KsSteps A,
+                                                               const uint64_t* __restrict__ ct,
+                                                               const uint64_t* __restrict__ dig) {
+  const uint32_t n = 1u << logn;
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int b0 = blockIdx.y * BCH;
+  const int l = blockIdx.z;
+  const ModDesc m = ms.m[l];
+  const uint32_t e = 2u * brev_bits(x, logn) + 1u, mask2n = 2u * n - 1u;
+  const uint64_t* drow[BCH];
+  const uint64_t* crow[BCH];
+  size_t orow[BCH];
+#pragma unroll
+  for (int bb = 0; bb < BCH; ++bb) {
+    const size_t b = (size_t)min(b0 + bb, B - 1);  // clamped: loads stay in bounds, stores are guarded
+    drow[bb] = dig + (b * L + l) * 4 * n;
+    crow[bb] = ct + (b * L + l) * 2 * n;
+    orow[bb] = (b * L + l) * 2 * n + x;
+  }
+  const size_t krow = (size_t)l * 8 * n + x;
+#pragma unroll 1
+  for (int s = 0; s < A.S; ++s) {
+    const uint32_t e2 = (e * A.gpow[s]) & mask2n;
+    const uint32_t src = brev_bits((e2 - 1u) >> 1, logn);
+    const uint64_t* K = A.keys[s] + krow;
+    uint64_t kv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kv[i] = __ldg(K + (size_t)i * n);  // swk0_0, swk1_0, swk0_1, ...
+    uint64_t dv[BCH][4], c0[BCH];
+#pragma unroll
+    for (int bb = 0; bb < BCH; ++bb) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dv[bb][i] = __ldg(drow[bb] + (size_t)i * n + src);
+      c0[bb] = __ldg(crow[bb] + src);
+    }
+    Split30 k0[4], k1[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      k0[i] = split30(kv[2 * i]);
+      k1[i] = split30(kv[2 * i + 1]);
+    }
+    uint64_t* out = A.out[s];
+#pragma unroll
+    for (int bb = 0; bb < BCH; ++bb) {
+      Acc30 s0, s1;
+      acc30_zero(s0);
+      acc30_zero(s1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const Split30 u = split30(dv[bb][i]);
+        mac30(s0, u, k0[i]);
+        mac30(s1, u, k1[i]);
+      }
+      uint64_t a0l, a0h, a1l, a1h;
+      acc30_get(s0, a0l, a0h);
+      acc30_get(s1, a1l, a1h);
+      if (b0 + bb < B) {
+        out[orow[bb]] = csub(redc(a0l, a0h, m) + c0[bb], m.q);
+        out[orow[bb] + n] = redc(a1l, a1h, m);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K4b
 // Fused PMult-accumulate of the conventional convolution (conv.py:457-564):
 // out[o][p] = Σ_{(r, w) in terms(o)} R[r][p] ⊙ PT[w]   (mod q, EVAL domain)
@@ -972,6 +1045,15 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
   return FHE_OK;
 }
 
+static bool ks_multi4() {  // FHE_KS_MULTI4=0 selects the generic multi-step kernel (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("FHE_KS_MULTI4");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int fhe_keyswitch_multi(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct, const uint64_t* digits,
                         int ndig, int S, const uint64_t* const* keys_mont, const uint64_t* gpows,
                         uint64_t* const* outs, void* stream) {
@@ -1006,7 +1088,9 @@ int fhe_keyswitch_multi(const uint64_t* moduli, int L, int B, int n, const uint6
       A.out[s] = outs[s0 + s];
       A.gpow[s] = (uint32_t)(gpows[s0 + s] & (2ull * n - 1));
     }
-    if (ndig <= 4 && w60)
+    if (ndig == 4 && w60 && ks_multi4())
+      keyswitch_multi4_kernel<bch><<<grid, 128, 0, st>>>(ms, logn, L, B, A, ct, digits);
+    else if (ndig <= 4 && w60)
       keyswitch_multi_kernel<4, bch, true><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, A, ct, digits);
     else if (ndig <= 4)
       keyswitch_multi_kernel<4, bch, false><<<grid, 128, 0, st>>>(ms, logn, L, B, ndig, A, ct, digits);

@@ -33,6 +33,8 @@ def main():
     torch.cuda.synchronize()
     _native.call("fhe_debug_trace", None)
     t = buf.cpu().numpy().reshape(8, 4096).astype(np.int64)
+    if conv._stack_order():  # issue_k1's launch order
+        layers = sorted(layers, key=lambda L: L["plan"].tc.x_bytes)
     t0 = t[2][0]
     rel = lambda v: int(v - t0) if v else -1  # noqa: E731
     tl = 0

@@ -206,3 +206,45 @@ def test_wire_format_frames():
     got = stack.host_stack()
     for i, c in enumerate(cts):
         assert np.array_equal(got[i, 0], c.c0.coeffs) and np.array_equal(got[i, 1], c.c1.coeffs)
+
+
+def test_wire_frames_match_reference_frames():
+    """Frames of privinfer's own bfv.ct_to_bytes (tests/golden/make_wire_golden.py):
+    a fresh seeded encryption (seed-compressed and full), an EVAL batch
+    ciphertext and a non-fresh sum, and a batch of unseeded frames; the
+    package's writer reproduces each byte string and its parser reads them."""
+    import hashlib
+    import json
+
+    from conftest import GOLDEN
+    from paper_2401_16732_b200 import bfv, params
+    from paper_2401_16732_b200.ring import Domain, ModPoly
+
+    P = params.default_params()
+    meta = json.loads((GOLDEN / "wire.json").read_text())
+    arr = np.load(GOLDEN / "wire.npz")
+    cts = {}
+    for name in meta["batch"]["order"]:
+        g = meta[name]
+        dom = Domain.EVAL if g["domain"] else Domain.COEFF
+        seed = arr[f"{name}_seed"].tobytes() or None
+        ct = bfv.Ciphertext(ModPoly(arr[f"{name}_c0"], P.q, dom), ModPoly(arr[f"{name}_c1"], P.q, dom),
+                            bfv.Encoding(g["encoding"]), dom, fresh=g["fresh"], seed=seed)
+        cts[name] = ct
+        seeded, full = bfv.ct_to_bytes(ct), bfv.ct_to_bytes(ct, seed_compress=False)
+        assert hashlib.sha256(seeded).hexdigest() == g["h:seeded"] and len(seeded) == g["len:seeded"]
+        assert hashlib.sha256(full).hexdigest() == g["h:full"] and len(full) == g["len:full"]
+        assert list(seeded[:3]) == g["head"]
+        back = bfv.ct_from_bytes(seeded, P)
+        assert np.array_equal(back.c0.coeffs, arr[f"{name}_c0"]) and np.array_equal(back.c1.coeffs, arr[f"{name}_c1"])
+        assert back.domain == dom and back.encoding == ct.encoding
+    assert bfv.ct_wire_size(P, True) == meta["wire_size"]["seeded"]
+    assert bfv.ct_wire_size(P, False) == meta["wire_size"]["full"]
+    blob = b"".join(bfv.ct_to_bytes(cts[k], seed_compress=False) for k in meta["batch"]["order"])
+    assert hashlib.sha256(blob).hexdigest() == meta["batch"]["h"]
+    # a batch of unseeded frames from mixed headers is refused by the stack parser
+    with pytest.raises(bfv.EncodingError):
+        bfv.cts_from_bytes(blob, 3, P, pin=False)
+    same = b"".join(bfv.ct_to_bytes(c, seed_compress=False) for c in (cts["summed"], cts["fresh"]))
+    stack = bfv.cts_from_bytes(same, 2, P, pin=False).host_stack()
+    assert np.array_equal(stack[1, 0], arr["fresh_c0"]) and np.array_equal(stack[0, 1], arr["summed_c1"])

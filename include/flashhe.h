@@ -140,7 +140,8 @@ int fhe_poly_add_delta(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
                        const uint64_t* base, const int64_t* m, uint64_t* out,
                        void* stream);
 /* bfv.encrypt_private combine step (bfv.py:181):
- * out = (delta * (m mod p) - as - e) mod q, m and e int64 (e small, signed),
+ * out = (delta * (m mod p) - as - e) mod q, m and e int64 (e small, signed;
+ * m NULL: encryptions of zero),
  * as canonical [0,q) (= iNTT(NTT(a) * s_eval)). */
 int fhe_encrypt_combine(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
                         const int64_t* m, const uint64_t* as, const int64_t* e,
@@ -172,6 +173,13 @@ int fhe_wide_finalize(int n, uint64_t q, const int64_t* lo, const int64_t* hi, u
 int fhe_decrypt_round(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
                       const uint64_t* u, uint64_t* m_out, uint64_t* maxw_out,
                       void* stream);
+/* fhe_decrypt_round with the per-row residual maxima folded into ONE device
+ * word: *max_all = max(*max_all, max |residual| of every row) (atomicMax; the
+ * caller zeroes it, fhe_zero, before the first round it covers). A layer's
+ * whole share exchange then needs one 8-byte read for its noise-budget check
+ * (the reference checks each decryption, bfv.py:278-293). */
+int fhe_decrypt_round_max(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* u,
+                          uint64_t* m_out, uint64_t* max_all, void* stream);
 
 /* ------------------------------------------ K1: Flash convolution core */
 /* Lazy DRot x CMult accumulation with one reduction per coefficient
@@ -220,9 +228,12 @@ typedef struct fhe_conv_tc_layer {
                              (zero elsewhere) — group r reads the window 32 r positions on */
 } fhe_conv_tc_layer;
 /* layers: HOST array of nl (<= 24) layers sharing (q, n), 2^56 <= q < 2^62.
- * X: DEVICE scratch of 3 operand buffers x_stride bytes apart (x_stride >= the
- *   largest layer's X; one buffer when nl == 1). Layer l uses buffer l % 3:
- *   layer l+1 is relaid out while layer l's GEMM runs.
+ * X: DEVICE scratch. x_stride > 0: 3 operand buffers x_stride bytes apart
+ *   (x_stride >= the largest layer's X; one buffer when nl == 1), layer l uses
+ *   buffer l % 3 (relayout runs up to three layers ahead of the GEMM).
+ *   x_stride == 0: every layer owns a region, consecutive and 256-byte
+ *   aligned (sum of ceil256(2*frags*ceil(c_i/32)*(n+2h)*256) bytes), and the
+ *   relayout of later layers never waits for earlier GEMMs.
  * sync: DEVICE uint64[3 + 3*24], zeroed once before first use: the launch
  *   counter and, per layer, work / relayout-done / GEMM-done counters. They
  *   only grow (graph-replay safe); reuse one sync buffer only for stacks with
@@ -273,6 +284,15 @@ int fhe_keyswitch_apply(const uint64_t* moduli, int L, int B, int n, const uint6
 int fhe_keyswitch_multi(const uint64_t* moduli, int L, int B, int n, const uint64_t* ct, const uint64_t* digits,
                         int ndig, int S, const uint64_t* const* keys_mont, const uint64_t* gpows,
                         uint64_t* const* outs, void* stream);
+
+/* Row plumbing (no arithmetic). fhe_gather_rows: srcs is a HOST array of k
+ * DEVICE row pointers (n words each) -> dst DEVICE [k][n] (the stack form of a
+ * list of polynomials). fhe_copy_2d: cudaMemcpy2DAsync device to device (e.g.
+ * interleaving c0 / c1 row stacks into [k][2][n]). fhe_zero: cudaMemsetAsync. */
+int fhe_gather_rows(const uint64_t* const* srcs, int k, int n, uint64_t* dst, void* stream);
+int fhe_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                void* stream);
+int fhe_zero(void* dst, size_t bytes, void* stream);
 
 /* Fused PMult-accumulate of the conventional convolution (conv.py:457-564:
  * the pmult + hadd chain per output ciphertext), EVAL domain, one launch:

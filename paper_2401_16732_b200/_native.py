@@ -63,6 +63,10 @@ SIGNATURES = {
     "fhe_wide_add_rotated": (_int, [_int, _vp, _vp, _i64, _vp, _vp, _vp]),
     "fhe_wide_finalize": (_int, [_int, _u64, _vp, _vp, _vp, _vp]),
     "fhe_decrypt_round":(_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp]),
+    "fhe_decrypt_round_max": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp]),
+    "fhe_gather_rows": (_int, [_vp, _int, _int, _vp, _vp]),
+    "fhe_copy_2d": (_int, [_vp, ctypes.c_size_t, _vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, _vp]),
+    "fhe_zero": (_int, [_vp, ctypes.c_size_t, _vp]),
     "fhe_conv_flash": (
         _int,
         [_u64, _int, _vp, _int, _vp, _int, _int, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp],

@@ -312,27 +312,30 @@ def server_round1_layer(conv_out, session: LayerSession, params: RingParams) -> 
     return msg
 
 
-def _check_budget_rows(params: RingParams, maxw: torch.Tensor):
-    if maxw.numel() and bfv._budget(params, int(maxw.max().item())) <= 0:
+def _check_budget_rows(params: RingParams, acc: "bfv.MaxAcc"):
+    """The client's noise-budget check over every decryption `acc` covers
+    (one 8-byte device read)."""
+    if bfv._budget(params, acc.value()) <= 0:
         raise ProtocolError("noise budget exhausted: ciphertext no longer decrypts reliably")
 
 
-def _decrypt_rows_checked(rows: torch.Tensor, domain, sk: bfv.SecretKey, pending: list | None = None) -> torch.Tensor:
+def _decrypt_rows_checked(rows: torch.Tensor, domain, sk: bfv.SecretKey, pending: "bfv.MaxAcc | None" = None
+                          ) -> torch.Tensor:
     """Decrypt a layer's messages; the noise-budget check runs now (one host
-    sync) or, with `pending`, is queued for the caller to run once at the end
-    of the exchange (run_layer_activation: no sync between the rounds)."""
+    sync) or, with `pending` (a device max accumulator), is left for the
+    caller to run once at the end of the exchange (run_layer_activation: no
+    sync between the rounds)."""
     params = sk.params
     cts = bfv.cts_from_rows(rows, params.q, Encoding.DIRECT, domain)
-    m, maxw = bfv.decrypt_rows_dev(cts, sk)
+    acc = pending if pending is not None else bfv.MaxAcc(rows.device)
+    m = bfv.decrypt_rows_max(cts, sk, acc)
     if pending is None:
-        _check_budget_rows(params, maxw)
-    else:
-        pending.append(maxw)
+        _check_budget_rows(params, acc)
     return m
 
 
 def client_round1_layer(msg: torch.Tensor, plan: RepackPlan, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
-                        codec: FixedPointCodec | None = None, pending: list | None = None
+                        codec: FixedPointCodec | None = None, pending: "bfv.MaxAcc | None" = None
                         ) -> tuple[torch.Tensor, torch.Tensor]:
     """Decrypt w = a + r, repack into the next layout (w'), return
     (⟦w'² + w'·2^f⟧ direct, ⟦w'⟧ batch) — one pass per step for the layer."""
@@ -364,7 +367,7 @@ def server_round2_layer(msgs: tuple[torch.Tensor, torch.Tensor], session: LayerS
 
 
 def client_round2_layer(msg: torch.Tensor, plan: RepackPlan, sk: bfv.SecretKey,
-                        zeros: bfv.ZeroRowPool, pending: list | None = None) -> torch.Tensor:
+                        zeros: bfv.ZeroRowPool, pending: "bfv.MaxAcc | None" = None) -> torch.Tensor:
     """Decrypt the batch messages, re-encrypt their slots direct (decode_batch
     as NTT mod p + slot gather fused into the encryption pass)."""
     params = sk.params
@@ -409,14 +412,16 @@ class _LayerGraph:
     def __init__(self, plan: RepackPlan, params: RingParams, f: int):
         n, ks, kd = params.n, plan.k_src, plan.k_dst
         dev = device.require_cuda()
-        z = lambda *shape: torch.zeros(shape, dtype=torch.int64, device=dev)  # noqa: E731
+        z = lambda *shape: device.zeros_i64(shape)  # noqa: E731
         self.inp, self.zeros = z(ks, 2, n), z(3 * kd, 2, n)
         self.r, self.two_r, self.v_eval, self.const = z(ks, n), z(kd, n), z(kd, n), z(kd, n)
         self.s_eval = z(n)
+        self.acc = bfv.MaxAcc(dev)  # the exchange's largest decryption residual (zeroed by every replay)
         key = _StaticKey(params, self.s_eval)
 
         def body():
-            pending: list = []
+            pending = self.acc
+            _native.call("fhe_zero", pending.t.data_ptr(), 8, device.stream())
             m1 = _encrypt_rows(self.inp, self.r, params)
             w = _decrypt_rows_checked(m1, Domain.COEFF, key, pending)
             ct_sq = _encrypt_rows(self.zeros[:kd], _gather(plan.idx, w), params, square=True, f=f)
@@ -431,7 +436,7 @@ class _LayerGraph:
             out = torch.empty_like(ct_sq)
             _native.call("fhe_act_finalize", params.q, params.p, params.delta, kd, n, ct_sq.data_ptr(),
                          back.data_ptr(), self.const.data_ptr(), out.data_ptr(), device.stream())
-            return out, torch.cat(pending)
+            return out
 
         body()  # plans, tables and kernels initialised outside the capture
         torch.cuda.synchronize()
@@ -439,7 +444,7 @@ class _LayerGraph:
         side.wait_stream(torch.cuda.current_stream())
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.stream(side), torch.cuda.graph(self.graph, stream=side):
-            self.out, self.maxw = body()
+            self.out = body()
         torch.cuda.current_stream().wait_stream(side)
 
     def run(self, conv_rows: torch.Tensor, session: "LayerSession", sk: bfv.SecretKey, zero_rows: torch.Tensor):
@@ -451,7 +456,7 @@ class _LayerGraph:
         self.const.copy_(session.const)
         self.s_eval.copy_(sk.s_eval_dev())
         self.graph.replay()
-        return self.out.clone(), self.maxw.clone()
+        return self.out.clone(), self.acc
 
 
 _layer_graphs: dict = {}
@@ -492,13 +497,13 @@ def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zer
         res = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
         return conv.PackedTensor(res, plan.dst, plan.channels, getattr(conv_out, "scale", 0))
     plan = session.plan
-    pending: list = []  # the client's noise-budget checks, run once after the exchange (one host sync)
+    pending = bfv.MaxAcc()  # the client's noise-budget checks, run once after the exchange (one host sync)
     m1 = server_round1_layer(conv_out, session, params)
     sq, w = client_round1_layer(m1, plan, sk, zeros, session.codec, pending)
     m2 = server_round2_layer((sq, w), session, params)
     back = client_round2_layer(m2, plan, sk, zeros, pending)
     out = server_finalize_layer(sq, back, session, params, getattr(conv_out, "scale", 0))
-    _check_budget_rows(params, torch.cat(pending))
+    _check_budget_rows(params, pending)
     return out
 
 
@@ -538,11 +543,11 @@ def run_repack_round(x, session: RepackSession, sk: bfv.SecretKey, zeros: bfv.Ze
         raise EncodingError("tensor does not match the repack session's layout")
     masked = _encrypt_rows(bfv.cts_rows(cts), session.r, params)  # server: ⟦a + r⟧
     session.round = Round.MASKED
-    pending: list = []
+    pending = bfv.MaxAcc()
     w = _decrypt_rows_checked(masked, Domain.COEFF, sk, pending)  # client: a + r, repacked, re-encrypted
     back = _encrypt_rows(zeros.take_rows(plan.k_dst), _gather(plan.idx, w), params)
     out = _encrypt_rows(back, session.neg_r_dst, params)  # server: ⟦a' + r'⟧ − r' (plain_add of −r')
     session.round = Round.DONE
-    _check_budget_rows(params, torch.cat(pending))
+    _check_budget_rows(params, pending)
     cts_out = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
     return conv.PackedTensor(cts_out, plan.dst, plan.channels, getattr(x, "scale", 0))

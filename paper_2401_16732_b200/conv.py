@@ -393,7 +393,7 @@ class ConvTcPlan:
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
         self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
         self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
-        self.sync = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=dev)  # counters of this plan's own launches
+        self.sync = device.zeros_i64(SYNC_WORDS)  # counters of this plan's own launches
         self.bias, self.mask = bias, mask
 
     @property
@@ -428,8 +428,13 @@ def _stack_sync_for(tcs) -> torch.Tensor:
     key = (torch.cuda.current_device(),) + tuple(id(tc) for tc in tcs)
     sync = _stack_sync.get(key)
     if sync is None:
-        sync = _stack_sync[key] = torch.zeros(SYNC_WORDS, dtype=torch.int64, device=device.require_cuda())
+        sync = _stack_sync[key] = device.zeros_i64(SYNC_WORDS)
     return sync
+
+
+def _x_total(tcs) -> int:
+    """Digit-plane scratch of one launch: each layer's X region, 256-byte aligned."""
+    return sum(-(-tc.x_bytes // 256) * 256 for tc in tcs)
 
 
 def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
@@ -442,10 +447,9 @@ def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
         raise ValueError(f"at most {MAX_STACK} layers per tensor-core launch")
     if sync is None:
         sync = _stack_sync_for([tc for tc, *_ in jobs])
-    need = -(-max(tc.x_bytes for tc, *_ in jobs) // 256) * 256
-    X = device.scratch("conv_tc_x", need * (3 if len(jobs) > 1 else 1))
+    X = device.scratch("conv_tc_x", _x_total([tc for tc, *_ in jobs]))  # every layer its own operand region
     arr = (_native.ConvTcLayer * len(jobs))(*[tc.layer(inp, out) for tc, inp, out in jobs])
-    rc = _native.fn("fhe_conv_tc_stack")(tc0.q, tc0.n, arr, len(jobs), X, need, sync.data_ptr(), device.stream())
+    rc = _native.fn("fhe_conv_tc_stack")(tc0.q, tc0.n, arr, len(jobs), X, 0, sync.data_ptr(), device.stream())
     if rc:
         _native.check(rc)
 
@@ -471,9 +475,9 @@ def issue_k1(items, on_gemm=None) -> list:
     Returns one completion event per job (jobs of one launch share it),
     recorded on the current stream. CUDA-graph capturable."""
     comp = torch.cuda.current_stream()
-    need = max((plan.tc.x_bytes for plan, *_ in items if plan.path == "tc"), default=0)
-    if need:  # size the operand buffers before anything is enqueued
-        device.scratch("conv_tc_x", 3 * (-(-need // 256) * 256))
+    tcs = [plan.tc for plan, *_ in items if plan.path == "tc"]
+    if tcs:  # size the operand buffers before anything is enqueued (covers every launch of the call)
+        device.scratch("conv_tc_x", _x_total(tcs))
     done = [None] * len(items)
     i = 0
     while i < len(items):
@@ -487,11 +491,9 @@ def issue_k1(items, on_gemm=None) -> list:
         if items[i][0].path == "tc":
             if on_gemm:
                 on_gemm(i, "start")
-            # Jobs of one launch are independent, so their order is free: the
-            # first job's relayout is exposed (nothing runs beside it) while a
-            # later job's is overlapped with the GEMMs of the jobs before it,
-            # so jobs with a small digit-plane operand go first (stable).
-            run = sorted(items[i:j], key=lambda it: it[0].tc.x_bytes) if _stack_order() else items[i:j]
+            # Jobs of one launch are independent, so their order is free (see
+            # _stack_schedule: the launch is a two-stage relayout -> GEMM pipeline).
+            run = _stack_schedule(items[i:j]) if _stack_order() else items[i:j]
             run_tc_stack([(plan.tc, inp, out) for plan, inp, _, out in run])
             if on_gemm:
                 on_gemm(i, "end")
@@ -506,10 +508,39 @@ def issue_k1(items, on_gemm=None) -> list:
 
 
 def _stack_order() -> bool:
-    """FLASHHE_STACK_ORDER = x (default: small digit-plane operands first) | given."""
+    """FLASHHE_STACK_ORDER = johnson (default, _stack_schedule) | given."""
     import os
 
-    return os.environ.get("FLASHHE_STACK_ORDER", "x") != "given"
+    return os.environ.get("FLASHHE_STACK_ORDER", "johnson") != "given"
+
+
+# Rough per-layer stage times of a stacked K1-TC launch (B200, measured):
+# relayout by the 4 relayout warps of every CTA ~0.9 TB/s of digit-plane
+# operand; GEMM bounded by the int8 MMA rate (~4 POPS, 16 ops per 60-bit x
+# 8-bit MAC) or by the epilogue's TMEM reads (32 B per output coefficient,
+# ~9.5 TB/s over the chip), plus ~2 us of per-layer pipeline fill.
+_RELAYOUT_BPS, _MMA_OPS, _TMEM_BPS, _LAYER_FILL_S = 0.9e12, 4.0e15, 9.5e12, 2e-6
+
+
+def _stage_times(plan: "ConvPlan") -> tuple[float, float]:
+    tc = plan.tc
+    macs = plan.n_out * plan.K * 2 * plan.n
+    gemm = max(16 * macs / _MMA_OPS, plan.n_out * 2 * plan.n * 32 / _TMEM_BPS) + _LAYER_FILL_S
+    return tc.x_bytes / _RELAYOUT_BPS, gemm
+
+
+def _stack_schedule(items):
+    """Order of the independent jobs of one stacked launch. The launch is a
+    two-stage pipeline — every job is relaid out (stage 1, relayout warps, in
+    order) and then multiplied (stage 2, the GEMM roles, in order, each job
+    once its operand is complete) — so Johnson's rule for the two-machine
+    flow shop minimises the makespan: jobs whose relayout is shorter than
+    their GEMM first, by increasing relayout time; then the others, by
+    decreasing GEMM time. Stable for equal keys."""
+    times = [_stage_times(it[0]) for it in items]
+    first = sorted((k for k, (r, g) in enumerate(times) if r < g), key=lambda k: times[k][0])
+    last = sorted((k for k, (r, g) in enumerate(times) if r >= g), key=lambda k: -times[k][1])
+    return [items[k] for k in first + last]
 
 
 def conv_plan(layer: ConvLayerSpec, layout: TileLayout, params: RingParams) -> ConvPlan:
@@ -594,13 +625,19 @@ def _bias_mask(layout: TileLayout, frag: int) -> np.ndarray:
 
 
 def conv_proposed(x: PackedTensor, layer: ConvLayerSpec, params: RingParams, lazy: bool = True,
-                  workers: int = 1) -> PackedTensor:
+                  workers: int = 1, out: torch.Tensor | None = None) -> PackedTensor:
     """Algorithm 1 (conv.py:355-411) as one K1 launch: every output channel
     and fragment at once, one modular reduction per coefficient. `lazy` and
     `workers` are accepted for API compatibility; the result is the same
-    canonical ciphertext either way (as in the reference)."""
+    canonical ciphertext either way (as in the reference). `out` (addition):
+    a device [c_o·frags, 2, n] int64 buffer the result is written into — a
+    caller running the same layer repeatedly (inference.he_forward) reuses
+    one buffer instead of a fresh large allocation per call."""
     plan = _proposed_plan(x, layer, params)
-    out = plan.run(bfv.cts_rows(x.cts))
+    if out is not None and (tuple(out.shape) != (plan.n_out, 2, params.n) or out.dtype != torch.int64
+                            or not out.is_contiguous()):
+        raise ParameterError(f"out must be a contiguous int64 [{plan.n_out}, 2, {params.n}] tensor")
+    out = plan.run(bfv.cts_rows(x.cts), out)
     cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
     return PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)
 
@@ -633,8 +670,8 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     up.wait_stream(comp)
     meta = [(x, layer, _proposed_plan(x, layer, params)) for x, layer in jobs]  # validate before enqueueing
     need = -(-max((plan.tc.x_bytes for *_, plan in meta if plan.path == "tc"), default=0) // 256) * 256
-    if need:  # issue_k1 (the non-fast jobs below) sizes the buffer 3x: do it once, before any job is enqueued
-        device.scratch("conv_tc_x", 3 * need)
+    if need:  # sized once, before any job is enqueued (every job is a one-layer launch)
+        device.scratch("conv_tc_x", need)
     # all of the call's host outputs in one pinned allocation (one allocator call, not one per job)
     sizes = [plan.n_out * 2 * params.n for *_, plan in meta]
     host_all = torch.empty(sum(sizes), dtype=torch.int64, pin_memory=True)
@@ -661,7 +698,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
             out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=comp.device)
             lay = (_native.ConvTcLayer * 1)(plan.tc.layer(inp, out))
             sync = _stack_sync_for([plan.tc])
-            X = device.scratch("conv_tc_x", 3 * need)  # already sized: never reallocated here
+            X = device.scratch("conv_tc_x", need)  # already sized: never reallocated here
             rc = fast(params.q, params.n, lay, pin.data_ptr(), pin.numel() * 8, hv.data_ptr(), hv.numel() * 8, X,
                       need, sync.data_ptr(), up.cuda_stream, comp.cuda_stream, down.cuda_stream,
                       ev_up.cuda_event, ev_comp.cuda_event)
@@ -824,20 +861,28 @@ def _rotations(cts, needed, swks, params) -> tuple[torch.Tensor, dict]:
         srcs[True] = bfv.keyswitch_rows(base, digits, bfv.COLUMN_ROTATION, swks)
         ring._bump("modmul", 2 * n * l * B)
     digs = {}
-    rows, index = [], {}
-    for step, swap in groups:
+    index = {}
+    R = torch.empty((len(groups) * B, 2, n), dtype=torch.int64, device=base.device)
+    for g, (step, swap) in enumerate(groups):
         src = srcs[swap]
+        dst = R[g * B : (g + 1) * B]
         if step == 0:
-            r = src
+            _copy_rows(dst, src)
         else:
             if swap not in digs:
                 digs[swap] = bfv.key_digits_rows(src[:, 1], params, T, l)
-            r = bfv.keyswitch_rows(src, digs[swap], step, swks)
+            bfv.keyswitch_rows(src, digs[swap], step, swks, out=dst)
             ring._bump("modmul", 2 * n * l * B)
         for b in range(B):
-            index[(b, step, swap)] = len(rows) * B + b
-        rows.append(r)
-    return torch.cat(rows, 0), index
+            index[(b, step, swap)] = g * B + b
+    return R, index
+
+
+def _copy_rows(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """Contiguous device copy (one D2D memcpy on the current stream)."""
+    src = src.contiguous()
+    _native.call("fhe_copy_2d", dst.data_ptr(), src.numel() * 8, src.data_ptr(), src.numel() * 8, src.numel() * 8, 1,
+                 device.stream())
 
 
 def _stacked_keys(swks: bfv.SwitchingKeySet, steps: tuple) -> torch.Tensor:
@@ -845,7 +890,10 @@ def _stacked_keys(swks: bfv.SwitchingKeySet, steps: tuple) -> torch.Tensor:
     cache = swks.__dict__.setdefault("_stacked", {})
     t = cache.get(steps)
     if t is None:
-        t = cache[steps] = torch.stack([swks.device_keys(s) for s in steps])
+        keys = [swks.device_keys(s) for s in steps]
+        t = cache[steps] = torch.empty((len(keys),) + tuple(keys[0].shape), dtype=torch.int64, device=keys[0].device)
+        for i, k in enumerate(keys):
+            _copy_rows(t[i], k)
     return t
 
 
@@ -894,7 +942,7 @@ def _conventional_fused(in_cts, plan, swks, params, out) -> None:
         _native.call("fhe_to_montgomery", _native.u64_array([q]), 1, 1, len(pt_rows), n, pt.data_ptr(),
                      pt_mont.data_ptr(), device.stream())
         dev = pt.device
-        K = _stacked_keys(swks, steps) if steps else torch.zeros(1, dtype=torch.int64, device=dev)
+        K = _stacked_keys(swks, steps) if steps else device.zeros_i64(1)
         st = {
             "swap": any(sw for _, sw in needed), "G": G, "tiles": tiles, "K": K, "pt": pt, "pt_mont": pt_mont,
             "g": torch.from_numpy(garr).to(dev), "gp": torch.from_numpy(gp.view(np.int64)).to(dev),
@@ -905,13 +953,17 @@ def _conventional_fused(in_cts, plan, swks, params, out) -> None:
     st = hit[1]
     ring._bump("modmul", 2 * n * (l * st["rotations"] + st["macs"]))
     base = bfv.cts_rows(in_cts).reshape(B, 2, n)
-    srcs = [base]
-    if st["swap"]:
-        digits0 = bfv.key_digits_rows(base[:, 1], params, T, l)
-        srcs.append(bfv.keyswitch_rows(base, digits0, bfv.COLUMN_ROTATION, swks))
+    nsrc = 2 if st["swap"] else 1
+    D = torch.empty((nsrc * B, l, n), dtype=torch.int64, device=base.device)  # digits of every source set
+    bfv.key_digits_rows(base[:, 1], params, T, l, out=D[:B])
+    if st["swap"]:  # src = swap * B + b: the inputs, then their column swaps
+        C = torch.empty((2 * B, 2, n), dtype=torch.int64, device=base.device)
+        _copy_rows(C[:B], base)
+        bfv.keyswitch_rows(base, D[:B], bfv.COLUMN_ROTATION, swks, out=C[B:])
         ring._bump("modmul", 2 * n * l * B)
-    C = torch.cat(srcs, 0).contiguous() if len(srcs) > 1 else base.contiguous()  # src = swap * B + b
-    D = torch.cat([bfv.key_digits_rows(src[:, 1], params, T, l) for src in srcs], 0).contiguous()
+        bfv.key_digits_rows(C[B:, 1], params, T, l, out=D[B:])
+    else:
+        C = base.contiguous()
     n_out, G, tiles = len(terms), st["G"], st["tiles"]
     chunks = max(1, min(G, -(-2 * 148 // ((n // 64) * tiles))))
     part = torch.empty((chunks, n_out, 2, n), dtype=torch.int64, device=C.device) if chunks > 1 else None

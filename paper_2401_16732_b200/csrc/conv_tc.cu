@@ -38,13 +38,17 @@
 // this layer is done, so relayout work fills the SMs that finish early (the
 // GEMM's wave-quantisation tail) and no per-layer launch gap remains.
 #include <algorithm>
+#include <atomic>
 
 #include "common.cuh"
 
 namespace fhe {
 namespace tc {
 
-constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant
+#ifndef FHE_EPI_WARPS
+#define FHE_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = FHE_EPI_WARPS;  // two (or four) per TMEM lane quadrant
 #ifndef FHE_REL_WARPS
 #define FHE_REL_WARPS 4
 #endif
@@ -62,6 +66,7 @@ constexpr int kStg = 2048;           // relayout staging bytes per warp (16 posi
 // stage ring: what 227 KB leaves after the relayout staging (kRelWarps x 2 KB) and the
 // barriers — 4 stages of the 16x16-map layers (54 KB each) fit, 3 did at 212 KB
 constexpr int kRingBudget = 227 * 1024 - kRelWarps * kStg - 1024;
+constexpr int kSlotWords = 4;  // tmem, epoch
 constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
 #ifndef FHE_RELAYOUT_STATIC
 #define FHE_RELAYOUT_STATIC 1
@@ -70,6 +75,16 @@ constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npo
 #define FHE_UNITS_PER_GRAB 1
 #endif
 constexpr int kUnitsPerGrab = FHE_UNITS_PER_GRAB;  // relayout units taken per work-counter grab
+#ifndef FHE_PF_AHEAD
+#define FHE_PF_AHEAD 4
+#endif
+constexpr int kPfAhead = FHE_PF_AHEAD;
+#ifndef FHE_XFENCE
+#define FHE_XFENCE 1  // relayout writers order their X stores into the async proxy (0: A/B probe only)
+#endif  // relayout inputs are prefetched into L2 this many layers ahead
+#ifndef FHE_EPI_PAIR
+#define FHE_EPI_PAIR 0  // 1: two TMEM chunk loads per tcgen05.wait::ld (measured 3 % slower on configs 4 and 5)
+#endif
 
 struct LayerDesc {
   const uint64_t* in;  // input ciphertext rows [n_in][2][n]
@@ -79,7 +94,8 @@ struct LayerDesc {
   const uint64_t* bias;
   const uint8_t* bmask;
   uint64_t* out;
-  size_t in_bytes, w_bytes;  // extents of the input and weights (L2 prefetch)
+  size_t in_bytes, w_bytes;  // extents of the input and weights (L2 prefetch, FHE_CHECKS)
+  size_t x_bytes, out_bytes;  // extents of this layer's X region and output (FHE_CHECKS)
   int Y, JB, F, c_i, fstride, c_o, OB, taps, h, npos, nst, stage_bytes, win_bytes, tiles, units;
   int toff;  // tiles of the previous layers mod gridDim.x: tiles are dealt round-robin over the whole stack
   int nacc;  // accumulators per tile: 1, or 2 (a 64-position tile: weights reused by both, TMEM single-buffered)
@@ -96,6 +112,7 @@ struct StackArgs {
   unsigned long long* sync;  // 3 + 3 * kMaxLayers counters (see the protocol note below)
   uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
   int n, nl;
+  int xrot;                  // 1: three X buffers rotate (layer l reuses l-3's); 0: every layer has its own
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -298,6 +315,21 @@ __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t 
 // masks, 8 in-register 4x4 byte transposes into the lane's 128-byte half
 // record, staged through the warp's shared memory (XOR-swizzled 16-byte
 // chunks) so X is written with full 128-byte lines.
+// FHE_CHECKS builds (tools/build_probe.py checked -DFHE_CHECKS=1; the sanitizer
+// substitute on a pool where compute-sanitizer is closed): every global
+// access of the kernel is bounds-checked against its operand's extent and the
+// shared-memory ring placement against the ring; a violation traps.
+#ifdef FHE_CHECKS
+#define FHE_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define FHE_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 struct UnitLoad {
   uint64_t x[16];
   uint32_t neg, keep;
@@ -327,6 +359,8 @@ __device__ __forceinline__ void relayout_load(const LayerDesc& d, int n, int uni
     int e = __shfl_sync(0xffffffffu, e0m, c) + yoff;
     const bool lo = e < n, hi = e >= 2 * n;
     e -= lo ? 0 : (hi ? 2 * n : n);
+    FHE_CHECK(e >= 0 && e < n &&
+              (const uint8_t*)(row + e) + 8 <= (const uint8_t*)d.in + d.in_bytes && (const uint64_t*)row >= d.in);
     U.x[c] = __ldg(&row[e]);
     neg |= (uint32_t)(lo || hi) << c;
   }
@@ -373,7 +407,10 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int idx = i * 32 + lane, pl = idx >> 3, ch = idx & 7, pos = half * 16 + pl;
-      if (pos < rows) dst[pos * 16 + ch] = st4[pl * 8 + (ch ^ (pl & 7))];
+      if (pos < rows) {
+        FHE_CHECK((const uint8_t*)(dst + pos * 16 + ch + 1) <= d.X + d.x_bytes);
+        dst[pos * 16 + ch] = st4[pl * 8 + (ch ^ (pl & 7))];
+      }
     }
     __syncwarp();
   }
@@ -397,10 +434,13 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
 // up to three layers, so a shared running count can reach "layer l done"
 // while a slow CTA is still on layer l (the config-5 stack, whose 80-fragment
 // stem is relaid out next to two small layers, showed exactly that).
-// The relayout warps run up to three layers ahead of the GEMM: layer l's X
-// buffer (three rotate) is overwritten only after every CTA finished the
-// GEMM of layer l-3. The loader waits for "X ready" before layer l's first
-// stage.
+// X buffers: with x_stride > 0 three buffers rotate and the relayout warps run
+// up to three layers ahead of the GEMM (layer l's buffer is overwritten only
+// after every CTA finished the GEMM of layer l-3); with x_stride == 0 every
+// layer owns its region of X and the relayout warps stream through the whole
+// stack without waiting for the GEMM (the default: the small early layers'
+// relayouts no longer throttle on the GEMMs three layers back). The loader
+// waits for "X ready" before layer l's first stage.
 // This CTA's 1/gridDim.x share of [p, p + bytes) into L2 (bulk prefetch).
 __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
   const size_t share = ((bytes + gridDim.x - 1) / gridDim.x + 15) & ~(size_t)15;
@@ -512,6 +552,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         relayout_store(d, q, lane, U0, stg);
         if (two) relayout_store(d, q, lane, U1, stg);
       }
+      // this warp's generic-proxy X stores -> the async proxy (the loaders'
+      // cp.async.bulk reads, in any CTA) and its ring staging (layer 0, epilogue
+      // warps) -> later bulk copies into the ring; then the release
+#if FHE_XFENCE
+      asm volatile("fence.proxy.async.global;");
+#endif
       asm volatile("fence.proxy.async.shared::cta;");
       __threadfence();
       __syncwarp();
@@ -540,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
         if (two) relayout_store(d, q, lane, U1, stg);
       }
     }
+    asm volatile("fence.proxy.async.global;");      // X stores -> the async proxy (cp.async.bulk readers)
     asm volatile("fence.proxy.async.shared::cta;");  // (epilogue warps) ring staging before later bulk copies
     __threadfence();  // this warp's X stores before its completion count
     __syncwarp();
@@ -669,7 +716,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
             used |= 1u << s;
             par ^= 1u << s;
-            const uint32_t sx = smem_u32(smem + s * d.stage_bytes);
+            const uint32_t pos = (uint32_t)(s * d.stage_bytes);
+            const uint32_t sx = smem_u32(smem + pos);
 #ifdef TC_PROBE_NOFILL  // timing probe only: MMAs on stale stage data, no fill traffic
             (void)sx;
             (void)xbase;
@@ -679,6 +727,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
                          "r"(win_load + wstage)
                          : "memory");
+            FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nst * d.stage_bytes) &&
+                      win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
+                      wbase + (size_t)(jb + 1) * wstage <= d.W + d.w_bytes);
             bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
             bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
 #endif
@@ -691,17 +742,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
     // ------------------------------------------------------- relayout warps
     if (tid == 32 * (2 + kEpiWarps)) TC_TRACE(2, 0);
     const bool pf = tid == 32 * (2 + kEpiWarps);  // one thread per CTA issues the L2 prefetches
-    if (pf && nl > 1) {
-      prefetch_l2(A.L[1].in, A.L[1].in_bytes);
+    if (pf) {  // the first layers' inputs (read by relayout) and layer 0's weights (read by the GEMM)
+      for (int k = 1; k <= kPfAhead && k < nl; ++k) prefetch_l2(A.L[k].in, A.L[k].in_bytes);
       prefetch_l2(A.L[0].W, A.L[0].w_bytes);
     }
     relayout_layer(0, P0);
     for (int l = 1; l < nl; ++l) {
-      if (pf) {  // next layer's input (read by relayout) and this layer's weights (read by the GEMM)
-        if (l + 1 < nl) prefetch_l2(A.L[l + 1].in, A.L[l + 1].in_bytes);
+      if (pf) {  // the input kPfAhead layers on, and this layer's weights
+        if (l + kPfAhead < nl) prefetch_l2(A.L[l + kPfAhead].in, A.L[l + kPfAhead].in_bytes);
         prefetch_l2(A.L[l].W, A.L[l].w_bytes);
       }
-      if (l >= 3) wait_count(A.sync + kGem + l - 3, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
+      if (A.xrot && l >= 3) wait_count(A.sync + kGem + l - 3, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
+      if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(2, 64 + l);  // this warp starts layer l's relayout
       relayout_layer(l, kRelWarps);
       if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(3, l);
     }
@@ -782,13 +834,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
 #ifdef TC_PROBE_NOSTORE  // timing probe only: results reduced but not stored
               if (o < c_o && (r[0] ^ r[1] ^ r[2] ^ r[3]) == 0x5eed5eedull) orow[0] = 1;
 #else
+              FHE_CHECK(o >= c_o || ((uint8_t*)(orow + 4 * k + 4) <= (uint8_t*)dout + d.out_bytes &&
+                                     s0 + 4 * k + 4 <= n));
               if (o < c_o)  // one 32-byte store per lane: a full sector (STG.256)
                 asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(orow + 4 * k), "l"(r[0]), "l"(r[1]),
                              "l"(r[2]), "l"(r[3])
                              : "memory");
 #endif
             };
-            if (kper % 2 == 0) {
+            if (FHE_EPI_PAIR && kper % 2 == 0) {
               // two chunks per TMEM round trip: both loads in flight before the
               // one wait (tcgen05.wait::ld covers every outstanding load)
 #pragma unroll 1
@@ -903,18 +957,27 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   if (n < 64 || (n & (n - 1))) return fail(FHE_ERR_VALUE, "tc path needs a power-of-two n >= 64");
   if (nl < 1 || nl > tc::kMaxLayers) return fail(FHE_ERR_VALUE, "tc stack: 1..%d layers", tc::kMaxLayers);
   if (!layers || !X || !sync) return fail(FHE_ERR_VALUE, "null tc stack operand");
-  static tc::StackArgs A;  // large: kept off the stack; launches are issued from one host thread at a time
+  // large: kept off the stack; per host thread (launches from several threads do not share it)
+  static thread_local tc::StackArgs A;
   A.q = q;
   A.w32p = h_shoup(1ull << 32, q);
   A.n = n;
   A.nl = nl;
+  A.xrot = x_stride ? 1 : 0;
+  size_t xoff = 0;
   A.sync = reinterpret_cast<unsigned long long*>(sync);
   int max_tiles = 0, ring = 0, toff = 0;
-  static int sms_now = 0;
+  // per device: the SM count (grid size) and the kernel's shared-memory attribute
+  constexpr int kMaxDevices = 64;
+  static std::atomic<int> sms_of[kMaxDevices];
+  static std::atomic<bool> attr_of[kMaxDevices];
+  int dev = 0;
+  FHE_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(FHE_ERR_VALUE, "device index %d out of range", dev);
+  int sms_now = sms_of[dev].load(std::memory_order_relaxed);
   if (!sms_now) {
-    int dev = 0;
-    FHE_CUDA(cudaGetDevice(&dev));
     FHE_CUDA(cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev));
+    sms_of[dev].store(sms_now, std::memory_order_relaxed);
   }
   for (int l = 0; l < nl; ++l) {
     const fhe_conv_tc_layer& s = layers[l];
@@ -935,7 +998,11 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
       return fail(FHE_ERR_VALUE, "tc layer %d: plane sums would exceed s32", l);
     d.in = s.in;
     d.chan = reinterpret_cast<const int2*>(s.chan);
-    d.X = X + (size_t)(l % 3) * x_stride;
+    if (x_stride) {
+      d.X = X + (size_t)(l % 3) * x_stride;
+    } else {  // own region per layer, consecutive, 256-byte aligned
+      d.X = X + xoff;
+    }
     d.W = reinterpret_cast<const uint8_t*>(s.w);
     d.bias = s.bias_delta;
     d.bmask = s.bias_mask;
@@ -955,6 +1022,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.tpos = s.pos_tile * rep;
     d.in_bytes = (size_t)s.n_in * 2 * n * 8;
     d.w_bytes = (size_t)d.OB * d.JB * d.taps * tc::kWTap;
+    d.out_bytes = (size_t)s.c_o * s.frags * 2 * n * 8;
     for (int t = 0; t < s.taps; ++t) {
       const int off = s.tap_steps[t] + s.h;
       if (off < 0 || off > 2 * s.h) return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
@@ -965,8 +1033,10 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
     if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
     d.tiles = (n / d.tpos) * d.OB * 2 * d.F;
-    if (nl > 1 && (size_t)2 * d.F * d.JB * d.Y * 256 > x_stride)
-      return fail(FHE_ERR_VALUE, "tc layer %d: X stride smaller than its operand", l);
+    const size_t xb = (size_t)2 * d.F * d.JB * d.Y * 256;
+    d.x_bytes = xb;
+    if (x_stride && nl > 1 && xb > x_stride) return fail(FHE_ERR_VALUE, "tc layer %d: X stride smaller than its operand", l);
+    xoff += (xb + 255) / 256 * 256;
     const long long units = 2ll * ((d.Y + 31) / 32) * d.JB * 2 * d.F;
     if (units > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc layer %d too large", l);
     d.units = (int)units;
@@ -976,11 +1046,10 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     ring = std::max(ring, d.nst * d.stage_bytes);
   }
   ring = std::max(ring, tc::kEpiWarps * tc::kStg);  // the epilogue warps' layer-0 staging lives in the ring
-  const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 16;
-  static bool attr = false;
-  if (!attr) {
+  const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 4 * tc::kSlotWords;
+  if (!attr_of[dev].load(std::memory_order_acquire)) {  // idempotent: a racing second set is harmless
     FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
+    attr_of[dev].store(true, std::memory_order_release);
   }
   // persistent and cooperative: every CTA must be resident for the grid barriers
   (void)max_tiles;

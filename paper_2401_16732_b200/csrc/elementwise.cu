@@ -223,7 +223,7 @@ __global__ void encrypt_combine_kernel(ModDesc mq, uint64_t p, uint64_t delta, c
                                        uint64_t* __restrict__ out, int64_t total) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
-  int64_t v = m[idx] % (int64_t)p;
+  int64_t v = m ? m[idx] % (int64_t)p : 0;  // m == NULL: encryptions of zero
   if (v < 0) v += (int64_t)p;
   const uint64_t q = mq.q;
   uint64_t t = csub(delta * (uint64_t)v, q);
@@ -297,7 +297,7 @@ __global__ void wide_fin_kernel(int n, ModDesc m, uint64_t w30, uint64_t w30p, c
 // ------------------------------------------------------- K6 decrypt round
 __global__ void decrypt_round_kernel(uint64_t p, uint64_t delta, uint64_t magic, int n,
                                      const uint64_t* __restrict__ u, uint64_t* __restrict__ mout,
-                                     uint64_t* __restrict__ maxw) {
+                                     uint64_t* __restrict__ maxw, unsigned long long* __restrict__ max_all) {
   const int64_t r = blockIdx.x;
   const uint64_t half = delta / 2;
   uint64_t local = 0;
@@ -325,8 +325,25 @@ __global__ void decrypt_round_kernel(uint64_t p, uint64_t delta, uint64_t magic,
   if (threadIdx.x == 0) {
     uint64_t mx = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = red[w] > mx ? red[w] : mx;
-    maxw[r] = mx;
+    if (maxw) maxw[r] = mx;
+    if (max_all) atomicMax(max_all, (unsigned long long)mx);
   }
+}
+
+// ------------------------------------------------------- row plumbing
+// Gather k device rows of n words (arbitrary addresses) into one contiguous
+// stack: the list form of a ciphertext batch (bfv.cts_rows of separate
+// Ciphertext objects) becomes one [k][n] operand without a torch kernel.
+constexpr int kGatherPtrs = 64;
+struct GatherPtrs {
+  const uint64_t* src[kGatherPtrs];
+};
+
+__global__ void gather_rows_kernel(const __grid_constant__ GatherPtrs P, int n, uint64_t* __restrict__ dst) {
+  const int r = blockIdx.y;
+  const uint64_t* s = P.src[r];
+  uint64_t* d = dst + (size_t)r * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) d[i] = s[i];
 }
 
 // ------------------------------------------------------------ K5 shares
@@ -974,7 +991,19 @@ int fhe_decrypt_round(uint64_t q, uint64_t p, uint64_t delta, int R, int n, cons
   if (q >= (1ull << 62)) return fail(FHE_ERR_PARAMETER, "modulus too large");
   if (!R) return FHE_OK;
   const uint64_t magic = ~0ull / delta;
-  decrypt_round_kernel<<<R, 256, 0, (cudaStream_t)stream>>>(p, delta, magic, n, u, m_out, maxw_out);
+  decrypt_round_kernel<<<R, 256, 0, (cudaStream_t)stream>>>(p, delta, magic, n, u, m_out, maxw_out, nullptr);
+  FHE_CHECK_LAUNCH("decrypt_round_kernel");
+  return FHE_OK;
+}
+
+int fhe_decrypt_round_max(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* u,
+                          uint64_t* m_out, uint64_t* max_all, void* stream) {
+  if (R < 0 || n < 1 || delta < 2 || p < 2 || !max_all) return fail(FHE_ERR_VALUE, "bad decrypt arguments");
+  if (q >= (1ull << 62)) return fail(FHE_ERR_PARAMETER, "modulus too large");
+  if (!R) return FHE_OK;
+  const uint64_t magic = ~0ull / delta;
+  decrypt_round_kernel<<<R, 256, 0, (cudaStream_t)stream>>>(p, delta, magic, n, u, m_out, nullptr,
+                                                            reinterpret_cast<unsigned long long*>(max_all));
   FHE_CHECK_LAUNCH("decrypt_round_kernel");
   return FHE_OK;
 }
@@ -1146,6 +1175,38 @@ int fhe_rot_pmac(uint64_t q, int n, int ndig, const uint64_t* C, const uint64_t*
     rot_pmac_reduce_kernel<<<grid_for(total), kThreads, 0, st>>>(q, Z, total, partial, out);
     FHE_CHECK_LAUNCH("rot_pmac_reduce_kernel");
   }
+  return FHE_OK;
+}
+
+int fhe_gather_rows(const uint64_t* const* srcs, int k, int n, uint64_t* dst, void* stream) {
+  if (k < 0 || n < 1 || (k && (!srcs || !dst))) return fail(FHE_ERR_VALUE, "bad gather arguments");
+  for (int r0 = 0; r0 < k; r0 += kGatherPtrs) {
+    GatherPtrs P;
+    const int cnt = std::min(kGatherPtrs, k - r0);
+    for (int r = 0; r < cnt; ++r) {
+      if (!srcs[r0 + r]) return fail(FHE_ERR_VALUE, "null source row %d", r0 + r);
+      P.src[r] = srcs[r0 + r];
+    }
+    const int bx = std::min(8, (n + 255) / 256);
+    gather_rows_kernel<<<dim3(bx, cnt), 256, 0, (cudaStream_t)stream>>>(P, n, dst + (size_t)r0 * n);
+    FHE_CHECK_LAUNCH("gather_rows_kernel");
+  }
+  return FHE_OK;
+}
+
+int fhe_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                void* stream) {
+  if (!height || !width) return FHE_OK;
+  if (!dst || !src) return fail(FHE_ERR_VALUE, "null copy operand");
+  FHE_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToDevice,
+                             (cudaStream_t)stream));
+  return FHE_OK;
+}
+
+int fhe_zero(void* dst, size_t bytes, void* stream) {
+  if (!bytes) return FHE_OK;
+  if (!dst) return fail(FHE_ERR_VALUE, "null zero operand");
+  FHE_CUDA(cudaMemsetAsync(dst, 0, bytes, (cudaStream_t)stream));
   return FHE_OK;
 }
 

@@ -16,6 +16,7 @@
 // one write per coefficient (the HBM roofline of 16 B/coefficient).
 // The padding x + x/16 keeps the 64-bit shared accesses at the 2-wavefront
 // minimum for every phase stride.
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -654,8 +655,9 @@ static bool row_direct_enabled() {  // FHE_NTT_ROW_DIRECT=0 selects the staged r
 
 // Radix of the row kernels' register phases (2^LOGR elements per thread,
 // n / 2^LOGR threads per row). Measured on the B200 at 512 rows: n = 4096
-// radix 8 (512 threads) 32.8 us vs radix 16 34.8 us forward; n = 2048 equal
-// at 8/16 and slower at 4. FHE_NTT_ROW_LOGR overrides it for A/B checks.
+// radix 8 (512 threads) 32.8 us vs radix 16 34.8 us forward; n = 2048 with
+// the direct kernel radix 8 13.4 us vs radix 16 14.2 us. FHE_NTT_ROW_LOGR
+// overrides it for A/B checks.
 static int row_logr(int logn) {
   static int v = -1;
   if (v < 0) {
@@ -663,7 +665,7 @@ static int row_logr(int logn) {
     v = e ? atoi(e) : 0;
     if (v < 2 || v > 4) v = 0;
   }
-  return v ? v : (logn == 12 ? 3 : 4);
+  return v ? v : 3;  // n = 2048: radix 8 (256 threads, direct first/last phases) 13.4 vs 14.2 us at 512 rows
 }
 
 template <bool INV, int LOGN>
@@ -740,11 +742,14 @@ template <int LOGR, bool INV>
 static int launch_t(const LimbSet& ls, const LoadMap& lm, uint64_t* dst, int rows, int n,
                     cudaStream_t st) {
   const size_t smem = (size_t)(n + (n >> 4) + 1) * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};  // one bit per device (cudaFuncSetAttribute is per device)
+  int dev = 0;
+  FHE_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
     FHE_CUDA(cudaFuncSetAttribute(ntt_kernel<LOGR, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   150 * 1024));
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_release);
   }
   int items = n >> LOGR;
   int threads = items < 512 ? items : 512;

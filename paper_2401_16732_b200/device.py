@@ -54,6 +54,13 @@ def empty_rows(rows: int, n: int) -> torch.Tensor:
     return torch.empty((rows, n), dtype=torch.int64, device=require_cuda())
 
 
+def zeros_i64(shape) -> torch.Tensor:
+    """Zeroed int64 device tensor via cudaMemsetAsync (fhe_zero), not a torch fill kernel."""
+    t = torch.empty(shape, dtype=torch.int64, device=require_cuda())
+    _native.call("fhe_zero", t.data_ptr(), t.numel() * 8, stream())
+    return t
+
+
 def to_device(arr: np.ndarray) -> torch.Tensor:
     """Host int64 array -> device tensor (staged through pinned memory)."""
     a = np.ascontiguousarray(arr, dtype=np.int64)

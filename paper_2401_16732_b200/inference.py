@@ -114,7 +114,10 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
         if l.kind == "conv":
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            y = conv.conv_proposed(cur, specs[l.name], P)
+            spec = specs[l.name]
+            buf = spec.__dict__.get("_out_buf")  # reused across inferences: the previous output is consumed
+            y = conv.conv_proposed(cur, spec, P, out=buf)
+            spec.__dict__["_out_buf"] = bfv.cts_rows(y.cts)
             torch.cuda.synchronize()
             t["conv_s"] += time.perf_counter() - t0
             per_conv.append(time.perf_counter() - t0)

@@ -152,7 +152,14 @@ def gather_rows(polys) -> torch.Tensor:
             return first.device()[i0 : i0 + len(polys)]
     if all(p._rows is None for p in polys):
         return device.to_device(np.stack([p._host for p in polys]))
-    return torch.stack([p.dev() for p in polys])
+    import ctypes
+
+    rows = [p.dev() for p in polys]
+    n = rows[0].shape[-1]
+    out = torch.empty((len(rows), n), dtype=torch.int64, device=rows[0].device)
+    ptrs = (ctypes.c_void_p * len(rows))(*[t.contiguous().data_ptr() for t in rows])
+    _native.call("fhe_gather_rows", ptrs, len(rows), n, out.data_ptr(), device.stream())
+    return out
 
 
 def polys_from_rows(t: torch.Tensor, modulus: int, domain: Domain) -> list[ModPoly]:
@@ -431,9 +438,8 @@ class WidePoly:
     __slots__ = ("lo", "hi", "modulus", "weight")
 
     def __init__(self, n: int, modulus: int):
-        dev = device.require_cuda()
-        self.lo = torch.zeros(n, dtype=torch.int64, device=dev)
-        self.hi = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.lo = device.zeros_i64(n)
+        self.hi = device.zeros_i64(n)
         self.modulus = modulus
         self.weight = 0
 

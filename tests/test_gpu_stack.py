@@ -39,8 +39,12 @@ def _oracle_check(P, L, out, rng, k=3):
 
 
 def _compare(layers, refs, tag):
-    for L, r in zip(layers, refs):
-        assert torch.equal(L["out"], r), f"{tag}: layer {L['layer'].name} differs from its single-layer launch"
+    bad = []
+    for k, (L, r) in enumerate(zip(layers, refs)):
+        if not torch.equal(L["out"], r):
+            rows = (L["out"] != r).reshape(L["out"].shape[0], -1).any(1).nonzero().flatten().tolist()
+            bad.append(f"#{k} {L['layer'].name}: {len(rows)} of {L['out'].shape[0]} output cts differ (first {rows[:4]})")
+    assert not bad, f"{tag}: " + "; ".join(bad)
 
 
 @pytest.mark.parametrize("workload", ["config4", "config5", "config3"])
@@ -90,10 +94,16 @@ def test_two_stacks_beyond_24_layers():
     _, a = bench.build_stack("config4", seed=41)
     _, b = bench.build_stack("config3", seed=42)
     layers = a + b
+    from paper_2401_16732_b200 import device
+
     refs = [L["plan"].run(L["dev"], torch.empty_like(L["out"])) for L in layers]
-    for rep in range(2):
+    for rep in range(3):
         for L in layers:
             L["out"].fill_(-1)
+        if rep == 2:  # poison the digit-plane scratch: a stale operand read would now show
+            conv.issue_k1([(L["plan"], L["dev"], None, L["out"]) for L in layers])  # (sizes the scratch)
+            torch.cuda.synchronize()
+            device._scratch[(torch.cuda.current_device(), "conv_tc_x")].fill_(0x5A)
         ev = conv.issue_k1([(L["plan"], L["dev"], None, L["out"]) for L in layers])
         assert len(set(map(id, ev))) == 2
         torch.cuda.synchronize()

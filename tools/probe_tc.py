@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--layer", default=None, help="only this config-4 layer name")
     ap.add_argument("--once", action="store_true", help="one launch per layer (for ncu)")
     ap.add_argument("--workload", default="config4")
+    ap.add_argument("--int", action="store_true", help="also time the integer-pipe kernel")
     args = ap.parse_args()
     P = params.default_params()
     rng = np.random.default_rng(0)
@@ -40,21 +41,24 @@ def main():
         if args.once:
             print(l.name, "ran once via", plan.path)
             continue
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for _ in range(10):
-                plan.run(inp, out)
-        g.replay()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) / 10 * 1e3
-        macs = plan.n_out * plan.K * 2 * P.n
-        print(f"{l.name:10s} {plan.path:3s} {us:8.1f} us  {macs / us / 1e6:7.1f} TMAC60/s  "
-              f"{16 * macs / us / 1e6:8.1f} int8 TOPS-equiv")
+        for path in ([plan.path, "int"] if args.int and plan.path == "tc" else [plan.path]):
+            plan.run(inp, out, path=path)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(10):
+                    plan.run(inp, out, path=path)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / 10 * 1e3
+            macs = plan.n_out * plan.K * 2 * P.n
+            print(f"{l.name:10s} {path:3s} {us:8.1f} us  {macs / us / 1e6:7.1f} TMAC60/s  "
+                  f"{16 * macs / us / 1e6:8.1f} int8 TOPS-equiv  {macs / 1e6:8.1f} M MAC60")
 
 
 if __name__ == "__main__":

@@ -34,12 +34,13 @@ def main():
     _native.call("fhe_debug_trace", None)
     t = buf.cpu().numpy().reshape(8, 4096).astype(np.int64)
     if conv._stack_order():  # issue_k1's launch order
-        layers = sorted(layers, key=lambda L: L["plan"].tc.x_bytes)
+        order = conv._stack_schedule([(L["plan"], k) for k, L in enumerate(layers)])
+        layers = [layers[k] for _, k in order]
     t0 = t[2][0]
     rel = lambda v: int(v - t0) if v else -1  # noqa: E731
     tl = 0
     toff = 0
-    print(f"{'layer':10s} {'rel_done':>9s} {'x_ready':>9s} {'mma0':>9s} {'mma_end':>9s} {'epi_end':>9s} tiles(CTA0)"
+    print(f"{'layer':10s} {'rel_start':>9s} {'rel_done':>9s} {'x_ready':>9s} {'mma0':>9s} {'mma_end':>9s} {'epi_end':>9s} tiles(CTA0)"
           f" {'mma/tile':>9s} {'wait/tile':>9s} {'epi/tile':>9s} {'commit->epi':>11s}")
     for l, L in enumerate(layers):
         d = L["plan"].tc
@@ -47,7 +48,7 @@ def main():
         mine = len(range((0 - toff) % 148, tiles, 148))
         toff = (toff + tiles) % 148
         first, last = tl, tl + mine - 1
-        print(f"{L['layer'].name:10s} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
+        print(f"{L['layer'].name:10s} {rel(t[2][64 + l]) if l else -1:9d} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
               f"{rel(t[1][last]) if mine else -1:9d} {rel(t[6][last]) if mine else -1:9d} {mine:11d}"
               f" {int(np.mean([t[1][i] - t[0][i] for i in range(first, last + 1)])) if mine else -1:9d}"
               f" {int(np.mean([t[4][i] - t[0][i] for i in range(first, last + 1)])) if mine else -1:9d}"

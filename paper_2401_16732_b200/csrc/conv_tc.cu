@@ -112,6 +112,8 @@ struct StackArgs {
   unsigned long long* sync;  // 3 + 3 * kMaxLayers counters (see the protocol note below)
   uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
   int n, nl;
+  int k8, k16, k24;          // 2^8, 2^16, 2^24 as launch values: ptxas cannot strength-reduce the epilogue's
+                             // plane recombination into shift / sign / carry sequences (one IMAD.WIDE each)
   int xrot;                  // 1: three X buffers rotate (layer l reuses l-3's); 0: every layer has its own
 };
 
@@ -760,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   } else {
     // -------------------------------------------------------------- epilogue
     const int quad = warp & 3, sub = (warp - 2) >> 2;
-    const int k8 = opaque(1 << 8), k16 = opaque(1 << 16), k24 = opaque(1 << 24);
+    const int k8 = A.k8, k16 = A.k16, k24 = A.k24;
     relayout_layer(0, P0);  // nothing to do yet but help with layer 0
     int tl = 0, nb = 0;
     uint32_t use = 0;  // per-buffer use parity (mirrors the MMA thread)
@@ -964,6 +966,9 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   A.n = n;
   A.nl = nl;
   A.xrot = x_stride ? 1 : 0;
+  A.k8 = 1 << 8;
+  A.k16 = 1 << 16;
+  A.k24 = 1 << 24;
   size_t xoff = 0;
   A.sync = reinterpret_cast<unsigned long long*>(sync);
   int max_tiles = 0, ring = 0, toff = 0;

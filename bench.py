@@ -219,7 +219,7 @@ def run_peaks():
             best = max(best, ops / (e0.elapsed_time(e1) * 1e-3))
         res[name] = best
     # dense int8 tcgen05 (M=128, N=256/128/64, K=32), one CTA per SM
-    usink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    usink = torch.zeros(8, dtype=torch.int32, device="cuda")
     for N in (256, 128, 64):
         _native.call("fhe_peak_tc_i8", 148, N, 16, usink.data_ptr(), st)
         torch.cuda.synchronize()
@@ -232,7 +232,34 @@ def run_peaks():
             torch.cuda.synchronize()
             best = max(best, 148 * it * 8 * 2 * 128 * N * 32 / (e0.elapsed_time(e1) * 1e-3))
         res["tc_i8_ops" if N == 256 else f"tc_i8_ops_n{N}"] = best
+        if N == 256:
+            cyc, ns = usink.view(torch.int64)[1:3].tolist()
+            res["tc_i8_probe_sm_mhz"] = round(cyc / ns * 1e3, 1) if ns else None
     return res
+
+
+def stack_clock_mhz(layers):
+    """SM clock during one (untimed) stacked launch: every CTA records clock64
+    and %globaltimer at its start and end (the kernel's debug-trace hook);
+    median over CTAs of cycles / ns."""
+    import torch
+
+    from paper_2401_16732_b200 import _native, conv
+
+    buf = torch.zeros(9 * 4096, dtype=torch.int64, device="cuda")
+    _native.call("fhe_debug_trace", buf.data_ptr())
+    try:
+        conv.issue_k1([(L["plan"], L["dev"], None, L["out"]) for L in layers])
+        torch.cuda.synchronize()
+    finally:
+        _native.call("fhe_debug_trace", None)
+    a = buf.cpu().numpy()
+    g = a[8 * 4096 : 8 * 4096 + 2 * 148].reshape(148, 2)
+    c = a[8 * 4096 + 512 : 8 * 4096 + 512 + 2 * 148].reshape(148, 2)
+    ok = (g[:, 1] > g[:, 0]) & (c[:, 1] > c[:, 0])
+    if not ok.any():
+        return None
+    return round(float(np.median((c[ok, 1] - c[ok, 0]) / (g[ok, 1] - g[ok, 0]) * 1e3)), 1)
 
 
 def verify_outputs(layers) -> bool:
@@ -768,6 +795,7 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
+    kernel_mhz = stack_clock_mhz(layers)
     verified = verify_outputs(layers)
     launches = launches_per_step * args.steps
     per_step = [a.elapsed_time(b) for a, b in step_ms]
@@ -801,6 +829,13 @@ def main():
                          "peak_source": "measured here: fhe_peak_tc_i8 (dense M128 N256 K32 kind::i8 MMAs, "
                                         "resident smem operands)",
                          "kernel_share_of_step": round(mma_s / step_s, 4),
+                         "kernel_sm_mhz": kernel_mhz, "peak_probe_sm_mhz": peaks.get("tc_i8_probe_sm_mhz"),
+                         "frac_at_kernel_clock": (round(achieved_tops / (peak_tops * kernel_mhz /
+                                                                         peaks["tc_i8_probe_sm_mhz"]), 4)
+                                                  if kernel_mhz and peaks.get("tc_i8_probe_sm_mhz") else None),
+                         "clock_note": "the stacked launch runs at kernel_sm_mhz (power-limited under tensor + HBM "
+                                       "load); the peak probe (no memory traffic) at peak_probe_sm_mhz; "
+                                       "frac_at_kernel_clock scales the peak to the kernel's clock",
                          "alg": "16 int8 ops per 60-bit x 8-bit MAC (8 byte planes); MACs = c_o*frags*c_i*f_w^2*2n",
                          "traffic": _traffic("conv_tc_stack_kernel"),
                          "alg_bytes_per_launch": int(alg_bytes),

@@ -68,7 +68,8 @@ int fhe_peak_butterfly(int blocks, int threads, int iters, uint64_t q, uint64_t*
                        void* stream);
 /* blocks*iters*8 dense tcgen05.mma.kind::i8 (M=128, N=n_tile, K=32; n_tile
  * 64, 128 or 256) on resident shared-memory operands: 2*128*n_tile*32 int8
- * ops each. */
+ * ops each. sink: DEVICE >= 6 uint32; words [2,4) / [4,6) receive CTA 0's
+ * SM cycles / nanoseconds of the MMA loop (its clock = cycles / ns). */
 int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stream);
 
 /* ------------------------------------------------- plans (ring.NttPlan) */

@@ -112,7 +112,7 @@ struct StackArgs {
   unsigned long long* sync;  // 3 + 3 * kMaxLayers counters (see the protocol note below)
   uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
   int n, nl;
-  int k8, k16, k24;          // 2^8, 2^16, 2^24 as launch values: ptxas cannot strength-reduce the epilogue's
+  int k1, k8, k16, k24;      // 1, 2^8, 2^16, 2^24 as launch values: ptxas cannot strength-reduce the epilogue's
                              // plane recombination into shift / sign / carry sequences (one IMAD.WIDE each)
   int xrot;                  // 1: three X buffers rotate (layer l reuses l-3's); 0: every layer has its own
 };
@@ -485,7 +485,12 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid_constant__ StackArgs A) {
+#if defined(FHE_STACK_MAXNREG)  // probe builds: a register cap instead of launch bounds
+#define FHE_STACK_BOUNDS __maxnreg__(FHE_STACK_MAXNREG)
+#else
+#define FHE_STACK_BOUNDS __launch_bounds__(kThreads, 1)
+#endif
+__global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ StackArgs A) {
   extern __shared__ __align__(1024) uint8_t smem[];
   unsigned long long* const trc = g_trace;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -528,6 +533,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = slot[0];
+  auto gtime = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (trc && tid == 0) {  // per-CTA start (globaltimer ns, SM clock)
+    trc[8 * 4096 + 2 * blockIdx.x] = gtime();
+    trc[8 * 4096 + 512 + 2 * blockIdx.x] = clock64();
+  }
   const unsigned long long e1 = slot[1];  // epoch - 1
   constexpr int P0 = kEpiWarps + kRelWarps;  // warps per CTA relaying out layer 0
   const unsigned long long Gu = (unsigned long long)G;
@@ -762,7 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   } else {
     // -------------------------------------------------------------- epilogue
     const int quad = warp & 3, sub = (warp - 2) >> 2;
-    const int k8 = A.k8, k16 = A.k16, k24 = A.k24;
+    const int k1 = A.k1, k8 = A.k8, k16 = A.k16, k24 = A.k24;
     relayout_layer(0, P0);  // nothing to do yet but help with layer 0
     int tl = 0, nb = 0;
     uint32_t use = 0;  // per-buffer use parity (mirrors the MMA thread)
@@ -810,17 +824,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
             uint64_t* orow = dout + ((size_t)(o * F + T.f) * 2 + T.p) * n + s0;
             // each warp of the quadrant takes a contiguous half of the chunks: a
             // lane then writes whole 128-byte lines of its channel row
-            const int kper = npos / 4 / (kEpiWarps / 4);
+            // the quadrant's npos/4 chunks split over its kEpiWarps/4 warps (contiguous ranges)
+            constexpr int kEpq = kEpiWarps / 4;
+            const int k_lo = sub * (npos / 4) / kEpq, k_hi = (sub + 1) * (npos / 4) / kEpq;
+            const int kper = k_hi - k_lo;
             // recombine the 4 positions of one 32-column chunk and store them
             auto finish = [&](const uint32_t* v, int k) {
               uint64_t r[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const int32_t* P = reinterpret_cast<const int32_t*>(v + 8 * j);
-                const long long lo =
-                    mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, (long long)q + P[0])));
-                const long long hi =
-                    mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, (long long)q + P[4])));
+                const long long lo = mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, mad_wide(P[0], k1, q))));
+                const long long hi = mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, mad_wide(P[4], k1, q))));
                 // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
                 const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(A.w32p, (uint64_t)hi) * q;
                 uint64_t val = (uint64_t)lo + uh;  // < 4q
@@ -848,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
               // two chunks per TMEM round trip: both loads in flight before the
               // one wait (tcgen05.wait::ld covers every outstanding load)
 #pragma unroll 1
-              for (int k = sub * kper; k < (sub + 1) * kper; k += 2) {
+              for (int k = k_lo; k < k_hi; k += 2) {
                 uint32_t va[32], vb[32];
                 TMEM_LD32(acc + k * 32, va);
                 TMEM_LD32(acc + (k + 1) * 32, vb);
@@ -858,7 +873,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
               }
             } else {
 #pragma unroll 1
-              for (int k = sub * kper; k < (sub + 1) * kper; ++k) {
+              for (int k = k_lo; k < k_hi; ++k) {
                 uint32_t v[32];
                 TMEM_LD32(acc + k * 32, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
@@ -880,6 +895,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_stack_kernel(const __grid
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * kAccCols));
+  if (trc && tid == 0) {  // per-CTA end
+    trc[8 * 4096 + 2 * blockIdx.x + 1] = gtime();
+    trc[8 * 4096 + 512 + 2 * blockIdx.x + 1] = clock64();
+  }
 }
 
 // Dense int8 tcgen05 roofline probe: back-to-back M=128 N K=32 MMAs on
@@ -903,7 +922,10 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, uint32_t* si
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *slot;
+  unsigned long long c0 = 0, g0 = 0;
   if (threadIdx.x == 0) {
+    c0 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
     const uint64_t ad = umma_desc(smem_u32(smem)), bd = umma_desc(smem_u32(smem + 4096));
     constexpr uint32_t idesc = idesc_i8(N);
     for (int it = 0; it < iters; ++it) {
@@ -913,6 +935,12 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, uint32_t* si
     mma_commit(smem_u32(bar));
   }
   mbar_wait(smem_u32(bar), 0);
+  if (threadIdx.x == 0 && blockIdx.x == 0) {  // SM clock of the probe: cycles and ns of CTA 0 (sink[2..5])
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    reinterpret_cast<unsigned long long*>(sink)[1] = clock64() - c0;
+    reinterpret_cast<unsigned long long*>(sink)[2] = g1 - g0;
+  }
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (threadIdx.x < 32) {
     uint32_t v[32];
@@ -966,6 +994,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   A.n = n;
   A.nl = nl;
   A.xrot = x_stride ? 1 : 0;
+  A.k1 = 1;
   A.k8 = 1 << 8;
   A.k16 = 1 << 16;
   A.k24 = 1 << 24;

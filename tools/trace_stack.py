@@ -27,12 +27,26 @@ def main():
     items = [(L["plan"], L["dev"], None, L["out"]) for L in layers]
     conv.issue_k1(items)
     torch.cuda.synchronize()
-    buf = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(9 * 4096, dtype=torch.int64, device="cuda")
     _native.call("fhe_debug_trace", buf.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     conv.issue_k1(items)
+    e1.record()
     torch.cuda.synchronize()
     _native.call("fhe_debug_trace", None)
-    t = buf.cpu().numpy().reshape(8, 4096).astype(np.int64)
+    allb = buf.cpu().numpy().astype(np.int64)
+    t = allb[: 8 * 4096].reshape(8, 4096)
+    ct = allb[8 * 4096 : 8 * 4096 + 2 * 148].reshape(148, 2)
+    print(f"traced launch: {e0.elapsed_time(e1) * 1e3:.1f} us (events)")
+    cc = allb[8 * 4096 + 512 : 8 * 4096 + 512 + 2 * 148].reshape(148, 2)
+    mhz = (cc[:, 1] - cc[:, 0]) / ((ct[:, 1] - ct[:, 0]) / 1e3)
+    print(f"SM clock during the launch (clock64 / globaltimer): median {np.median(mhz):.0f} MHz "
+          f"(min {mhz.min():.0f}, max {mhz.max():.0f})")
+    t0g = ct[:, 0].min()
+    ends = (ct[:, 1] - t0g) / 1e3
+    print(f"per-CTA globaltimer (us from the first CTA start): start spread {(ct[:, 0].max() - t0g) / 1e3:.1f}, "
+          f"end min {ends.min():.1f} median {np.median(ends):.1f} max {ends.max():.1f} (CTA {int(ends.argmax())})")
     if conv._stack_order():  # issue_k1's launch order
         order = conv._stack_schedule([(L["plan"], k) for k, L in enumerate(layers)])
         layers = [layers[k] for _, k in order]

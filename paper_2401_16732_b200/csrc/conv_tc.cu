@@ -39,6 +39,7 @@
 // GEMM's wave-quantisation tail) and no per-layer launch gap remains.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -76,7 +77,7 @@ constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npo
 #endif
 constexpr int kUnitsPerGrab = FHE_UNITS_PER_GRAB;  // relayout units taken per work-counter grab
 #ifndef FHE_PF_AHEAD
-#define FHE_PF_AHEAD 4
+#define FHE_PF_AHEAD 2
 #endif
 constexpr int kPfAhead = FHE_PF_AHEAD;
 #ifndef FHE_XFENCE
@@ -100,6 +101,7 @@ struct LayerDesc {
   int toff;  // tiles of the previous layers mod gridDim.x: tiles are dealt round-robin over the whole stack
   int nacc;  // accumulators per tile: 1, or 2 (a 64-position tile: weights reused by both, TMEM single-buffered)
   int tpos;  // positions per tile = npos * nacc, or npos * rep
+  int slot_bytes, nslots;  // ring partition this layer runs in: nslots slots of slot_bytes >= stage_bytes
   int rep;   // 32-position groups stacked in the 128 accumulator rows (c_o <= 128 / rep): 1, 2 or 4
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
@@ -497,7 +499,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   const int n = A.n, nl = A.nl, G = gridDim.x;
   const uint64_t q = A.q;
   int ring_bytes = kEpiWarps * kStg;  // (same rule as the host's smem sizing)
-  for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].nst * A.L[l].stage_bytes);
+  for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].nslots * A.L[l].slot_bytes);
   // relayout staging: the relayout warps own areas after the ring; the epilogue
   // warps (layer 0 only, before any stage is loaded) borrow the ring
   uint8_t* stg = warp >= 2 + kEpiWarps ? smem + ring_bytes + (warp - 2 - kEpiWarps) * kStg
@@ -576,8 +578,15 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
 #endif
       asm volatile("fence.proxy.async.shared::cta;");
       __threadfence();
+      // every lane's X stores happen-before lane 0 (warp barrier), and lane 0's
+      // own gpu-scope fence AFTER the barrier makes them (cumulatively) visible
+      // before its completion count: a fence only before the barrier orders a
+      // lane's stores with that lane's later operations, not lane 0's atomic
       __syncwarp();
-      if (lane == 0) atomicAdd(A.sync + kRdy + l, 1ull);
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(A.sync + kRdy + l, 1ull);
+      }
       return;
     }
 #endif
@@ -606,7 +615,10 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     asm volatile("fence.proxy.async.shared::cta;");  // (epilogue warps) ring staging before later bulk copies
     __threadfence();  // this warp's X stores before its completion count
     __syncwarp();
-    if (lane == 0) atomicAdd(A.sync + kRdy + l, 1ull);
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(A.sync + kRdy + l, 1ull);
+    }
   };
 
   if (warp == 0) {
@@ -617,7 +629,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     // weights: half the weight traffic per position). Per-buffer use counts
     // give the tmem_full / tmem_empty parities on both sides.
     {  // the whole warp runs the issue loop; elect.sync issues (see mma_i8w_elect)
-      int s_mma = 0, prev_sb = -1, tl = 0, nb = 0;
+      int s_mma = 0, prev_sb = -1, prev_ns = -1, tl = 0, nb = 0;
       uint32_t par = 0, use = 0;  // per-stage full parity; per-buffer use parity (bit b)
       const uint64_t desc0 = umma_desc(smem_u32(smem));  // ring base; stage s adds s * stage_bytes / 16
       const uint32_t dlo0 = (uint32_t)desc0, dhi = (uint32_t)(desc0 >> 32);
@@ -629,11 +641,12 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
         // the parameter bank (dependent LDCs) at every stage.
         const int tiles = d.tiles, t0 = first_tile(d);
         if (tiles <= t0) continue;  // no tiles of this layer here (the loader skips it too)
-        const int stage_bytes = d.stage_bytes, JB = d.JB, nacc = d.nacc, taps = d.taps, nst = d.nst;
-        if (stage_bytes != prev_sb) s_mma = 0;  // the loader drained and re-partitioned the ring
-        prev_sb = stage_bytes;
+        const int slot_bytes = d.slot_bytes, JB = d.JB, nacc = d.nacc, taps = d.taps, nst = d.nslots;
+        if (slot_bytes != prev_sb || nst != prev_ns) s_mma = 0;  // the loader drained and re-partitioned the ring
+        prev_sb = slot_bytes;
+        prev_ns = nst;
         const uint32_t idesc = idesc_i8(8 * d.npos);
-        const uint32_t sstep = (uint32_t)(stage_bytes >> 4), wdesc = (uint32_t)(d.win_bytes >> 4);
+        const uint32_t sstep = (uint32_t)(slot_bytes >> 4), wdesc = (uint32_t)(d.win_bytes >> 4);
         const uint32_t adelta = (uint32_t)(d.npos * 256 >> 4);  // second accumulator's positions
         uint32_t off16[16];  // this layer's DRot offsets in 16-byte descriptor units (fast paths)
 #pragma unroll
@@ -705,17 +718,18 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   } else if (warp == 1) {
     // ------------------------------------------------------------ stage loads
     if (lane == 0) {
-      int s_ld = 0, prev_sb = -1;
+      int s_ld = 0, prev_sb = -1, prev_ns = -1;
       uint32_t par = 0, used = 0;  // per-stage fill parity; stages filled at least once
       for (int l = 0; l < nl; ++l) {
         const LayerDesc& d = A.L[l];
         if (d.tiles <= first_tile(d)) continue;  // no tiles of this layer here
-        if (d.stage_bytes != prev_sb) {
+        if (d.slot_bytes != prev_sb || d.nslots != prev_ns) {
           // new ring partition: every stage of the old one must be consumed first
           for (int s = 0; s < kMaxStages; ++s)
             if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
           s_ld = 0;
-          prev_sb = d.stage_bytes;
+          prev_sb = d.slot_bytes;
+          prev_ns = d.nslots;
         }
         wait_count(A.sync + kRdy + l, ready_target(l));  // layer l's X is complete
         TC_TRACE(7, l);
@@ -732,7 +746,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
             used |= 1u << s;
             par ^= 1u << s;
-            const uint32_t pos = (uint32_t)(s * d.stage_bytes);
+            const uint32_t pos = (uint32_t)(s * d.slot_bytes);
             const uint32_t sx = smem_u32(smem + pos);
 #ifdef TC_PROBE_NOFILL  // timing probe only: MMAs on stale stage data, no fill traffic
             (void)sx;
@@ -743,13 +757,14 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
                          "r"(win_load + wstage)
                          : "memory");
-            FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nst * d.stage_bytes) &&
+            FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nslots * d.slot_bytes) &&
+                      d.stage_bytes <= d.slot_bytes &&
                       win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
                       wbase + (size_t)(jb + 1) * wstage <= d.W + d.w_bytes);
             bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
             bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
 #endif
-            s_ld = s + 1 == d.nst ? 0 : s + 1;
+            s_ld = s + 1 == d.nslots ? 0 : s + 1;
           }
         }
       }
@@ -888,7 +903,10 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
       }
       // this CTA consumed all of layer l's X (every tile's MMAs completed)
       asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue));
-      if (tid == 64) atomicAdd(A.sync + kGem + l, 1ull);
+      if (tid == 64) {
+        __threadfence();
+        atomicAdd(A.sync + kGem + l, 1ull);
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -981,6 +999,15 @@ int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stre
   return FHE_OK;
 }
 
+static bool keep_partition() {  // FHE_TC_KEEP_RING=0: re-partition at every stage-size change (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_TC_KEEP_RING");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl, uint8_t* X, size_t x_stride,
                       uint64_t* sync, void* stream) {
   if (q < (1ull << 56) || q >= (1ull << 62)) return fail(FHE_ERR_VALUE, "tc path needs 2^56 <= q < 2^62");
@@ -1066,6 +1093,16 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.stage_bytes = d.win_bytes + d.taps * tc::kWTap;
     d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
     if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
+    // Keep the previous layer's ring partition when this layer's stages fit its
+    // slots without losing depth: the loader then streams on without draining
+    // the ring at the layer boundary (s3 -> s4 layers, same-shape layers).
+    if (l > 0 && d.stage_bytes <= A.L[l - 1].slot_bytes && A.L[l - 1].nslots >= d.nst && keep_partition()) {
+      d.slot_bytes = A.L[l - 1].slot_bytes;
+      d.nslots = A.L[l - 1].nslots;
+    } else {
+      d.slot_bytes = d.stage_bytes;
+      d.nslots = d.nst;
+    }
     d.tiles = (n / d.tpos) * d.OB * 2 * d.F;
     const size_t xb = (size_t)2 * d.F * d.JB * d.Y * 256;
     d.x_bytes = xb;
@@ -1077,7 +1114,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     max_tiles = std::max(max_tiles, d.tiles);
     d.toff = toff;
     toff = (toff + d.tiles) % sms_now;
-    ring = std::max(ring, d.nst * d.stage_bytes);
+    ring = std::max(ring, d.nslots * d.slot_bytes);
   }
   ring = std::max(ring, tc::kEpiWarps * tc::kStg);  // the epilogue warps' layer-0 staging lives in the ring
   const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 4 * tc::kSlotWords;

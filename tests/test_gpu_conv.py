@@ -124,6 +124,35 @@ def test_conv_proposed_stream_matches_single_calls():
         assert np.array_equal(_out(y.cts), ref)
 
 
+def test_conv_proposed_stream_large_pinned_after_pageable():
+    """Large pinned host jobs after a pageable tensor-core job (which takes
+    the issue_k1 path) in one call, with the digit-plane scratch first grown
+    to its final size inside the call: every job still equals conv_proposed
+    (the fast path once kept a scratch pointer across a growth),
+    repeated so the allocator recycles the inputs and outputs."""
+    from paper_2401_16732_b200 import bfv, conv, device
+
+    P = _P()
+    rng = np.random.default_rng(78)
+    geoms = [(16, 3, 32, 40, False), (64, 3, 64, 64, True), (56, 3, 64, 64, True), (8, 3, 64, 130, True)]
+    specs = []
+    for H, f_w, c_i, c_o, pin in geoms:
+        lay = conv.layout_direct(P, H, H, f_w)
+        spec = conv.ConvLayerSpec(H, H, f_w, c_i, c_o, rng.integers(-127, 128, (c_o, c_i, f_w, f_w)))
+        specs.append((lay, spec, c_i, pin))
+    for rep in range(2):
+        jobs, refs = [], []
+        for lay, spec, c_i, pin in specs:
+            arr = rng.integers(0, Q, (lay.ct_count(c_i), 2, N), dtype=np.int64)
+            refs.append(_out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, c_i), spec, P).cts))
+            jobs.append((conv.PackedTensor(bfv.cts_from_host(arr, Q, pin=pin), lay, c_i), spec))
+        torch.cuda.synchronize()
+        device._scratch.pop((torch.cuda.current_device(), "conv_tc_x"), None)  # the call sizes it afresh
+        outs = conv.conv_proposed_stream(jobs, P)
+        for k, (y, ref) in enumerate(zip(outs, refs)):
+            assert np.array_equal(y.cts.host_stack(), ref), f"rep {rep} job {k}"
+
+
 def test_conv_cfg1_full_arrays():
     from paper_2401_16732_b200 import conv
 

@@ -43,7 +43,19 @@ def _compare(layers, refs, tag):
     for k, (L, r) in enumerate(zip(layers, refs)):
         if not torch.equal(L["out"], r):
             rows = (L["out"] != r).reshape(L["out"].shape[0], -1).any(1).nonzero().flatten().tolist()
-            bad.append(f"#{k} {L['layer'].name}: {len(rows)} of {L['out'].shape[0]} output cts differ (first {rows[:4]})")
+            o = L["out"].reshape(L["out"].shape[0], -1)
+            untouched = int((o == -1).all(1).sum())
+            diff = int((L["out"] != r).sum())
+            dpos = (L["out"] != r).reshape(L["out"].shape[0], 2, -1).any(0)  # [2, n] positions differing in any ct
+            spans = []
+            for p in range(2):
+                idx = dpos[p].nonzero().flatten().tolist()
+                if idx:
+                    spans.append(f"poly {p}: {len(idx)} slots in [{idx[0]}, {idx[-1]}]")
+            bad.append(f"#{k} {L['layer'].name} ({'; '.join(spans)}): "
+                       f"{len(rows)} of {L['out'].shape[0]} output cts differ (first {rows[:4]}), "
+                       f"{diff} coefficients, {untouched} rows never written, out[0,0,:3]={o[0, :3].tolist()} "
+                       f"ref[0,0,:3]={r.reshape(r.shape[0], -1)[0, :3].tolist()}")
     assert not bad, f"{tag}: " + "; ".join(bad)
 
 

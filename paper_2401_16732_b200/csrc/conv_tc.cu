@@ -67,7 +67,7 @@ constexpr int kStg = 2048;           // relayout staging bytes per warp (16 posi
 // stage ring: what 227 KB leaves after the relayout staging (kRelWarps x 2 KB) and the
 // barriers — 4 stages of the 16x16-map layers (54 KB each) fit, 3 did at 212 KB
 constexpr int kRingBudget = 227 * 1024 - kRelWarps * kStg - 1024;
-constexpr int kSlotWords = 4;  // tmem, epoch
+constexpr int kSlotWords = 4 + kMaxLayers;  // tmem, epoch, (pad), per-layer relayout-done counts of this CTA
 constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npos <= 32)
 #ifndef FHE_RELAYOUT_STATIC
 #define FHE_RELAYOUT_STATIC 1
@@ -430,8 +430,9 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
 //                       mode only), taken g = kUnitsPerGrab units at a time:
 //                       launch e starts at (e-1)·(g·ceil(units/g) + g·G·P(l))
 //                       (each participating warp overshoots it exactly once)
-//   sync[kRdy + l]      layer l's relayout completions (one per participating
-//                       warp): its X is complete at e·G·P(l)
+//   sync[kRdy + l]      layer l's relayout completions, one per CTA (its last
+//                       participating warp publishes, see `publish`): its X
+//                       is complete at e·G
 //   sync[kGem + l]      layer l's GEMM completions (one per CTA): its X has
 //                       been fully consumed at e·G
 // Every layer has its OWN completion counters: warps and CTAs run ahead by
@@ -514,6 +515,8 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   auto tempty_bar = [&](int b) { return bar0 + 8 * (2 * kMaxStages + 2 + b); };
 
   if (tid == 0) slot[1] = (unsigned)(atomicAdd(A.sync, 1ull) / (unsigned long long)G);  // epoch - 1
+  unsigned* const cta_done = reinterpret_cast<unsigned*>(slot + 4);  // [kMaxLayers] warps of this CTA done
+  if (tid < kMaxLayers) cta_done[tid] = 0;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
                  "n"(2 * kAccCols));
@@ -547,12 +550,25 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   const unsigned long long e1 = slot[1];  // epoch - 1
   constexpr int P0 = kEpiWarps + kRelWarps;  // warps per CTA relaying out layer 0
   const unsigned long long Gu = (unsigned long long)G;
-  auto ready_target = [&](int l) { return (e1 + 1) * Gu * (l == 0 ? P0 : kRelWarps); };
+  auto ready_target = [&](int) { return (e1 + 1) * Gu; };  // one count per CTA per layer
   auto gemm_target = [&](int) { return (e1 + 1) * Gu; };
   // relayout units of layer l until none is left, then publish this warp's completion
   // relayout units of layer l until none is left, then publish this warp's
   // completion. The next grab's atomic is issued before the current unit is
   // processed, so its round trip overlaps useful work.
+  // A warp finished its share of layer l's relayout (lane 0, after the warp
+  // barrier): the CTA's last participating warp publishes ONE count for the
+  // CTA (148 global atomics per layer instead of 148 x participants, all on
+  // one address). Each warp's gpu-scope fence precedes its shared-memory
+  // increment; the last warp, having read every increment, fences again
+  // before the global count (cumulative release of all the CTA's X stores).
+  auto publish = [&](int l, int participants) {
+    __threadfence();
+    if (atomicAdd(&cta_done[l], 1u) == (unsigned)participants - 1) {
+      __threadfence();
+      atomicAdd(A.sync + kRdy + l, 1ull);
+    }
+  };
   auto relayout_layer = [&](int l, int participants) {
     const LayerDesc& d = A.L[l];
 #if FHE_RELAYOUT_STATIC
@@ -583,10 +599,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
       // before its completion count: a fence only before the barrier orders a
       // lane's stores with that lane's later operations, not lane 0's atomic
       __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        atomicAdd(A.sync + kRdy + l, 1ull);
-      }
+      if (lane == 0) publish(l, participants);
       return;
     }
 #endif
@@ -615,10 +628,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     asm volatile("fence.proxy.async.shared::cta;");  // (epilogue warps) ring staging before later bulk copies
     __threadfence();  // this warp's X stores before its completion count
     __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      atomicAdd(A.sync + kRdy + l, 1ull);
-    }
+    if (lane == 0) publish(l, participants);
   };
 
   if (warp == 0) {

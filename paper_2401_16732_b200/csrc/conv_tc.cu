@@ -543,6 +543,8 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
   };
+  if (trc && tid == 0 && blockIdx.x == 0)
+    for (int l = 0; l < nl; ++l) trc[7 * 4096 + 2048 + l] = A.L[l].toff;  // the launch's tile dealing
   if (trc && tid == 0) {  // per-CTA start (globaltimer ns, SM clock)
     trc[8 * 4096 + 2 * blockIdx.x] = gtime();
     trc[8 * 4096 + 512 + 2 * blockIdx.x] = clock64();
@@ -1009,6 +1011,18 @@ int fhe_peak_tc_i8(int blocks, int n_tile, int iters, uint32_t* sink, void* stre
   return FHE_OK;
 }
 
+// FHE_TC_BALANCE=1: cost-aware dealing of each layer's extra tiles (measured
+// 1 % slower than the round-robin continuation on configs 4 and 5: the
+// per-tile cost estimate misses the pipeline overlap; kept as an option)
+static bool balance_tiles() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_TC_BALANCE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static bool keep_partition() {  // FHE_TC_KEEP_RING=0: re-partition at every stage-size change (A/B checks)
   static int v = -1;
   if (v < 0) {
@@ -1038,6 +1052,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   size_t xoff = 0;
   A.sync = reinterpret_cast<unsigned long long*>(sync);
   int max_tiles = 0, ring = 0, toff = 0;
+  double load[1024] = {0};  // estimated work per CTA (tile dealing, see balance_tiles)
   // per device: the SM count (grid size) and the kernel's shared-memory attribute
   constexpr int kMaxDevices = 64;
   static std::atomic<int> sms_of[kMaxDevices];
@@ -1050,6 +1065,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     FHE_CUDA(cudaDeviceGetAttribute(&sms_now, cudaDevAttrMultiProcessorCount, dev));
     sms_of[dev].store(sms_now, std::memory_order_relaxed);
   }
+  if (sms_now > 1024) return fail(FHE_ERR_VALUE, "too many SMs");
   for (int l = 0; l < nl; ++l) {
     const fhe_conv_tc_layer& s = layers[l];
     tc::LayerDesc& d = A.L[l];
@@ -1122,8 +1138,33 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     if (units > (1ll << 30)) return fail(FHE_ERR_VALUE, "tc layer %d too large", l);
     d.units = (int)units;
     max_tiles = std::max(max_tiles, d.tiles);
-    d.toff = toff;
-    toff = (toff + d.tiles) % sms_now;
+    if (balance_tiles()) {
+      // Cost-aware dealing: every CTA gets tiles/G tiles of this layer, the
+      // tiles % G extra ones go to a window of consecutive CTAs; place that
+      // window where the CTAs' estimated accumulated work is lowest (tile cost:
+      // its MMAs, 128 cycles each, or the epilogue's ~3.4k cycles, whichever
+      // binds), so the extra tiles of successive big layers do not pile up on
+      // the same CTAs and the stack's slowest CTA finishes earlier.
+      const int G = sms_now, extra = d.tiles % G;
+      const double cost = std::max(128.0 * d.JB * d.taps, 3400.0) + 600.0;
+      int best = toff;
+      if (extra > 0 && extra < G) {
+        double best_max = 1e300;
+        for (int st = 0; st < G; ++st) {  // window [st, st + extra) cyclic: its max load
+          double mx = 0;
+          for (int k = 0; k < extra; ++k) mx = std::max(mx, load[(st + k) % G]);
+          if (mx < best_max - 1e-9) {
+            best_max = mx;
+            best = st;
+          }
+        }
+      }
+      d.toff = best;
+      for (int b = 0; b < G; ++b) load[b] += cost * (d.tiles / G + (((b - best + G) % G) < extra ? 1 : 0));
+    } else {
+      d.toff = toff;
+      toff = (toff + d.tiles) % sms_now;
+    }
     ring = std::max(ring, d.nslots * d.slot_bytes);
   }
   ring = std::max(ring, tc::kEpiWarps * tc::kStg);  // the epilogue warps' layer-0 staging lives in the ring

@@ -248,3 +248,41 @@ def test_wire_frames_match_reference_frames():
     same = b"".join(bfv.ct_to_bytes(c, seed_compress=False) for c in (cts["summed"], cts["fresh"]))
     stack = bfv.cts_from_bytes(same, 2, P, pin=False).host_stack()
     assert np.array_equal(stack[1, 0], arr["fresh_c0"]) and np.array_equal(stack[0, 1], arr["summed_c1"])
+
+
+def test_stack_schedule_is_johnson_optimal():
+    """conv._stack_schedule orders a stacked launch's independent jobs by
+    Johnson's rule for the two-stage (relayout -> GEMM) flow shop: on random
+    small instances its makespan equals the brute-force optimum."""
+    import itertools
+    from types import SimpleNamespace
+
+    from paper_2401_16732_b200 import conv
+
+    def makespan(order, times):
+        t1 = t2 = 0.0
+        for k in order:
+            r, g = times[k]
+            t1 += r
+            t2 = max(t2, t1) + g
+        return t2
+
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        m = int(rng.integers(2, 7))
+        times = [(float(rng.uniform(0.1, 5)), float(rng.uniform(0.1, 5))) for _ in range(m)]
+        stub = {}
+        items = []
+        for k, (r, g) in enumerate(times):
+            plan = SimpleNamespace(tag=k)
+            stub[k] = (r, g)
+            items.append((plan, None, None, None))
+        orig = conv._stage_times
+        conv._stage_times = lambda plan: stub[plan.tag]  # the rule under test, on chosen stage times
+        try:
+            order = [it[0].tag for it in conv._stack_schedule(items)]
+        finally:
+            conv._stage_times = orig
+        assert sorted(order) == list(range(m))
+        best = min(makespan(p, times) for p in itertools.permutations(range(m)))
+        assert abs(makespan(order, times) - best) < 1e-9

@@ -59,8 +59,8 @@ def main():
     for l, L in enumerate(layers):
         d = L["plan"].tc
         tiles = (P.n // (d.pos_tile * d.rep)) * -(-d.c_o // 128) * 2 * d.frags
+        toff = int(t[7][2048 + l])  # the kernel's dealing offset of this layer
         mine = len(range((0 - toff) % 148, tiles, 148))
-        toff = (toff + tiles) % 148
         first, last = tl, tl + mine - 1
         print(f"{L['layer'].name:10s} {rel(t[2][64 + l]) if l else -1:9d} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
               f"{rel(t[1][last]) if mine else -1:9d} {rel(t[6][last]) if mine else -1:9d} {mine:11d}"

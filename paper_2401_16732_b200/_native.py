@@ -148,7 +148,7 @@ class ConvTcLayer(ctypes.Structure):
     _fields_ = [
         ("in_", _vp), ("n_in", _int), ("c_i", _int), ("frags", _int), ("fstride", _int), ("chan", _vp), ("h", _int),
         ("w", _vp), ("c_o", _int), ("taps", _int), ("pos_tile", _int), ("tap_steps", _vp),
-        ("bias_delta", _vp), ("bias_mask", _vp), ("out", _vp), ("rep", _int),
+        ("bias_delta", _vp), ("bias_mask", _vp), ("out", _vp), ("rep", _int), ("tsplit", _int),
     ]
 
 

@@ -322,30 +322,46 @@ class ConvTcPlan:
         return 32
 
     @staticmethod
-    def rep_for(c_o: int, JB: int, taps: int, h: int) -> int:
-        """Position groups stacked in the 128 accumulator rows (csrc/conv_tc.cu
-        LayerDesc.rep). A layer with c_o <= 64 fills only c_o TMEM lanes, so
-        only the warps of c_o/32 lane quadrants (SM sub-partitions) can read
-        its accumulators: short contractions (JB·taps <= 16 MMAs per tile —
-        the stems) are then bound by the epilogue's TMEM reads, not the MMAs.
-        With rep groups, rows r·128/rep + o compute channel o at positions
-        32 r.. of the tile (the same window, tap offsets + 32 r): every
-        quadrant's warps run the epilogue, for the same MMA work per position.
-        FLASHHE_TC_REP (1 | 2 | 4) forces a value where it is valid."""
+    def rep_for(c_o: int, JB: int, taps: int, h: int) -> tuple[int, int]:
+        """(rep, tsplit): position groups stacked in the 128 accumulator rows
+        (csrc/conv_tc.cu LayerDesc.rep) and the number of pipeline stages a
+        32-channel block's MMAs are spread over. A layer with c_o <= 64 fills
+        only c_o TMEM lanes, so only the warps of c_o/32 lane quadrants (SM
+        sub-partitions) can read its accumulators: short contractions (JB·taps
+        <= 18 MMAs per 32 positions — the stems, the 64-channel layers) are
+        then bound by the epilogue, not the MMAs. With rep groups, rows
+        r·128/rep + o compute channel o at positions 32 r.. of the tile (the
+        same window, tap offsets + 32 r): every quadrant's warps run the
+        epilogue, for the same MMA work per position. When the taps·rep weight
+        tiles make a stage too large for two in flight, they can be split over
+        tsplit stages (each reloads the window) — FLASHHE_TC_TSPLIT=1; off by
+        default: the 64-channel 3x3 layers ran 5-10 % slower that way (two
+        stages in flight starve the MMAs). FLASHHE_TC_REP (1 | 2 | 4) forces a
+        rep where it is valid."""
         import os
 
+        splits = (1, 2, 3) if os.environ.get("FLASHHE_TC_TSPLIT") == "1" else (1,)
+
+        def fit(r):
+            for ts in splits:
+                if (taps * r) % ts:
+                    continue
+                stage = -(-(32 * r + 2 * h) * 256 // 1024) * 1024 + (taps * r // ts) * 32 * ConvTcPlan.OC_TILE
+                if 2 * stage <= 218 * 1024:
+                    return ts
+            return None
+
         def ok(r):
-            if r == 1:
-                return True
-            stage = -(-(32 * r + 2 * h) * 256 // 1024) * 1024 + taps * r * 32 * ConvTcPlan.OC_TILE
-            return c_o <= ConvTcPlan.OC_TILE // r and taps * r <= 64 and 2 * stage <= 218 * 1024
+            return r == 1 or (c_o <= ConvTcPlan.OC_TILE // r and taps * r <= 64 and fit(r) is not None)
 
         forced = os.environ.get("FLASHHE_TC_REP")
-        if forced:
-            return int(forced) if ok(int(forced)) else 1
-        if JB * taps > 16:
-            return 1
-        return next(r for r in (4, 2, 1) if ok(r))
+        if forced and ok(int(forced)):
+            r = int(forced)
+        elif forced or JB * taps > (18 if len(splits) > 1 else 16):
+            r = 1
+        else:
+            r = next(r for r in (4, 2, 1) if ok(r))
+        return r, (fit(r) or 1) if r > 1 else 1
 
     @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
@@ -373,7 +389,7 @@ class ConvTcPlan:
         self.pos_tile = self.pos_tile_for(self.c_o, self.n, self.frags, self.h, self.taps, self.c_i)
         N = self.OC_TILE
         OB, JB = -(-self.c_o // N), -(-self.c_i // 32)
-        self.rep = self.rep_for(self.c_o, JB, self.taps, self.h) if self.pos_tile == 32 else 1
+        self.rep, self.tsplit = self.rep_for(self.c_o, JB, self.taps, self.h) if self.pos_tile == 32 else (1, 1)
         j = np.arange(self.c_i)
         if chan is not None:
             chan = np.asarray(chan, dtype=np.int64).reshape(self.c_i, 2)
@@ -406,7 +422,7 @@ class ConvTcPlan:
         return _native.ConvTcLayer(
             inp.data_ptr(), inp.numel() // (2 * self.n), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
             self.c_o, self.taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
-            device.ptr(self.mask), out.data_ptr(), self.rep)
+            device.ptr(self.mask), out.data_ptr(), self.rep, self.tsplit)
 
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
         """One cooperative persistent launch of this layer alone (relayout,

@@ -102,6 +102,7 @@ struct LayerDesc {
   int nacc;  // accumulators per tile: 1, or 2 (a 64-position tile: weights reused by both, TMEM single-buffered)
   int tpos;  // positions per tile = npos * nacc, or npos * rep
   int slot_bytes, nslots;  // ring partition this layer runs in: nslots slots of slot_bytes >= stage_bytes
+  int tsplit, tg;          // tap groups per 32-channel block (stages per block) and taps per group
   int rep;   // 32-position groups stacked in the 128 accumulator rows (c_o <= 128 / rep): 1, 2 or 4
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
@@ -543,8 +544,6 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
   };
-  if (trc && tid == 0 && blockIdx.x == 0)
-    for (int l = 0; l < nl; ++l) trc[7 * 4096 + 2048 + l] = A.L[l].toff;  // the launch's tile dealing
   if (trc && tid == 0) {  // per-CTA start (globaltimer ns, SM clock)
     trc[8 * 4096 + 2 * blockIdx.x] = gtime();
     trc[8 * 4096 + 512 + 2 * blockIdx.x] = clock64();
@@ -663,6 +662,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
         uint32_t off16[16];  // this layer's DRot offsets in 16-byte descriptor units (fast paths)
 #pragma unroll
         for (int tp = 0; tp < 16; ++tp) off16[tp] = tp < taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
+        const int TS = d.tsplit, tg = d.tg, nstage = JB * TS;
         for (int t = t0; t < tiles; t += G, ++tl) {
           int b0 = 0, b1 = 1;
           if (nacc == 1) {
@@ -671,7 +671,8 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
           }
           if (lane == 0) TC_TRACE(0, tl);
           const bool more_tiles = t + G < tiles;
-          for (int jb = 0; jb < JB; ++jb) {
+          for (int st = 0; st < nstage; ++st) {  // stage = (32-channel block, tap group)
+            const int jb = st;                   // (the fast paths run with one tap group: st == jb)
             const int s = s_mma;
             const int s_next = s + 1 == nst ? 0 : s + 1;
             if (!pre) {
@@ -682,10 +683,10 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t blo0 = dlo0 + (uint32_t)s * sstep;  // window at the stage base
             const uint32_t alo = blo0 + wdesc;                  // weights after the window
-            const bool has_next = jb + 1 < JB || more_tiles;    // next stage of this layer on this CTA
+            const bool has_next = st + 1 < nstage || more_tiles;  // next stage of this layer on this CTA
             for (int a = 0; a < nacc; ++a) {
               const int b = a == 0 ? b0 : b1;
-              if (jb == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
+              if (st == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
                 mbar_wait(tempty_bar(b), ((use >> b) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 if (a == 0 && lane == 0) TC_TRACE(4, tl);
@@ -699,7 +700,14 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                   pre = true;
                 }
               };
-              if (taps == 9) {
+              if (TS > 1) {  // one tap group of several: offsets of group g, weights at the stage base
+                const int g = st % TS;
+                for (int tp = 0; tp < tg; ++tp) {
+                  if (tp == tg - 1) wait_next();
+                  mma_i8w_elect(acc, alo + (uint32_t)(tp * (4096 >> 4)), blo + (uint32_t)d.tap_off[g * tg + tp] * 16,
+                                dhi, idesc, (st | tp) != 0);
+                }
+              } else if (taps == 9) {
                 issue_taps<9>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
               } else if (taps == 1) {
                 issue_taps<1>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
@@ -753,7 +761,8 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
           const Tile T = tile_of(t, d, n);
           const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
           const uint8_t* wbase = d.W + (size_t)T.ob * d.JB * wstage;
-          for (int jb = 0; jb < d.JB; ++jb) {
+          for (int st = 0; st < d.JB * d.tsplit; ++st) {  // stage = (32-channel block, tap group)
+            const int jb = st / d.tsplit, g = st - jb * d.tsplit;
             const int s = s_ld;
             if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
             used |= 1u << s;
@@ -766,15 +775,16 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             (void)wbase;
             mbar_arrive(full_bar(s));
 #else
+            const uint32_t wgroup = (uint32_t)d.tg * kWTap;  // this stage's tap group of weights
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
-                         "r"(win_load + wstage)
+                         "r"(win_load + wgroup)
                          : "memory");
             FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nslots * d.slot_bytes) &&
                       d.stage_bytes <= d.slot_bytes &&
                       win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
-                      wbase + (size_t)(jb + 1) * wstage <= d.W + d.w_bytes);
+                      wbase + (size_t)jb * wstage + (size_t)(g + 1) * wgroup <= d.W + d.w_bytes);
             bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
-            bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
+            bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage + (size_t)g * wgroup, wgroup, full_bar(s));
 #endif
             s_ld = s + 1 == d.nslots ? 0 : s + 1;
           }
@@ -899,6 +909,8 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                 finish(vb, k + 1);
               }
             } else {
+              // (unrolling by two — distinct registers for consecutive chunks —
+              // measured 3 % slower: more spills)
 #pragma unroll 1
               for (int k = k_lo; k < k_hi; ++k) {
                 uint32_t v[32];
@@ -990,9 +1002,12 @@ using namespace fhe;
 
 extern "C" {
 
+static unsigned long long* g_trace_host = nullptr;  // host copy of the trace pointer (launch metadata)
+
 int fhe_debug_trace(void* dev_buf) {
   unsigned long long* p = (unsigned long long*)dev_buf;
   FHE_CUDA(cudaMemcpyToSymbol(tc::g_trace, &p, sizeof(p)));
+  g_trace_host = p;
   return FHE_OK;
 }
 
@@ -1101,7 +1116,10 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.fstride = s.fstride;
     d.c_o = s.c_o;
     d.OB = (s.c_o + tc::kOcTile - 1) / tc::kOcTile;
-    d.taps = s.taps * rep;  // MMAs per stage: every tap for every stacked position group
+    d.taps = s.taps * rep;  // MMAs per 32-channel block: every tap for every stacked position group
+    d.tsplit = s.tsplit < 1 ? 1 : s.tsplit;  // the block's MMAs over this many stages (tap groups)
+    if (d.taps % d.tsplit) return fail(FHE_ERR_VALUE, "tc layer %d: taps x rep not divisible by tsplit", l);
+    d.tg = d.taps / d.tsplit;
     d.rep = rep;
     d.h = s.h;
     d.npos = std::min(s.pos_tile, 32);  // positions per MMA (N = 8 npos <= 256)
@@ -1116,7 +1134,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
       for (int r = 0; r < rep; ++r) d.tap_off[r * s.taps + t] = (int16_t)(off + r * d.npos);  // group r: +32 r
     }
     d.win_bytes = ((d.tpos + 2 * d.h) * 256 + 1023) / 1024 * 1024;
-    d.stage_bytes = d.win_bytes + d.taps * tc::kWTap;
+    d.stage_bytes = d.win_bytes + d.tg * tc::kWTap;
     d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
     if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
     // Keep the previous layer's ring partition when this layer's stages fit its
@@ -1185,6 +1203,12 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   attr_coop.val.cooperative = 1;
   cfg.attrs = &attr_coop;
   cfg.numAttrs = 1;
+  if (g_trace_host) {  // trace mode: the launch's tile dealing offsets for tools/trace_stack.py
+    static thread_local unsigned long long toffs[tc::kMaxLayers];
+    for (int l = 0; l < nl; ++l) toffs[l] = (unsigned long long)A.L[l].toff;
+    FHE_CUDA(cudaMemcpyAsync(g_trace_host + 7 * 4096 + 2048, toffs, sizeof(unsigned long long) * nl,
+                             cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  }
   FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel, A));
   FHE_CHECK_LAUNCH("conv_tc_stack_kernel");
   return FHE_OK;

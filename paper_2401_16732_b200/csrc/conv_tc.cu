@@ -110,8 +110,12 @@ struct LayerDesc {
 constexpr int kRdy = 3 + kMaxLayers;      // sync index of layer 0's relayout-done counter
 constexpr int kGem = 3 + 2 * kMaxLayers;  // sync index of layer 0's GEMM-done counter
 
-struct StackArgs {
-  LayerDesc L[kMaxLayers];
+// ML = layers the parameter block holds: kMaxLayers for stacks, 1 for the
+// one-layer launches of the drop-in path (an 8 KB parameter block copied at
+// every launch would cost that path microseconds of launch overhead)
+template <int ML>
+struct StackArgsT {
+  LayerDesc L[ML];
   unsigned long long* sync;  // 3 + 3 * kMaxLayers counters (see the protocol note below)
   uint64_t q, w32p;          // modulus; Shoup companion of 2^32 (q > 2^56)
   int n, nl;
@@ -119,6 +123,7 @@ struct StackArgs {
                              // plane recombination into shift / sign / carry sequences (one IMAD.WIDE each)
   int xrot;                  // 1: three X buffers rotate (layer l reuses l-3's); 0: every layer has its own
 };
+using StackArgs = StackArgsT<kMaxLayers>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -494,7 +499,8 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 #else
 #define FHE_STACK_BOUNDS __launch_bounds__(kThreads, 1)
 #endif
-__global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ StackArgs A) {
+template <int ML>
+__global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ StackArgsT<ML> A) {
   extern __shared__ __align__(1024) uint8_t smem[];
   unsigned long long* const trc = g_trace;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1188,7 +1194,10 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   ring = std::max(ring, tc::kEpiWarps * tc::kStg);  // the epilogue warps' layer-0 staging lives in the ring
   const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 4 * tc::kSlotWords;
   if (!attr_of[dev].load(std::memory_order_acquire)) {  // idempotent: a racing second set is harmless
-    FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel<tc::kMaxLayers>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
     attr_of[dev].store(true, std::memory_order_release);
   }
   // persistent and cooperative: every CTA must be resident for the grid barriers
@@ -1209,7 +1218,23 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     FHE_CUDA(cudaMemcpyAsync(g_trace_host + 7 * 4096 + 2048, toffs, sizeof(unsigned long long) * nl,
                              cudaMemcpyHostToDevice, (cudaStream_t)stream));
   }
-  FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel, A));
+  if (nl == 1) {
+    static thread_local tc::StackArgsT<1> A1;
+    A1.L[0] = A.L[0];
+    A1.sync = A.sync;
+    A1.q = A.q;
+    A1.w32p = A.w32p;
+    A1.n = A.n;
+    A1.nl = 1;
+    A1.k1 = A.k1;
+    A1.k8 = A.k8;
+    A1.k16 = A.k16;
+    A1.k24 = A.k24;
+    A1.xrot = A.xrot;
+    FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel<1>, A1));
+  } else {
+    FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel<tc::kMaxLayers>, A));
+  }
   FHE_CHECK_LAUNCH("conv_tc_stack_kernel");
   return FHE_OK;
 }

@@ -239,11 +239,13 @@ typedef struct fhe_conv_tc_layer {
  *   x_stride == 0: every layer owns a region, consecutive and 256-byte
  *   aligned (sum of ceil256(2*frags*ceil(c_i/32)*(n+2h)*256) bytes), and the
  *   relayout of later layers never waits for earlier GEMMs.
- * sync: DEVICE uint64[3 + 3*24], zeroed once before first use: the launch
- *   counter and, per layer, work / relayout-done / GEMM-done counters. They
- *   only grow (graph-replay safe); reuse one sync buffer only for stacks with
- *   the same number of layers and never for launches that may run
- *   concurrently. */
+ * sync: DEVICE uint64[3 + 4*24], zeroed once before first use: the launch
+ *   counter and, per layer, work / relayout-done / GEMM-done / tile counters
+ *   (CTAs grab tiles dynamically, the last grab of a launch resets the
+ *   layer's tile counter; FHE_TC_DYNAMIC=0 deals them statically). The other
+ *   counters only grow (graph-replay safe); reuse one sync buffer only for
+ *   stacks with the same number of layers and never for launches that may
+ *   run concurrently. */
 int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl,
                       uint8_t* X, size_t x_stride, uint64_t* sync, void* stream);
 /* conv.avg_pool (conv.py:604-623): every row (polynomial) of in [rows][n]

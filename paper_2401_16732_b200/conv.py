@@ -446,7 +446,7 @@ class ConvTcPlan:
         return out
 
 
-SYNC_WORDS = 3 + 3 * 24  # fhe_conv_tc_stack: launch counter + per-layer work / relayout-done / GEMM-done counters
+SYNC_WORDS = 3 + 4 * 24  # fhe_conv_tc_stack: launch counter + per-layer work / relayout-done / GEMM-done / tile counters
 MAX_STACK = 24
 _stack_sync: dict[tuple, torch.Tensor] = {}
 

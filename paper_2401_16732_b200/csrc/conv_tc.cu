@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -50,12 +51,26 @@ namespace tc {
 #define FHE_EPI_WARPS 8
 #endif
 constexpr int kEpiWarps = FHE_EPI_WARPS;  // two (or four) per TMEM lane quadrant
-#ifndef FHE_REL_WARPS
-#define FHE_REL_WARPS 4
+#ifndef FHE_REL_SKIP0
+#define FHE_REL_SKIP0 0  // 1 measured ~1 % slower on config 5 (one relayout warp fewer per other sub-partition)
 #endif
-constexpr int kRelWarps = FHE_REL_WARPS;  // dedicated relayout warps (run ahead of the GEMM); 4 measured
-                                           // best of 2..10 (fewer warps leave more registers per thread)
+#ifndef FHE_REL_WARPS
+#define FHE_REL_WARPS (4 + FHE_REL_SKIP0)
+#endif
+constexpr int kRelWarps = FHE_REL_WARPS;  // dedicated relayout warps (run ahead of the GEMM)
 constexpr int kWarps = 2 + kEpiWarps + kRelWarps;
+// The MMA issuer (warp 0) shares sub-partition 0 with warps 4k. Integer-heavy
+// warps there delay its per-MMA descriptor moves enough to starve the tensor
+// pipe (tools/mma_contention.cu; config-5 stem MMAs ran at ~2.3x their issue
+// time with every quadrant's epilogue busy). With FHE_REL_SKIP0 the relayout
+// warps on sub-partition 0 help with layer 0 only; the others stream the rest.
+__host__ __device__ constexpr bool rel_late(int w) { return !(FHE_REL_SKIP0 && (w & 3) == 0); }
+__host__ __device__ constexpr int rel_late_rank(int w) {  // rank of relayout warp w among the late ones
+  int r = 0;
+  for (int v = 2 + kEpiWarps; v < w; ++v) r += rel_late(v) ? 1 : 0;
+  return r;
+}
+constexpr int kRelLate = rel_late_rank(kWarps);  // relayout warps of layers 1..
 constexpr int kThreads = 32 * kWarps;
 constexpr int kMaxTaps = 64;
 constexpr int kMaxStages = 6;
@@ -83,6 +98,12 @@ constexpr int kPfAhead = FHE_PF_AHEAD;
 #ifndef FHE_XFENCE
 #define FHE_XFENCE 1  // relayout writers order their X stores into the async proxy (0: A/B probe only)
 #endif  // relayout inputs are prefetched into L2 this many layers ahead
+#ifndef FHE_EPI_PIPE
+#define FHE_EPI_PIPE 0  // 1: software-pipelined TMEM loads in the pair epilogue (measured 2.5 % slower on config 5)
+#endif
+#ifndef FHE_EPI_SLEEP
+#define FHE_EPI_SLEEP 0
+#endif
 #ifndef FHE_EPI_PAIR
 #define FHE_EPI_PAIR 0  // 1: two TMEM chunk loads per tcgen05.wait::ld (measured 3 % slower on configs 4 and 5)
 #endif
@@ -102,13 +123,19 @@ struct LayerDesc {
   int nacc;  // accumulators per tile: 1, or 2 (a 64-position tile: weights reused by both, TMEM single-buffered)
   int tpos;  // positions per tile = npos * nacc, or npos * rep
   int slot_bytes, nslots;  // ring partition this layer runs in: nslots slots of slot_bytes >= stage_bytes
+  int res_bytes;           // > 0: the layer's weights (one output block) stay resident at the ring base and
+                           // a stage is just the window (slots follow the weights); loaded once per CTA
   int tsplit, tg;          // tap groups per 32-channel block (stages per block) and taps per group
   int rep;   // 32-position groups stacked in the 128 accumulator rows (c_o <= 128 / rep): 1, 2 or 4
+  int pair;  // 1: plane sums are below 2^31 / 257 (short contraction): the epilogue pairs planes in 32 bits
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
 
 constexpr int kRdy = 3 + kMaxLayers;      // sync index of layer 0's relayout-done counter
 constexpr int kGem = 3 + 2 * kMaxLayers;  // sync index of layer 0's GEMM-done counter
+constexpr int kTile = 3 + 3 * kMaxLayers; // sync index of layer 0's tile counter (dynamic tile scheduling)
+constexpr int kSyncWords = 3 + 4 * kMaxLayers;
+constexpr int kTq = 32;                   // tile-sequence ring entries (loader -> MMA issuer, epilogue)
 
 // ML = layers the parameter block holds: kMaxLayers for stacks, 1 for the
 // one-layer launches of the drop-in path (an 8 KB parameter block copied at
@@ -122,6 +149,13 @@ struct StackArgsT {
   int k1, k8, k16, k24;      // 1, 2^8, 2^16, 2^24 as launch values: ptxas cannot strength-reduce the epilogue's
                              // plane recombination into shift / sign / carry sequences (one IMAD.WIDE each)
   int xrot;                  // 1: three X buffers rotate (layer l reuses l-3's); 0: every layer has its own
+  int dyn;                   // 1: CTAs grab tiles from per-layer counters (dynamic); 0: static round-robin
+  // pseudo-Mersenne epilogue (pm = 1 when q = 2^60 - delta with delta < 2^35, the reference's
+  // default modulus): 2^60 = delta (mod q) folds the 2^32-shifted half in two multiply-adds
+  // instead of a 64x64 Shoup product (see finish_pm)
+  int pm;
+  uint32_t pm_dlo, pm_dhi;   // delta = pm_dhi * 2^32 + pm_dlo
+  uint64_t pm_ca;            // = -2^88 (mod q), >= 2^56: the low half's offset (the high half's is 2^56)
 };
 using StackArgs = StackArgsT<kMaxLayers>;
 
@@ -258,6 +292,19 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])  \
       : "r"(taddr))
 
+// tcgen05.wait::ld that also "rewrites" the 32 destination registers of the
+// outstanding load: arithmetic on them cannot be scheduled above the wait
+// (the software-pipelined epilogue computes on one chunk while the next loads)
+#define TMEM_WAIT32(v)                                                                                            \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                                   \
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),  \
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),         \
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),       \
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),       \
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])                                                            \
+               :                                                                                                  \
+               : "memory")
+
 // Optional timeline instrumentation (fhe_debug_trace): CTA 0 records
 // clock64() at pipeline events, [kind][index] with 4096 slots per kind.
 __device__ unsigned long long* g_trace = nullptr;
@@ -303,6 +350,46 @@ __device__ __forceinline__ long long mad_wide(int32_t a, int32_t b, long long c)
   long long d;
   asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
   return d;
+}
+
+// V = Σ_d 2^(8d) P_d mod q for q = 2^60 - delta, delta < 2^35 (|P_d| < 2^31):
+//   A = ca + Σ_{d<4} 2^(8d) P_d   in (2^54, 2^60.2)     (ca in [2^56, 2^56 + q), ca = -2^88 mod q)
+//   B = 2^56 + Σ_{d>=4} 2^(8(d-4)) P_d in (2^55, 2^56.6)
+//   A + 2^32 B = V + ca + 2^88 = V (mod q);  B = bh 2^28 + bl, 2^60 = delta:
+//   W = A + bl 2^32 + delta bh      < 2^60.2 + 2^60 + 2^63.6 < 2^64
+//   W = wh 2^60 + wl:  U = wl + delta wh < 2^60 + 2^39 < 2q;  r = U mod q (one subtraction)
+// 30 integer instructions per coefficient instead of ~50 (Shoup on the high half).
+// (A, B) -> A + 2^32 B mod q, the pseudo-Mersenne folds
+__device__ __forceinline__ uint64_t reduce_pm(long long a, long long b, uint32_t dlo, uint32_t dhi, uint64_t q) {
+  const uint32_t blo = (uint32_t)b, bhi = (uint32_t)((unsigned long long)b >> 32);
+  const uint32_t bh = __funnelshift_r(blo, bhi, 28), bl = blo & 0x0FFFFFFFu;
+  uint64_t w = (uint64_t)bh * dlo + (uint64_t)a;  // IMAD.WIDE.U32 with a 64-bit addend
+  uint32_t wlo = (uint32_t)w, whi = (uint32_t)(w >> 32) + (bh * dhi + bl);
+  const uint32_t wh = whi >> 28;
+  whi &= 0x0FFFFFFFu;
+  uint64_t u = (uint64_t)wh * dlo + (((uint64_t)whi << 32) | wlo);
+  u += (uint64_t)(wh * dhi) << 32;
+  return u >= q ? u - q : u;
+}
+
+__device__ __forceinline__ uint64_t finish_pm(const int32_t* P, int k1, int k8, int k16, int k24, uint64_t ca,
+                                              uint32_t dlo, uint32_t dhi, uint64_t q) {
+  const long long a = mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, mad_wide(P[0], k1, (long long)ca))));
+  const long long b =
+      mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, mad_wide(P[4], k1, 1ll << 56))));
+  return reduce_pm(a, b, dlo, dhi, q);
+}
+
+// Short contractions (LayerDesc.pair: 127·255·257·K < 2^31 for the K = c_i·taps
+// products summed into one accumulator row — the stems and the 1x1 projections):
+// byte-plane pairs P_2i + 2^8 P_2i+1 are exact in 32 bits, so each half is two
+// 32-bit multiply-adds and two wide ones instead of four wide ones and their adds.
+__device__ __forceinline__ uint64_t finish_pm_pair(const int32_t* P, int k1, int k8, int k16, uint64_t ca,
+                                                   uint32_t dlo, uint32_t dhi, uint64_t q) {
+  const int32_t q0 = P[1] * k8 + P[0], q1 = P[3] * k8 + P[2], q2 = P[5] * k8 + P[4], q3 = P[7] * k8 + P[6];
+  const long long a = mad_wide(q1, k16, mad_wide(q0, k1, (long long)ca));
+  const long long b = mad_wide(q3, k16, mad_wide(q2, k1, 1ll << 56));
+  return reduce_pm(a, b, dlo, dhi, q);
 }
 
 __device__ __forceinline__ void transpose4x4(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t& p0,
@@ -494,6 +581,30 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Tile-sequence ring: the loader decides which tile this CTA runs next (a
+// static round-robin share or a dynamic grab) and publishes entry sq =
+// {tag = sq + 1, layer << 24 | tile} with one release store; the MMA issuer
+// and the epilogue warps read the same sequence (acquire loads). A sentinel
+// entry with layer = nl ends it. The ring cannot overflow: the loader writes
+// entry sq only after a stage slot freed by the MMAs of tile >= sq - 6 - 1, and
+// the MMA issuer starts tile i only after the epilogue released tile i - 2.
+__device__ __forceinline__ void tq_put(uint64_t* tq, int sq, int l, int t) {
+  const uint64_t v = ((uint64_t)(((uint32_t)l << 24) | (uint32_t)t) << 32) | (uint32_t)(sq + 1);
+  asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(tq + (sq % kTq))), "l"(v) : "memory");
+}
+__device__ __forceinline__ bool tq_peek(const uint64_t* tq, int sq, uint32_t& lt) {
+  uint64_t v;
+  asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(smem_u32(tq + (sq % kTq))) : "memory");
+  lt = (uint32_t)(v >> 32);
+  return (uint32_t)v == (uint32_t)(sq + 1);
+}
+__device__ __forceinline__ uint32_t tq_get(const uint64_t* tq, int sq) {
+  uint32_t lt;
+  for (uint32_t i = 0; !tq_peek(tq, sq, lt); ++i)
+    if (i > (1u << 28)) __trap();
+  return lt;
+}
+
 #if defined(FHE_STACK_MAXNREG)  // probe builds: a register cap instead of launch bounds
 #define FHE_STACK_BOUNDS __maxnreg__(FHE_STACK_MAXNREG)
 #else
@@ -507,7 +618,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   const int n = A.n, nl = A.nl, G = gridDim.x;
   const uint64_t q = A.q;
   int ring_bytes = kEpiWarps * kStg;  // (same rule as the host's smem sizing)
-  for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].nslots * A.L[l].slot_bytes);
+  for (int l = 0; l < nl; ++l) ring_bytes = max(ring_bytes, A.L[l].res_bytes + A.L[l].nslots * A.L[l].slot_bytes);
   // relayout staging: the relayout warps own areas after the ring; the epilogue
   // warps (layer 0 only, before any stage is loaded) borrow the ring
   uint8_t* stg = warp >= 2 + kEpiWarps ? smem + ring_bytes + (warp - 2 - kEpiWarps) * kStg
@@ -515,6 +626,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes + kRelWarps * kStg);
   // [0,6) full, [6,12) empty, 12+{0,1} tmem_full, 12+{2,3} tmem_empty
   uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 4);
+  uint64_t* const tq = reinterpret_cast<uint64_t*>(slot + kSlotWords);  // [kTq] tile sequence
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
   auto empty_bar = [&](int s) { return bar0 + 8 * (kMaxStages + s); };
@@ -524,6 +636,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   if (tid == 0) slot[1] = (unsigned)(atomicAdd(A.sync, 1ull) / (unsigned long long)G);  // epoch - 1
   unsigned* const cta_done = reinterpret_cast<unsigned*>(slot + 4);  // [kMaxLayers] warps of this CTA done
   if (tid < kMaxLayers) cta_done[tid] = 0;
+  if (tid < kTq) tq[tid] = 0;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
                  "n"(2 * kAccCols));
@@ -544,7 +657,11 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = slot[0];
+  // one CTA per SM allocates all 512 columns: the allocation starts at lane 0,
+  // column 0. Using the constant (checked) keeps the MMA issuer's accumulator
+  // addresses in uniform registers (no vector-to-uniform moves per MMA).
+  if (slot[0] != 0) __trap();
+  constexpr uint32_t tmem = 0;
   auto gtime = [] {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -583,7 +700,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     // a time. No shared work counter: ~1.7k atomics per layer on one address
     // serialised the early (small, latency-bound) layers; 2 % faster stack.
     {
-      const int wi = participants == P0 ? warp - 2 : warp - (2 + kEpiWarps);
+      const int wi = participants == P0 ? warp - 2 : rel_late_rank(warp);
       const int R = G * participants;
       for (int u = wi * G + (int)blockIdx.x; u < d.units; u += 2 * R) {
         UnitLoad U0, U1;
@@ -646,22 +763,28 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     // weights: half the weight traffic per position). Per-buffer use counts
     // give the tmem_full / tmem_empty parities on both sides.
     {  // the whole warp runs the issue loop; elect.sync issues (see mma_i8w_elect)
-      int s_mma = 0, prev_sb = -1, prev_ns = -1, tl = 0, nb = 0;
+      int s_mma = 0, prev_sb = -1, prev_ns = -1, prev_res = 0, tl = 0, nb = 0;
       uint32_t par = 0, use = 0;  // per-stage full parity; per-buffer use parity (bit b)
       const uint64_t desc0 = umma_desc(smem_u32(smem));  // ring base; stage s adds s * stage_bytes / 16
       const uint32_t dlo0 = (uint32_t)desc0, dhi = (uint32_t)(desc0 >> 32);
       bool pre = false;  // the current stage's full barrier was already waited for
+      uint32_t lt = tq_get(tq, 0);  // the loader's tile sequence (layers in increasing order)
       for (int l = 0; l < nl; ++l) {
+        if ((int)(lt >> 24) != l) continue;  // no tiles of this layer here
         const LayerDesc& d = A.L[l];
-        // Per-layer values in registers: the barrier asm below clobbers memory,
-        // so fields read through `d` inside the loops would be re-fetched from
-        // the parameter bank (dependent LDCs) at every stage.
-        const int tiles = d.tiles, t0 = first_tile(d);
-        if (tiles <= t0) continue;  // no tiles of this layer here (the loader skips it too)
+        // Per-layer values in registers, scoped to the layer: the barrier asm below
+        // clobbers memory, so fields read through `d` inside the loops would be
+        // re-fetched from the parameter bank (dependent LDCs) at every stage, and
+        // loop-carried copies leave the issue path vector-to-uniform moves per MMA.
         const int slot_bytes = d.slot_bytes, JB = d.JB, nacc = d.nacc, taps = d.taps, nst = d.nslots;
-        if (slot_bytes != prev_sb || nst != prev_ns) s_mma = 0;  // the loader drained and re-partitioned the ring
+        const int res = d.res_bytes;
+        // the loader drained and re-partitioned the ring (resident weights: always)
+        if (slot_bytes != prev_sb || nst != prev_ns || res || prev_res) s_mma = 0;
         prev_sb = slot_bytes;
         prev_ns = nst;
+        prev_res = res;
+        const uint32_t rlo = dlo0 + (uint32_t)(res >> 4);  // first slot (after any resident weights)
+        const uint32_t wtap = (uint32_t)(taps * (kWTap >> 4));  // resident weights: one 32-channel block
         const uint32_t idesc = idesc_i8(8 * d.npos);
         const uint32_t sstep = (uint32_t)(slot_bytes >> 4), wdesc = (uint32_t)(d.win_bytes >> 4);
         const uint32_t adelta = (uint32_t)(d.npos * 256 >> 4);  // second accumulator's positions
@@ -669,14 +792,13 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
 #pragma unroll
         for (int tp = 0; tp < 16; ++tp) off16[tp] = tp < taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
         const int TS = d.tsplit, tg = d.tg, nstage = JB * TS;
-        for (int t = t0; t < tiles; t += G, ++tl) {
+        for (;; ++tl) {  // this CTA's tiles of layer l, in the loader's order
           int b0 = 0, b1 = 1;
           if (nacc == 1) {
             b0 = nb;
             nb ^= 1;
           }
           if (lane == 0) TC_TRACE(0, tl);
-          const bool more_tiles = t + G < tiles;
           for (int st = 0; st < nstage; ++st) {  // stage = (32-channel block, tap group)
             const int jb = st;                   // (the fast paths run with one tap group: st == jb)
             const int s = s_mma;
@@ -687,9 +809,16 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             }
             pre = false;
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint32_t blo0 = dlo0 + (uint32_t)s * sstep;  // window at the stage base
-            const uint32_t alo = blo0 + wdesc;                  // weights after the window
-            const bool has_next = st + 1 < nstage || more_tiles;  // next stage of this layer on this CTA
+            const uint32_t blo0 = rlo + (uint32_t)s * sstep;  // window at the stage base
+            // weights after the window, or resident at the ring base
+            const uint32_t alo = res ? dlo0 + (uint32_t)jb * wtap : blo0 + wdesc;
+            // a next stage of this layer: within the tile, or the sequence's next tile
+            // when it is already published and of this layer
+            bool has_next = st + 1 < nstage;
+            if (!has_next) {
+              uint32_t nlt;
+              has_next = tq_peek(tq, tl + 1, nlt) && (int)(nlt >> 24) == l;
+            }
             for (int a = 0; a < nacc; ++a) {
               const int b = a == 0 ? b0 : b1;
               if (st == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
@@ -738,32 +867,69 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             use ^= 1u << b;
           }
           if (lane == 0) TC_TRACE(1, tl);
+          lt = tq_get(tq, tl + 1);
+          if ((int)(lt >> 24) != l) {
+            ++tl;
+            break;
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ stage loads
     if (lane == 0) {
-      int s_ld = 0, prev_sb = -1, prev_ns = -1;
+      int s_ld = 0, prev_sb = -1, prev_ns = -1, prev_res = 0, sq = 0;
       uint32_t par = 0, used = 0;  // per-stage fill parity; stages filled at least once
       for (int l = 0; l < nl; ++l) {
         const LayerDesc& d = A.L[l];
-        if (d.tiles <= first_tile(d)) continue;  // no tiles of this layer here
-        if (d.slot_bytes != prev_sb || d.nslots != prev_ns) {
-          // new ring partition: every stage of the old one must be consumed first
-          for (int s = 0; s < kMaxStages; ++s)
-            if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
-          s_ld = 0;
-          prev_sb = d.slot_bytes;
-          prev_ns = d.nslots;
-        }
+        const int tiles = d.tiles;
+        // this CTA's tiles of layer l: a static round-robin share, or grabbed from the
+        // layer's counter (one grab stays in flight ahead of the loads). Every CTA
+        // overshoots the counter exactly once, so the grab that returns tiles + G - 1
+        // is the launch's last one: that CTA resets the counter for the next launch
+        // (no epoch arithmetic: a counter buffer shared by different stacks stays valid).
+        unsigned long long* const ctr = A.sync + kTile + l;
+        int t_static = first_tile(d);
+        if (!A.dyn && tiles <= t_static) continue;  // no tiles of this layer here
         wait_count(A.sync + kRdy + l, ready_target(l));  // layer l's X is complete
         TC_TRACE(7, l);
         asm volatile("fence.proxy.async.global;");  // generic-proxy X stores -> cp.async.bulk reads
+        unsigned long long nxt = A.dyn ? atomicAdd(ctr, 1ull) : 0ull;
+        bool first = true, res_pending = false;
         const uint32_t wstage = (uint32_t)d.taps * kWTap;
         const size_t plane_stride = (size_t)d.Y * 256;
         const uint32_t win_load = (uint32_t)((d.tpos + 2 * d.h) * 256);
-        for (int t = first_tile(d); t < d.tiles; t += G) {
+        for (;;) {
+          int t;
+          if (A.dyn) {
+            if (nxt >= (unsigned long long)tiles) {
+              if (nxt == (unsigned long long)tiles + Gu - 1) atomicExch(ctr, 0ull);
+              break;
+            }
+            t = (int)nxt;
+            nxt = atomicAdd(ctr, 1ull);
+          } else {
+            if (t_static >= tiles) break;
+            t = t_static;
+            t_static += G;
+          }
+          if (first) {
+            first = false;
+            if (d.slot_bytes != prev_sb || d.nslots != prev_ns || d.res_bytes || prev_res) {
+              // new ring partition (or new resident weights): every stage of the old one must be
+              // consumed first (MMAs complete in order: the last stage's release also frees the
+              // previous layer's resident weights)
+              for (int s = 0; s < kMaxStages; ++s)
+                if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
+              s_ld = 0;
+              prev_sb = d.slot_bytes;
+              prev_ns = d.nslots;
+              prev_res = d.res_bytes;
+            }
+            res_pending = d.res_bytes > 0;  // the resident weights ride on the layer's first stage
+          }
+          if (trc && blockIdx.x == 0 && sq < 1024) trc[7 * 4096 + 1024 + sq] = l;  // the sequence's layers (trace)
+          tq_put(tq, sq++, l, t);
           const Tile T = tile_of(t, d, n);
           const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
           const uint8_t* wbase = d.W + (size_t)T.ob * d.JB * wstage;
@@ -773,7 +939,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
             used |= 1u << s;
             par ^= 1u << s;
-            const uint32_t pos = (uint32_t)(s * d.slot_bytes);
+            const uint32_t pos = (uint32_t)(d.res_bytes + s * d.slot_bytes);
             const uint32_t sx = smem_u32(smem + pos);
 #ifdef TC_PROBE_NOFILL  // timing probe only: MMAs on stale stage data, no fill traffic
             (void)sx;
@@ -781,21 +947,36 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             (void)wbase;
             mbar_arrive(full_bar(s));
 #else
-            const uint32_t wgroup = (uint32_t)d.tg * kWTap;  // this stage's tap group of weights
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
-                         "r"(win_load + wgroup)
-                         : "memory");
-            FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nslots * d.slot_bytes) &&
-                      d.stage_bytes <= d.slot_bytes &&
-                      win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
-                      wbase + (size_t)jb * wstage + (size_t)(g + 1) * wgroup <= d.W + d.w_bytes);
-            bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
-            bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage + (size_t)g * wgroup, wgroup, full_bar(s));
+            if (d.res_bytes) {  // window only; the first stage also brings the resident weights
+              const uint32_t extra = res_pending ? (uint32_t)d.res_bytes : 0u;
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
+                           "r"(win_load + extra)
+                           : "memory");
+              FHE_CHECK(pos + (uint32_t)d.slot_bytes <= (uint32_t)(d.res_bytes + d.nslots * d.slot_bytes) &&
+                        win_load <= (uint32_t)d.slot_bytes && d.OB == 1 &&
+                        xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
+                        (size_t)d.res_bytes <= d.w_bytes);
+              bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+              if (res_pending) bulk_load(smem_u32(smem), d.W, (uint32_t)d.res_bytes, full_bar(s));
+              res_pending = false;
+            } else {
+              const uint32_t wgroup = (uint32_t)d.tg * kWTap;  // this stage's tap group of weights
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
+                           "r"(win_load + wgroup)
+                           : "memory");
+              FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nslots * d.slot_bytes) &&
+                        d.stage_bytes <= d.slot_bytes &&
+                        win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
+                        wbase + (size_t)jb * wstage + (size_t)(g + 1) * wgroup <= d.W + d.w_bytes);
+              bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+              bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage + (size_t)g * wgroup, wgroup, full_bar(s));
+            }
 #endif
             s_ld = s + 1 == d.nslots ? 0 : s + 1;
           }
         }
       }
+      tq_put(tq, sq, nl, 0);  // end of this CTA's sequence
     }
   } else if (warp >= 2 + kEpiWarps) {
     // ------------------------------------------------------- relayout warps
@@ -806,37 +987,43 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
       prefetch_l2(A.L[0].W, A.L[0].w_bytes);
     }
     relayout_layer(0, P0);
-    for (int l = 1; l < nl; ++l) {
+    for (int l = 1; l < nl && rel_late(warp); ++l) {
       if (pf) {  // the input kPfAhead layers on, and this layer's weights
         if (l + kPfAhead < nl) prefetch_l2(A.L[l + kPfAhead].in, A.L[l + kPfAhead].in_bytes);
         prefetch_l2(A.L[l].W, A.L[l].w_bytes);
       }
       if (A.xrot && l >= 3) wait_count(A.sync + kGem + l - 3, gemm_target(l - 3));  // X[l % 3] no longer read anywhere
       if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(2, 64 + l);  // this warp starts layer l's relayout
-      relayout_layer(l, kRelWarps);
+      relayout_layer(l, kRelLate);
       if (lane == 0 && warp == 2 + kEpiWarps) TC_TRACE(3, l);
     }
   } else {
     // -------------------------------------------------------------- epilogue
     const int quad = warp & 3, sub = (warp - 2) >> 2;
     const int k1 = A.k1, k8 = A.k8, k16 = A.k16, k24 = A.k24;
+    const int pm = A.pm;
+    const uint64_t pm_ca = A.pm_ca;
+    const uint32_t pm_dlo = A.pm_dlo, pm_dhi = A.pm_dhi;
     relayout_layer(0, P0);  // nothing to do yet but help with layer 0
-    int tl = 0, nb = 0;
+    int nb = 0, tl = 0;
     uint32_t use = 0;  // per-buffer use parity (mirrors the MMA thread)
+    uint32_t lt = tq_get(tq, 0);  // the loader's tile sequence (layers in increasing order)
     for (int l = 0; l < nl; ++l) {
-      const LayerDesc& d = A.L[l];
-      // per-layer values in registers (the store asm below clobbers memory:
-      // fields read through `d` in the chunk loop were re-fetched from the
-      // parameter bank every chunk)
-      const int c_o = d.c_o, F = d.F, npos = d.npos, nacc = d.nacc;
-      // rows of the accumulator: rep groups of rows_per output channels, group
-      // r holding positions [32 r, 32 r + 32) of the tile
-      const int rows_per = kOcTile / d.rep;
-      const int grp = (quad * 32 + lane) / rows_per, orow = (quad * 32 + lane) % rows_per;
-      uint64_t* const dout = d.out;
-      const uint8_t* const bmask = d.bmask;
-      const uint64_t* const bias = d.bias;
-      for (int t = first_tile(d); t < d.tiles; t += G, ++tl) {
+      if ((int)(lt >> 24) == l) {
+        const LayerDesc& d = A.L[l];
+        // per-layer values in registers (the store asm below clobbers memory:
+        // fields read through `d` in the chunk loop were re-fetched from the
+        // parameter bank every chunk)
+        const int c_o = d.c_o, F = d.F, npos = d.npos, nacc = d.nacc, pair = d.pair;
+        // rows of the accumulator: rep groups of rows_per output channels, group
+        // r holding positions [32 r, 32 r + 32) of the tile
+        const int rows_per = kOcTile / d.rep;
+        const int grp = (quad * 32 + lane) / rows_per, orow = (quad * 32 + lane) % rows_per;
+        uint64_t* const dout = d.out;
+        const uint8_t* const bmask = d.bmask;
+        const uint64_t* const bias = d.bias;
+        for (;; ++tl) {  // this CTA's tiles of layer l, in the loader's order
+        const int t = (int)(lt & 0xFFFFFFu);
         const Tile T = tile_of(t, d, n);
         const int o = T.ob * kOcTile + orow;
         const bool active = T.ob * kOcTile + (quad * 32) % rows_per < c_o;  // warp-uniform (rows_per >= 32)
@@ -850,9 +1037,17 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             buf = a;
           }
           const int s0 = T.s0 + (a + grp) * npos;
+#if FHE_EPI_SLEEP
           mbar_wait_sleep(tfull_bar(buf), (use >> buf) & 1, 64);
+#else
+          // no nanosleep: a sleeping warp woke up to ~1k cycles after its accumulator was
+          // ready, and the slowest epilogue warp sets the tile period (try_wait suspends
+          // the warp in hardware between polls)
+          mbar_wait(tfull_bar(buf), (use >> buf) & 1);
+#endif
           use ^= 1u << buf;
           if (lane == 0 && warp == 2) TC_TRACE(5, tl);
+          if (lane == 0) TC_TRACE(9 + warp - 2, tl);  // every epilogue warp: tfull seen
           asm volatile("tcgen05.fence::after_thread_sync;");
 #ifdef TC_PROBE_NOEPI  // timing probe only: accumulators released unread
           if (false) {
@@ -872,18 +1067,24 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             const int k_lo = sub * (npos / 4) / kEpq, k_hi = (sub + 1) * (npos / 4) / kEpq;
             const int kper = k_hi - k_lo;
             // recombine the 4 positions of one 32-column chunk and store them
-            auto finish = [&](const uint32_t* v, int k) {
+            auto finish = [&](const uint32_t* v, int k, auto pm_tag) {
               uint64_t r[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const int32_t* P = reinterpret_cast<const int32_t*>(v + 8 * j);
-                const long long lo = mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, mad_wide(P[0], k1, q))));
-                const long long hi = mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, mad_wide(P[4], k1, q))));
-                // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
-                const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(A.w32p, (uint64_t)hi) * q;
-                uint64_t val = (uint64_t)lo + uh;  // < 4q
-                val = val >= 2 * q ? val - 2 * q : val;
-                r[j] = val >= q ? val - q : val;
+                if constexpr (decltype(pm_tag)::value == 2) {
+                  r[j] = finish_pm_pair(P, k1, k8, k16, pm_ca, pm_dlo, pm_dhi, q);
+                } else if constexpr (decltype(pm_tag)::value == 1) {
+                  r[j] = finish_pm(P, k1, k8, k16, k24, pm_ca, pm_dlo, pm_dhi, q);
+                } else {
+                  const long long lo = mad_wide(P[3], k24, mad_wide(P[2], k16, mad_wide(P[1], k8, mad_wide(P[0], k1, q))));
+                  const long long hi = mad_wide(P[7], k24, mad_wide(P[6], k16, mad_wide(P[5], k8, mad_wide(P[4], k1, q))));
+                  // 2^32 hi mod q by Shoup (w = 2^32 < q): result in [0, 2q)
+                  const uint64_t uh = ((uint64_t)hi << 32) - __umul64hi(A.w32p, (uint64_t)hi) * q;
+                  uint64_t val = (uint64_t)lo + uh;  // < 4q
+                  val = val >= 2 * q ? val - 2 * q : val;
+                  r[j] = val >= q ? val - q : val;
+                }
               }
               if (bd) {
                 const uint32_t mk = *reinterpret_cast<const uint32_t*>(bmask + (size_t)T.f * n + s0 + 4 * k);
@@ -902,33 +1103,84 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                              : "memory");
 #endif
             };
-            if (FHE_EPI_PAIR && kper % 2 == 0) {
-              // two chunks per TMEM round trip: both loads in flight before the
-              // one wait (tcgen05.wait::ld covers every outstanding load)
+            auto chunks = [&](auto pm_tag) {
+              if (FHE_EPI_PAIR && kper % 2 == 0) {
+                // two chunks per TMEM round trip: both loads in flight before the
+                // one wait (tcgen05.wait::ld covers every outstanding load)
 #pragma unroll 1
-              for (int k = k_lo; k < k_hi; k += 2) {
-                uint32_t va[32], vb[32];
-                TMEM_LD32(acc + k * 32, va);
-                TMEM_LD32(acc + (k + 1) * 32, vb);
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-                finish(va, k);
-                finish(vb, k + 1);
-              }
-            } else {
-              // (unrolling by two — distinct registers for consecutive chunks —
-              // measured 3 % slower: more spills)
+                for (int k = k_lo; k < k_hi; k += 2) {
+                  uint32_t va[32], vb[32];
+                  TMEM_LD32(acc + k * 32, va);
+                  TMEM_LD32(acc + (k + 1) * 32, vb);
+                  asm volatile("tcgen05.wait::ld.sync.aligned;");
+                  finish(va, k, pm_tag);
+                  finish(vb, k + 1, pm_tag);
+                }
+              } else {
+#if FHE_EPI_PIPE && !defined(TC_PROBE_NOLD) && !defined(TC_PROBE_LDONLY) && !defined(TC_PROBE_Q0LD)
+                // software pipeline: chunk k+1's TMEM load is in flight while
+                // chunk k is recombined and stored (two register sets, no copies)
+                if (decltype(pm_tag)::value == 2 && k_lo < k_hi) {  // (the pair path: fewest temporaries)
+                  uint32_t va[32], vb[32];
+                  TMEM_LD32(acc + k_lo * 32, va);
+                  TMEM_WAIT32(va);
 #pragma unroll 1
-              for (int k = k_lo; k < k_hi; ++k) {
-                uint32_t v[32];
-                TMEM_LD32(acc + k * 32, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-                finish(v, k);
+                  for (int k = k_lo;; k += 2) {
+                    const bool m1 = k + 1 < k_hi;
+                    if (m1) TMEM_LD32(acc + (k + 1) * 32, vb);
+                    finish(va, k, pm_tag);
+                    if (!m1) break;
+                    TMEM_WAIT32(vb);
+                    const bool m2 = k + 2 < k_hi;
+                    if (m2) TMEM_LD32(acc + (k + 2) * 32, va);
+                    finish(vb, k + 1, pm_tag);
+                    if (!m2) break;
+                    TMEM_WAIT32(va);
+                  }
+                }
+                if (decltype(pm_tag)::value != 2)
+#endif
+#pragma unroll 1
+                for (int k = k_lo; k < k_hi; ++k) {
+                  uint32_t v[32];
+#if defined(TC_PROBE_NOLD)  // timing probe only: arithmetic and stores on register garbage, no TMEM loads
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) v[i] = (uint32_t)opaque(k * 32 + i);
+#else
+                  TMEM_LD32(acc + k * 32, v);
+                  asm volatile("tcgen05.wait::ld.sync.aligned;");
+#endif
+#if defined(TC_PROBE_LDONLY)  // timing probe only: TMEM loads, no arithmetic or stores
+                  if (v[0] == 0x5eed5eedu && v[31] == 0x1234567u) dout[0] = v[7];
+#elif defined(TC_PROBE_Q0LD)  // timing probe only: the MMA warp's sub-partition (quadrant 0) skips the arithmetic
+                  if (quad == 0) {
+                    if (v[0] == 0x5eed5eedu && v[31] == 0x1234567u) dout[0] = v[7];
+                  } else {
+                    finish(v, k, pm_tag);
+                  }
+#else
+                  finish(v, k, pm_tag);
+#endif
+                }
               }
-            }
+            };
+            if (pm && pair)
+              chunks(std::integral_constant<int, 2>{});
+            else if (pm)
+              chunks(std::integral_constant<int, 1>{});
+            else
+              chunks(std::integral_constant<int, 0>{});
           }
           asm volatile("tcgen05.fence::before_thread_sync;");
           mbar_arrive(tempty_bar(buf));
           if (lane == 0 && warp == 2) TC_TRACE(6, tl);
+          if (lane == 0) TC_TRACE(9 + kEpiWarps + warp - 2, tl);  // every epilogue warp: done
+        }
+        lt = tq_get(tq, tl + 1);
+        if ((int)(lt >> 24) != l) {
+          ++tl;
+          break;
+        }
         }
       }
       // this CTA consumed all of layer l's X (every tile's MMAs completed)
@@ -1044,6 +1296,33 @@ static bool balance_tiles() {
   return v == 1;
 }
 
+static bool pm_allowed() {  // FHE_TC_NO_PM=1: the general (Shoup) epilogue for every modulus (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_TC_NO_PM");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static bool resident_allowed() {  // FHE_TC_RESIDENT=0: weights streamed with every stage (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_TC_RESIDENT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static bool dynamic_tiles() {  // FHE_TC_DYNAMIC=0: static round-robin tile dealing (A/B checks)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FHE_TC_DYNAMIC");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool keep_partition() {  // FHE_TC_KEEP_RING=0: re-partition at every stage-size change (A/B checks)
   static int v = -1;
   if (v < 0) {
@@ -1066,10 +1345,21 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
   A.n = n;
   A.nl = nl;
   A.xrot = x_stride ? 1 : 0;
+  A.dyn = dynamic_tiles() ? 1 : 0;
   A.k1 = 1;
   A.k8 = 1 << 8;
   A.k16 = 1 << 16;
   A.k24 = 1 << 24;
+  {
+    const uint64_t delta = (1ull << 60) - q;  // pseudo-Mersenne fast path (finish_pm)
+    A.pm = (q < (1ull << 60) && delta < (1ull << 35) && pm_allowed()) ? 1 : 0;
+    A.pm_dlo = (uint32_t)delta;
+    A.pm_dhi = (uint32_t)(delta >> 32);
+    const unsigned __int128 t88 = (unsigned __int128)1 << 88;
+    uint64_t ca = (uint64_t)((q - (uint64_t)(t88 % q)) % q);  // -2^88 mod q
+    if (ca < (1ull << 56)) ca += q;
+    A.pm_ca = ca;
+  }
   size_t xoff = 0;
   A.sync = reinterpret_cast<unsigned long long*>(sync);
   int max_tiles = 0, ring = 0, toff = 0;
@@ -1127,6 +1417,8 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     if (d.taps % d.tsplit) return fail(FHE_ERR_VALUE, "tc layer %d: taps x rep not divisible by tsplit", l);
     d.tg = d.taps / d.tsplit;
     d.rep = rep;
+    // |P_d| <= 127·255·c_i·taps (each accumulator row sums one position group's taps)
+    d.pair = 127ll * 255 * 257 * s.c_i * s.taps < (1ll << 31) ? 1 : 0;
     d.h = s.h;
     d.npos = std::min(s.pos_tile, 32);  // positions per MMA (N = 8 npos <= 256)
     d.nacc = s.pos_tile / d.npos;       // 64-position tiles use both TMEM buffers
@@ -1146,7 +1438,18 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     // Keep the previous layer's ring partition when this layer's stages fit its
     // slots without losing depth: the loader then streams on without draining
     // the ring at the layer boundary (s3 -> s4 layers, same-shape layers).
-    if (l > 0 && d.stage_bytes <= A.L[l - 1].slot_bytes && A.L[l - 1].nslots >= d.nst && keep_partition()) {
+    // Resident weights: a layer with one output-channel block and no tap split
+    // reuses one weight slab (JB x taps x 4 KB) in every tile; when it fits
+    // beside >= 3 window slots it is loaded once per CTA and a stage is just the
+    // window (the 7x7 stem: 74 -> 18 KB per tile, 2 -> 6 stages in flight).
+    const int wres = d.JB * d.taps * tc::kWTap;
+    d.res_bytes = 0;
+    if (d.OB == 1 && d.tsplit == 1 && resident_allowed() && wres + 3 * d.win_bytes <= tc::kRingBudget) {
+      d.res_bytes = wres;
+      d.slot_bytes = d.win_bytes;
+      d.nslots = std::min(tc::kMaxStages, (tc::kRingBudget - wres) / d.win_bytes);
+    } else if (l > 0 && !A.L[l - 1].res_bytes && d.stage_bytes <= A.L[l - 1].slot_bytes &&
+               A.L[l - 1].nslots >= d.nst && keep_partition()) {
       d.slot_bytes = A.L[l - 1].slot_bytes;
       d.nslots = A.L[l - 1].nslots;
     } else {
@@ -1189,10 +1492,11 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
       d.toff = toff;
       toff = (toff + d.tiles) % sms_now;
     }
-    ring = std::max(ring, d.nslots * d.slot_bytes);
+    ring = std::max(ring, d.res_bytes + d.nslots * d.slot_bytes);
   }
   ring = std::max(ring, tc::kEpiWarps * tc::kStg);  // the epilogue warps' layer-0 staging lives in the ring
-  const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 4 * tc::kSlotWords;
+  const size_t smem = (size_t)ring + tc::kRelWarps * tc::kStg + 8 * (2 * tc::kMaxStages + 4) + 4 * tc::kSlotWords +
+                      8 * tc::kTq;
   if (!attr_of[dev].load(std::memory_order_acquire)) {  // idempotent: a racing second set is harmless
     FHE_CUDA(cudaFuncSetAttribute(tc::conv_tc_stack_kernel<tc::kMaxLayers>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1231,6 +1535,11 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     A1.k16 = A.k16;
     A1.k24 = A.k24;
     A1.xrot = A.xrot;
+    A1.dyn = A.dyn;
+    A1.pm = A.pm;
+    A1.pm_dlo = A.pm_dlo;
+    A1.pm_dhi = A.pm_dhi;
+    A1.pm_ca = A.pm_ca;
     FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel<1>, A1));
   } else {
     FHE_CUDA(cudaLaunchKernelEx(&cfg, tc::conv_tc_stack_kernel<tc::kMaxLayers>, A));

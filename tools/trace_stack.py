@@ -22,12 +22,18 @@ from paper_2401_16732_b200 import _native, conv  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="config4")
+    ap.add_argument("--only", default=None, help="trace this layer alone (a single-layer launch)")
+    ap.add_argument("--cta-dump", default=None, help="write per-CTA [start, end] globaltimer ns and the dealing offsets (.npz)")
+    ap.add_argument("--detail", default=None, help="per-epilogue-warp timing of this layer's tiles (CTA 0)")
     args = ap.parse_args()
     P, layers = bench.build_stack(args.workload)
+    if args.only:  # one layer alone: the drop-in single-layer launch (conv_proposed's path)
+        layers = [L for L in layers if L["layer"].name == args.only]
     items = [(L["plan"], L["dev"], None, L["out"]) for L in layers]
     conv.issue_k1(items)
     torch.cuda.synchronize()
-    buf = torch.zeros(9 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.full((25 * 4096,), -1, dtype=torch.int64, device="cuda")
+    buf[: 7 * 4096].zero_()
     _native.call("fhe_debug_trace", buf.data_ptr())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -43,6 +49,8 @@ def main():
     mhz = (cc[:, 1] - cc[:, 0]) / ((ct[:, 1] - ct[:, 0]) / 1e3)
     print(f"SM clock during the launch (clock64 / globaltimer): median {np.median(mhz):.0f} MHz "
           f"(min {mhz.min():.0f}, max {mhz.max():.0f})")
+    if args.cta_dump:
+        np.savez(args.cta_dump, ct=ct, toff=allb[7 * 4096 + 2048 : 7 * 4096 + 2048 + 24])
     t0g = ct[:, 0].min()
     ends = (ct[:, 1] - t0g) / 1e3
     print(f"per-CTA globaltimer (us from the first CTA start): start spread {(ct[:, 0].max() - t0g) / 1e3:.1f}, "
@@ -58,16 +66,24 @@ def main():
           f" {'mma/tile':>9s} {'wait/tile':>9s} {'epi/tile':>9s} {'commit->epi':>11s}")
     for l, L in enumerate(layers):
         d = L["plan"].tc
-        tiles = (P.n // (d.pos_tile * d.rep)) * -(-d.c_o // 128) * 2 * d.frags
-        toff = int(t[7][2048 + l])  # the kernel's dealing offset of this layer
-        mine = len(range((0 - toff) % 148, tiles, 148))
-        first, last = tl, tl + mine - 1
+        seq = t[7][1024:2048]  # the layer of each tile CTA 0 ran (the kernel's tile sequence)
+        idx = np.nonzero(seq[: int(np.count_nonzero(t[0][:1024]))] == l)[0]
+        mine = len(idx)
+        first, last = (int(idx[0]), int(idx[-1])) if mine else (tl, tl - 1)
         print(f"{L['layer'].name:10s} {rel(t[2][64 + l]) if l else -1:9d} {rel(t[3][l]) if l else -1:9d} {rel(t[7][l]):9d} {rel(t[0][first]) if mine else -1:9d} "
               f"{rel(t[1][last]) if mine else -1:9d} {rel(t[6][last]) if mine else -1:9d} {mine:11d}"
               f" {int(np.mean([t[1][i] - t[0][i] for i in range(first, last + 1)])) if mine else -1:9d}"
               f" {int(np.mean([t[4][i] - t[0][i] for i in range(first, last + 1)])) if mine else -1:9d}"
               f" {int(np.mean([t[6][i] - t[5][i] for i in range(first, last + 1)])) if mine else -1:9d}"
               f" {int(np.mean([t[5][i] - t[1][i] for i in range(first, last + 1)])) if mine else -1:11d}")
+        if args.detail == L["layer"].name and mine:
+            W = allb[9 * 4096 : 25 * 4096].reshape(16, 4096)
+            for i in range(first, min(last + 1, first + 12)):
+                seen = W[:8, i] - t[0][first]
+                done = W[8:, i] - t[0][first]
+                print(f"  tile {i - first:3d}: mma start {int(t[0][i] - t[0][first]):7d} tempty {int(t[4][i] - t[0][first]):7d} "
+                      f"commit {int(t[1][i] - t[0][first]):7d} | tfull seen per warp " + " ".join(f"{int(v):7d}" for v in seen)
+                      + " | done " + " ".join(f"{int(v):7d}" for v in done))
         tl += mine
 
 

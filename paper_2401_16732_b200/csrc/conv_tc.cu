@@ -691,6 +691,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
     if (atomicAdd(&cta_done[l], 1u) == (unsigned)participants - 1) {
       __threadfence();
       atomicAdd(A.sync + kRdy + l, 1ull);
+      if (trc && l < 2) trc[8 * 4096 + 1024 + 2 * blockIdx.x + l] = gtime();  // this CTA's layer-0/1 relayout done (trace)
     }
   };
   auto relayout_layer = [&](int l, int participants) {
@@ -718,6 +719,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
 #endif
       asm volatile("fence.proxy.async.shared::cta;");
       __threadfence();
+
       // every lane's X stores happen-before lane 0 (warp barrier), and lane 0's
       // own gpu-scope fence AFTER the barrier makes them (cumulatively) visible
       // before its completion count: a fence only before the barrier orders a

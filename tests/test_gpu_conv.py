@@ -406,3 +406,47 @@ def test_conv_conventional_fused_matches_materialized(monkeypatch, H, c_i, c_o):
         for dx in range(3):
             want += np.einsum("oi,ihw->ohw", w[:, :, dy, dx], pad[:, dy : dy + H, dx : dx + H])
     assert np.array_equal(conv.unpack(mat, sk), bfv.centered(want, P.p))
+
+
+# K1-TC epilogue variants (csrc/conv_tc.cu): q = 2^60 - delta with delta < 2^35
+# takes the pseudo-Mersenne reduction (finish_pm / finish_pm_pair, the
+# reference's default q), any other 2^56 <= q < 2^62 the Shoup reduction; the
+# 32-bit plane pairs apply to short contractions (127·255·257·c_i·taps < 2^31:
+# 1x1 projections, the tap-folded 7x7 stem). Each case is checked against the
+# integer-pipe kernel (an independent implementation) and the oracle. (The
+# moduli are primes = 1 mod 2n, as RingParams requires.)
+_EPI_MODULI = {
+    "pm_default": 1152921486375014401,  # delta = 0x43eb3afff
+    "pm_edge": 1152921470247149569,  # delta = 0x7ffff5fff, just below 2^35
+    "shoup_60": 1152921467550908417,  # delta = 0x8a0b4bfff >= 2^35
+    "shoup_61": 2305843003754438657,  # a 61-bit q
+    "shoup_57": 72057595874308097,  # a 57-bit q (2^56 <= q)
+}
+
+
+@pytest.mark.parametrize("qname", sorted(_EPI_MODULI))
+@pytest.mark.parametrize("geom", [(8, 3, 64, 130), (16, 1, 64, 96), (32, 7, 3, 16)])
+def test_tc_epilogue_moduli(qname, geom, monkeypatch):
+    from paper_2401_16732_b200 import conv, params
+
+    q = _EPI_MODULI[qname]
+    H, f_w, c_i, c_o = geom
+    P = params.RingParams(n=N, q=q, p=P_, sigma=3.2, decomp_log=16)
+    rng = np.random.default_rng(H + 7 * c_o)
+    lay = conv.layout_direct(P, H, H, f_w)
+    arr = rng.integers(0, q, (lay.ct_count(c_i), 2, N), dtype=np.int64)
+    arr[:, :, ::13] = q - 1  # extreme coefficients: the largest plane sums
+    w = rng.choice([-127, 127, -1, 0, 1, 5], size=(c_o, c_i, f_w, f_w))
+    w[: c_o // 2] = 127  # a channel block of maximal positive sums
+    spec = conv.ConvLayerSpec(H, H, f_w, c_i, c_o, w)
+    assert conv.conv_plan(spec, lay, P).tc is not None
+    monkeypatch.setenv("FLASHHE_CONV_PATH", "tc")
+    y_tc = _out(conv.conv_proposed(conv.PackedTensor(_cts(arr, q), lay, c_i), spec, P).cts)
+    monkeypatch.setenv("FLASHHE_CONV_PATH", "int")
+    y_int = _out(conv.conv_proposed(conv.PackedTensor(_cts(arr, q), lay, c_i), spec, P).cts)
+    assert np.array_equal(y_tc, y_int)
+    layd = {"n": N, "w_p": lay.w_p, "pad": lay.pad, "tile": lay.tile, "c_n": lay.c_n, "frags": lay.frags}
+    chans = sorted({0, c_o // 2, c_o - 1})
+    ref = O.conv_proposed(arr, w.reshape(c_o, c_i, -1), layd, q, channels=chans)
+    got = y_tc.reshape(c_o, lay.frags, 2, N)[chans].reshape(-1, 2, N)
+    assert np.array_equal(got, ref.reshape(-1, 2, N))

@@ -52,6 +52,13 @@ def main():
     if args.cta_dump:
         np.savez(args.cta_dump, ct=ct, toff=allb[7 * 4096 + 2048 : 7 * 4096 + 2048 + 24])
     t0g = ct[:, 0].min()
+    rd = allb[8 * 4096 + 1024 : 8 * 4096 + 1024 + 2 * 148].reshape(148, 2)
+    for k in range(2):
+        v = (rd[:, k] - t0g) / 1e3
+        v = v[rd[:, k] > 0]
+        if len(v):
+            print(f"layer {k} relayout done per CTA (us): min {v.min():.1f} p50 {np.median(v):.1f} p90 "
+                  f"{np.percentile(v, 90):.1f} max {v.max():.1f}")
     ends = (ct[:, 1] - t0g) / 1e3
     print(f"per-CTA globaltimer (us from the first CTA start): start spread {(ct[:, 0].max() - t0g) / 1e3:.1f}, "
           f"end min {ends.min():.1f} median {np.median(ends):.1f} max {ends.max():.1f} (CTA {int(ends.argmax())})")

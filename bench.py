@@ -437,7 +437,40 @@ def sub_benchmarks(steps, warmup, hbm, peaks=None):
     res["act2pc_layer"] = act2pc_layer(steps, warmup)
     res["pool_fc_tail"] = pool_fc_tail(steps, warmup)
     res["inference_chain"] = {name: inference_chain(name) for name in ("config3", "config4", "config5")}
+    res["inference_chain_batched"] = {"config5": inference_chain_many("config5", 8)}
     return res
+
+
+def inference_chain_many(name, reqs):
+    """inference.he_forward_many: `reqs` independent requests in lockstep, each
+    conv layer of all requests as one stacked tensor-core launch (the drop-in
+    path batched over requests); per-request conv time against the one-request
+    chain. One run after a warm-up run, every request checked against the
+    integer model."""
+    from paper_2401_16732_b200 import bfv, inference, params
+
+    P = params.default_params()
+    layers = inference.config_layers(name)
+    convs = inference._convs(layers)
+    rng = np.random.default_rng(77)
+    weights = inference.random_weights(layers, rng)
+    specs = inference.layer_specs(layers, weights)
+    sk = bfv.keygen(P, np.random.default_rng(78))
+    out = {}
+    for it in range(2):
+        rng = np.random.default_rng(90 + it)
+        xs = [rng.integers(0, 8, (convs[0].c_i, convs[0].H, convs[0].W), dtype=np.int64) for _ in range(reqs)]
+        t = {}
+        got = inference.he_forward_many(layers, xs, weights, sk, rng, P, timings=t, specs=specs)
+        ok = all(np.array_equal(g, inference.plain_forward(layers, x, weights, P.p)) for x, g in zip(xs, got))
+        per_conv = t.pop("per_conv_s")
+        out = {"requests": reqs, "convs": len(convs), "bit_exact_vs_integer_model": ok,
+               "conv_ms_total": round(t["conv_s"] * 1e3, 2), "conv_ms_per_request": round(t["conv_s"] * 1e3 / reqs, 3),
+               "act_ms_per_request": round(t["act_s"] * 1e3 / reqs, 2),
+               "per_conv_layer_ms_all_requests": [round(v * 1e3, 3) for v in per_conv],
+               "note": "conv time per request with the layer's convs of all requests in one stacked launch "
+                       "(conv.conv_proposed_many); activations and repacks stay per request"}
+    return out
 
 
 def inference_chain(name):

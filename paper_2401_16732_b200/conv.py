@@ -674,6 +674,32 @@ def conv_proposed(x: PackedTensor, layer: ConvLayerSpec, params: RingParams, laz
     return PackedTensor(cts, _out_layout(x.layout), layer.c_o, x.scale + layer.weight_scale)
 
 
+def conv_proposed_many(xs, layer: ConvLayerSpec, params: RingParams, outs=None) -> list[PackedTensor]:
+    """conv_proposed over several independent inputs of ONE layer — e.g. the
+    same layer of several inference requests (inference.he_forward_many).
+    The tensor-core jobs run as stacked launches (issue_k1: up to 24 jobs in
+    one fhe_conv_tc_stack launch, sharing the layer's packed weights), so the
+    per-launch relayout latency and launch overhead of the one-job drop-in
+    call are paid once per stack. `outs` (optional): one device output buffer
+    per input, as conv_proposed's `out=`. Results equal conv_proposed's."""
+    xs = list(xs)
+    items, plans = [], []
+    for i, x in enumerate(xs):
+        plan = _proposed_plan(x, layer, params)
+        out = outs[i] if outs is not None else None
+        if out is not None and (tuple(out.shape) != (plan.n_out, 2, params.n) or out.dtype != torch.int64
+                                or not out.is_contiguous()):
+            raise ParameterError(f"out must be a contiguous int64 [{plan.n_out}, 2, {params.n}] tensor")
+        inp = bfv.cts_rows(x.cts).contiguous()
+        if out is None:
+            out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=inp.device)
+        items.append((plan, inp, None, out))
+        plans.append(plan)
+    issue_k1(items)
+    return [PackedTensor(bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF), _out_layout(x.layout),
+                         layer.c_o, x.scale + layer.weight_scale) for x, (_, _, _, out) in zip(xs, items)]
+
+
 _out_layouts: dict = {}
 
 

@@ -157,5 +157,88 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
     return out
 
 
+def he_forward_many(layers, xs, weights: dict, sk: bfv.SecretKey, rng, params: RingParams, frac_bits: int = 0,
+                    timings: dict | None = None, specs: dict | None = None) -> list[np.ndarray]:
+    """he_forward over several independent requests in lockstep: each conv
+    layer of all requests runs as stacked tensor-core launches
+    (conv.conv_proposed_many -> conv.issue_k1, up to 24 requests per launch);
+    the layer exchanges (act2pc) and the tail stay per request. Returns each
+    request's decrypted logits mod p (equal to he_forward's)."""
+    import time
+
+    import torch
+
+    P = params
+    seq, pool, fc = main_path(layers)
+    specs = specs if specs is not None else layer_specs(layers, weights)
+    t = dict(conv_s=0.0, act_s=0.0, offline_s=0.0, repack_s=0.0)
+    per_conv = []
+    first = seq[0]
+    t0 = time.perf_counter()
+    curs = []
+    for x in xs:
+        c = conv.pack_input(x, P, first.f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
+        rows = bfv.cts_rows(c.cts).contiguous()
+        curs.append(conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), c.layout,
+                                      c.channels, c.scale))
+    torch.cuda.synchronize()
+    t["input_s"] = time.perf_counter() - t0
+
+    def next_layout(i, h):
+        nxt = seq[i + 1]
+        return conv.layout_direct(P, h, h, nxt.f_w if nxt.kind == "conv" else 3)
+
+    for i, l in enumerate(seq):
+        if l.kind == "conv":
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ys = conv.conv_proposed_many(curs, specs[l.name], P)
+            torch.cuda.synchronize()
+            t["conv_s"] += time.perf_counter() - t0
+            per_conv.append(time.perf_counter() - t0)
+            nxt = []
+            for y in ys:
+                if l.stride > 1:  # subsampled by the client's repack below
+                    y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
+                t0 = time.perf_counter()
+                plan = act2pc.repack_plan(y.layout, l.c_o, next_layout(i, l.H // l.stride), P)
+                sess = act2pc.offline_prepare_layer(plan, P, rng, frac_bits=frac_bits)
+                zeros = bfv.precompute_zero_rows(sk, rng, 3 * plan.k_dst)
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                nxt.append(act2pc.run_layer_activation(y, sess, sk, zeros, P))
+                torch.cuda.synchronize()
+                t["offline_s"] += t1 - t0
+                t["act_s"] += time.perf_counter() - t1
+            curs = nxt
+        elif l.kind == "pool" and l is not pool:
+            nxt = []
+            for cur in curs:
+                t0 = time.perf_counter()
+                pooled = conv.avg_pool(cur, l.f_w, P)
+                h = cur.layout.height // l.f_w
+                plan = act2pc.repack_plan(pooled.layout, l.c_o, next_layout(i, h), P)
+                rs = act2pc.offline_prepare_repack(plan, P, rng)
+                zeros = bfv.precompute_zero_rows(sk, rng, plan.k_dst)
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                nxt.append(act2pc.run_repack_round(pooled, rs, sk, zeros, P))
+                torch.cuda.synchronize()
+                t["offline_s"] += t1 - t0
+                t["repack_s"] += time.perf_counter() - t1
+            curs = nxt
+    t0 = time.perf_counter()
+    outs = []
+    for cur in curs:
+        pooled = conv.avg_pool(cur, pool.f_w, P)
+        logits = conv.fully_connected(pooled, weights["fc"], P)
+        outs.append(bfv.centered(conv.read_scalar_outputs(logits, sk), P.p) % P.p)
+    t["tail_s"] = time.perf_counter() - t0
+    if timings is not None:
+        timings.update(t)
+        timings["per_conv_s"] = per_conv
+    return outs
+
+
 def config_layers(name: str):
     return stacks.CONFIGS[name]()

@@ -450,3 +450,22 @@ def test_tc_epilogue_moduli(qname, geom, monkeypatch):
     ref = O.conv_proposed(arr, w.reshape(c_o, c_i, -1), layd, q, channels=chans)
     got = y_tc.reshape(c_o, lay.frags, 2, N)[chans].reshape(-1, 2, N)
     assert np.array_equal(got, ref.reshape(-1, 2, N))
+
+
+def test_conv_proposed_many_matches_single_calls():
+    """conv_proposed_many (one stacked launch for several inputs of one layer,
+    incl. more than the 24 jobs of one launch) equals conv_proposed per input."""
+    from paper_2401_16732_b200 import conv
+
+    P = _P()
+    rng = np.random.default_rng(99)
+    for H, f_w, c_i, c_o, count in [(16, 3, 32, 48, 3), (8, 3, 64, 130, 26)]:
+        lay = conv.layout_direct(P, H, H, f_w)
+        spec = conv.ConvLayerSpec(H, H, f_w, c_i, c_o, rng.integers(-127, 128, (c_o, c_i, f_w, f_w)))
+        xs = [conv.PackedTensor(_cts(rng.integers(0, Q, (lay.ct_count(c_i), 2, N), dtype=np.int64)), lay, c_i)
+              for _ in range(count)]
+        ys = conv.conv_proposed_many(xs, spec, P)
+        for x, y in zip(xs, ys):
+            ref = conv.conv_proposed(x, spec, P)
+            assert np.array_equal(_out(y.cts), _out(ref.cts))
+            assert y.layout == ref.layout and y.channels == ref.channels and y.scale == ref.scale

@@ -466,9 +466,11 @@ def inference_chain_many(name, reqs):
         per_conv = t.pop("per_conv_s")
         out = {"requests": reqs, "convs": len(convs), "bit_exact_vs_integer_model": ok,
                "conv_ms_total": round(t["conv_s"] * 1e3, 2), "conv_ms_per_request": round(t["conv_s"] * 1e3 / reqs, 3),
+               "conv_gpu_ms_per_request": round(t["conv_gpu_s"] * 1e3 / reqs, 3),
                "act_ms_per_request": round(t["act_s"] * 1e3 / reqs, 2),
                "per_conv_layer_ms_all_requests": [round(v * 1e3, 3) for v in per_conv],
-               "note": "conv time per request with the layer's convs of all requests in one stacked launch "
+               "note": "conv time per request (wall clock incl. host issue; conv_gpu: CUDA events around the "
+                       "launches) with the layer's convs of all requests in one stacked launch "
                        "(conv.conv_proposed_many); activations and repacks stay per request"}
     return out
 

@@ -192,9 +192,13 @@ def he_forward_many(layers, xs, weights: dict, sk: bfv.SecretKey, rng, params: R
         if l.kind == "conv":
             torch.cuda.synchronize()
             t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             ys = conv.conv_proposed_many(curs, specs[l.name], P)
+            e1.record()
             torch.cuda.synchronize()
             t["conv_s"] += time.perf_counter() - t0
+            t["conv_gpu_s"] = t.get("conv_gpu_s", 0.0) + e0.elapsed_time(e1) / 1e3  # device time of the launches
             per_conv.append(time.perf_counter() - t0)
             nxt = []
             for y in ys:

@@ -227,10 +227,9 @@ typedef struct fhe_conv_tc_layer {
                              positions; w then holds taps*rep tap blocks, block r*taps + t
                              carrying tap t's weights in rows [r*128/rep, r*128/rep + c_o)
                              (zero elsewhere) — group r reads the window 32 r positions on */
-  int tsplit;             /* 1 (or 0) or a divisor of taps*rep: a 32-channel block's MMAs are
-                             spread over tsplit pipeline stages of taps*rep/tsplit weight
-                             tiles each (the window is loaded per stage): shared-memory
-                             stages stay small enough for two in flight */
+  int tsplit;             /* reserved, 0 or 1 (a 32-channel block's MMAs run in one pipeline
+                             stage; layers with one output-channel block keep their weights
+                             resident in shared memory instead) */
 } fhe_conv_tc_layer;
 /* layers: HOST array of nl (<= 24) layers sharing (q, n), 2^56 <= q < 2^62.
  * X: DEVICE scratch. x_stride > 0: 3 operand buffers x_stride bytes apart

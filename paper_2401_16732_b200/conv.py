@@ -303,15 +303,15 @@ class ConvTcPlan:
 
     @staticmethod
     def pos_tile_for(c_o: int, n: int, frags: int, h: int, taps: int, c_i: int = 32) -> int:
-        """Positions per tile (csrc/conv_tc.cu): 32, or 16 when 32 does not
-        fit. FLASHHE_TC_POS = 32 (default) | 16 | 64 | auto. 64 (two
-        accumulators share each weight stage: half the weight bytes per
-        position, but no TMEM double buffering) measured 6 % slower on the
-        config-4 stack; `auto` uses it for long contractions
-        (ceil(c_i/32)·taps >= 72)."""
+        """Positions per tile (csrc/conv_tc.cu): 32, 64 or 16. FLASHHE_TC_POS =
+        auto (default) | 32 | 16 | 64. `auto` takes 64 (two accumulators share
+        each weight stage: half the weight bytes per position, but no TMEM
+        double buffering) for long contractions (ceil(c_i/32)·taps >= 72, the
+        s3/s4 layers: measured 1.2 % faster on config 5 and 0.5 % on config 4
+        with dynamic tile scheduling), 16 when 32 does not fit, else 32."""
         import os
 
-        mode = os.environ.get("FLASHHE_TC_POS", "32")
+        mode = os.environ.get("FLASHHE_TC_POS", "auto")
         if mode != "auto":
             return int(mode) if int(mode) <= 32 or ConvTcPlan._fits(int(mode), h, taps) else 32
         if not ConvTcPlan._fits(32, h, taps):
@@ -322,45 +322,35 @@ class ConvTcPlan:
 
     @staticmethod
     def rep_for(c_o: int, JB: int, taps: int, h: int) -> tuple[int, int]:
-        """(rep, tsplit): position groups stacked in the 128 accumulator rows
-        (csrc/conv_tc.cu LayerDesc.rep) and the number of pipeline stages a
-        32-channel block's MMAs are spread over. A layer with c_o <= 64 fills
-        only c_o TMEM lanes, so only the warps of c_o/32 lane quadrants (SM
+        """(rep, 1): position groups stacked in the 128 accumulator rows
+        (csrc/conv_tc.cu LayerDesc.rep). A layer with c_o <= 64 fills only
+        c_o TMEM lanes, so only the warps of c_o/32 lane quadrants (SM
         sub-partitions) can read its accumulators: short contractions (JB·taps
-        <= 18 MMAs per 32 positions — the stems, the 64-channel layers) are
-        then bound by the epilogue, not the MMAs. With rep groups, rows
-        r·128/rep + o compute channel o at positions 32 r.. of the tile (the
-        same window, tap offsets + 32 r): every quadrant's warps run the
-        epilogue, for the same MMA work per position. When the taps·rep weight
-        tiles make a stage too large for two in flight, they can be split over
-        tsplit stages (each reloads the window) — FLASHHE_TC_TSPLIT=1; off by
-        default: the 64-channel 3x3 layers ran 5-10 % slower that way (two
-        stages in flight starve the MMAs). FLASHHE_TC_REP (1 | 2 | 4) forces a
-        rep where it is valid."""
+        <= 16 MMAs per 32 positions — the stems) are then bound by the
+        epilogue, not the MMAs. With rep groups, rows r·128/rep + o compute
+        channel o at positions 32 r.. of the tile (the same window, tap offsets
+        + 32 r): every quadrant's warps run the epilogue, for the same MMA work
+        per position. FLASHHE_TC_REP (1 | 2 | 4) forces a rep where it is
+        valid. (The second value is the C ABI's reserved tsplit field: a
+        block's MMAs always run in one stage; a split over several stages was
+        measured slower and removed.)"""
         import os
 
-        splits = (1, 2, 3) if os.environ.get("FLASHHE_TC_TSPLIT") == "1" else (1,)
-
         def fit(r):
-            for ts in splits:
-                if (taps * r) % ts:
-                    continue
-                stage = -(-(32 * r + 2 * h) * 256 // 1024) * 1024 + (taps * r // ts) * 32 * ConvTcPlan.OC_TILE
-                if 2 * stage <= 218 * 1024:
-                    return ts
-            return None
+            stage = -(-(32 * r + 2 * h) * 256 // 1024) * 1024 + taps * r * 32 * ConvTcPlan.OC_TILE
+            return 2 * stage <= 218 * 1024
 
         def ok(r):
-            return r == 1 or (c_o <= ConvTcPlan.OC_TILE // r and taps * r <= 64 and fit(r) is not None)
+            return r == 1 or (c_o <= ConvTcPlan.OC_TILE // r and taps * r <= 64 and fit(r))
 
         forced = os.environ.get("FLASHHE_TC_REP")
         if forced and ok(int(forced)):
             r = int(forced)
-        elif forced or JB * taps > (18 if len(splits) > 1 else 16):
+        elif forced or JB * taps > 16:
             r = 1
         else:
             r = next(r for r in (4, 2, 1) if ok(r))
-        return r, (fit(r) or 1) if r > 1 else 1
+        return r, 1
 
     @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:

@@ -125,7 +125,6 @@ struct LayerDesc {
   int slot_bytes, nslots;  // ring partition this layer runs in: nslots slots of slot_bytes >= stage_bytes
   int res_bytes;           // > 0: the layer's weights (one output block) stay resident at the ring base and
                            // a stage is just the window (slots follow the weights); loaded once per CTA
-  int tsplit, tg;          // tap groups per 32-channel block (stages per block) and taps per group
   int rep;   // 32-position groups stacked in the 128 accumulator rows (c_o <= 128 / rep): 1, 2 or 4
   int pair;  // 1: plane sums are below 2^31 / 257 (short contraction): the epilogue pairs planes in 32 bits
   int16_t tap_off[kMaxTaps];  // step_t + h
@@ -793,7 +792,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
         uint32_t off16[16];  // this layer's DRot offsets in 16-byte descriptor units (fast paths)
 #pragma unroll
         for (int tp = 0; tp < 16; ++tp) off16[tp] = tp < taps ? (uint32_t)d.tap_off[tp] * 16 : 0u;
-        const int TS = d.tsplit, tg = d.tg, nstage = JB * TS;
+        const int nstage = JB;
         for (;; ++tl) {  // this CTA's tiles of layer l, in the loader's order
           int b0 = 0, b1 = 1;
           if (nacc == 1) {
@@ -801,8 +800,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             nb ^= 1;
           }
           if (lane == 0) TC_TRACE(0, tl);
-          for (int st = 0; st < nstage; ++st) {  // stage = (32-channel block, tap group)
-            const int jb = st;                   // (the fast paths run with one tap group: st == jb)
+          for (int jb = 0; jb < nstage; ++jb) {  // stage = one 32-channel block
             const int s = s_mma;
             const int s_next = s + 1 == nst ? 0 : s + 1;
             if (!pre) {
@@ -816,14 +814,14 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
             const uint32_t alo = res ? dlo0 + (uint32_t)jb * wtap : blo0 + wdesc;
             // a next stage of this layer: within the tile, or the sequence's next tile
             // when it is already published and of this layer
-            bool has_next = st + 1 < nstage;
+            bool has_next = jb + 1 < nstage;
             if (!has_next) {
               uint32_t nlt;
               has_next = tq_peek(tq, tl + 1, nlt) && (int)(nlt >> 24) == l;
             }
             for (int a = 0; a < nacc; ++a) {
               const int b = a == 0 ? b0 : b1;
-              if (st == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
+              if (jb == 0) {  // first use of this buffer in the tile: the epilogue must have drained it
                 mbar_wait(tempty_bar(b), ((use >> b) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 if (a == 0 && lane == 0) TC_TRACE(4, tl);
@@ -837,14 +835,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                   pre = true;
                 }
               };
-              if (TS > 1) {  // one tap group of several: offsets of group g, weights at the stage base
-                const int g = st % TS;
-                for (int tp = 0; tp < tg; ++tp) {
-                  if (tp == tg - 1) wait_next();
-                  mma_i8w_elect(acc, alo + (uint32_t)(tp * (4096 >> 4)), blo + (uint32_t)d.tap_off[g * tg + tp] * 16,
-                                dhi, idesc, (st | tp) != 0);
-                }
-              } else if (taps == 9) {
+              if (taps == 9) {
                 issue_taps<9>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
               } else if (taps == 1) {
                 issue_taps<1>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
@@ -935,8 +926,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
           const Tile T = tile_of(t, d, n);
           const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
           const uint8_t* wbase = d.W + (size_t)T.ob * d.JB * wstage;
-          for (int st = 0; st < d.JB * d.tsplit; ++st) {  // stage = (32-channel block, tap group)
-            const int jb = st / d.tsplit, g = st - jb * d.tsplit;
+          for (int jb = 0; jb < d.JB; ++jb) {  // stage = one 32-channel block
             const int s = s_ld;
             if ((used >> s) & 1) mbar_wait_sleep(empty_bar(s), ((par >> s) & 1) ^ 1, 32);
             used |= 1u << s;
@@ -962,16 +952,15 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
               if (res_pending) bulk_load(smem_u32(smem), d.W, (uint32_t)d.res_bytes, full_bar(s));
               res_pending = false;
             } else {
-              const uint32_t wgroup = (uint32_t)d.tg * kWTap;  // this stage's tap group of weights
               asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full_bar(s)),
-                           "r"(win_load + wgroup)
+                           "r"(win_load + wstage)
                            : "memory");
               FHE_CHECK(pos + (uint32_t)d.stage_bytes <= (uint32_t)(d.nslots * d.slot_bytes) &&
                         d.stage_bytes <= d.slot_bytes &&
                         win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
-                        wbase + (size_t)jb * wstage + (size_t)(g + 1) * wgroup <= d.W + d.w_bytes);
+                        wbase + (size_t)(jb + 1) * wstage <= d.W + d.w_bytes);
               bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
-              bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage + (size_t)g * wgroup, wgroup, full_bar(s));
+              bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
             }
 #endif
             s_ld = s + 1 == d.nslots ? 0 : s + 1;
@@ -1415,9 +1404,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.c_o = s.c_o;
     d.OB = (s.c_o + tc::kOcTile - 1) / tc::kOcTile;
     d.taps = s.taps * rep;  // MMAs per 32-channel block: every tap for every stacked position group
-    d.tsplit = s.tsplit < 1 ? 1 : s.tsplit;  // the block's MMAs over this many stages (tap groups)
-    if (d.taps % d.tsplit) return fail(FHE_ERR_VALUE, "tc layer %d: taps x rep not divisible by tsplit", l);
-    d.tg = d.taps / d.tsplit;
+    if (s.tsplit > 1) return fail(FHE_ERR_VALUE, "tc layer %d: tsplit is reserved (0 or 1)", l);
     d.rep = rep;
     // |P_d| <= 127·255·c_i·taps (each accumulator row sums one position group's taps)
     d.pair = 127ll * 255 * 257 * s.c_i * s.taps < (1ll << 31) ? 1 : 0;
@@ -1434,7 +1421,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
       for (int r = 0; r < rep; ++r) d.tap_off[r * s.taps + t] = (int16_t)(off + r * d.npos);  // group r: +32 r
     }
     d.win_bytes = ((d.tpos + 2 * d.h) * 256 + 1023) / 1024 * 1024;
-    d.stage_bytes = d.win_bytes + d.tg * tc::kWTap;
+    d.stage_bytes = d.win_bytes + d.taps * tc::kWTap;
     d.nst = std::min(tc::kMaxStages, tc::kRingBudget / d.stage_bytes);
     if (d.nst < 2) return fail(FHE_ERR_VALUE, "tc layer %d: halo too large for the tc path", l);
     // Keep the previous layer's ring partition when this layer's stages fit its
@@ -1446,7 +1433,7 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     // window (the 7x7 stem: 74 -> 18 KB per tile, 2 -> 6 stages in flight).
     const int wres = d.JB * d.taps * tc::kWTap;
     d.res_bytes = 0;
-    if (d.OB == 1 && d.tsplit == 1 && resident_allowed() && wres + 3 * d.win_bytes <= tc::kRingBudget) {
+    if (d.OB == 1 && resident_allowed() && wres + 3 * d.win_bytes <= tc::kRingBudget) {
       d.res_bytes = wres;
       d.slot_bytes = d.win_bytes;
       d.nslots = std::min(tc::kMaxStages, (tc::kRingBudget - wres) / d.win_bytes);

@@ -133,7 +133,8 @@ struct LayerDesc {
 constexpr int kRdy = 3 + kMaxLayers;      // sync index of layer 0's relayout-done counter
 constexpr int kGem = 3 + 2 * kMaxLayers;  // sync index of layer 0's GEMM-done counter
 constexpr int kTile = 3 + 3 * kMaxLayers; // sync index of layer 0's tile counter (dynamic tile scheduling)
-constexpr int kSyncWords = 3 + 4 * kMaxLayers;
+constexpr int kSyncWords = 3 + 4 * kMaxLayers;  // counter words of a sync buffer (conv.SYNC_WORDS)
+static_assert(kTile + kMaxLayers == kSyncWords, "sync layout");
 constexpr int kTq = 32;                   // tile-sequence ring entries (loader -> MMA issuer, epilogue)
 
 // ML = layers the parameter block holds: kMaxLayers for stacks, 1 for the

@@ -673,6 +673,8 @@ def conv_proposed_many(xs, layer: ConvLayerSpec, params: RingParams, outs=None) 
     call are paid once per stack. `outs` (optional): one device output buffer
     per input, as conv_proposed's `out=`. Results equal conv_proposed's."""
     xs = list(xs)
+    if not xs:
+        return []
     items, plans = [], []
     for i, x in enumerate(xs):
         plan = _proposed_plan(x, layer, params)

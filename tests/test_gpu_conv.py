@@ -469,3 +469,18 @@ def test_conv_proposed_many_matches_single_calls():
             ref = conv.conv_proposed(x, spec, P)
             assert np.array_equal(_out(y.cts), _out(ref.cts))
             assert y.layout == ref.layout and y.channels == ref.channels and y.scale == ref.scale
+
+
+def test_conv_proposed_many_edges():
+    """No inputs -> no launch, empty result; a geometry mismatch raises like conv_proposed."""
+    from paper_2401_16732_b200 import conv
+    from paper_2401_16732_b200.errors import ParameterError
+
+    P = _P()
+    rng = np.random.default_rng(5)
+    spec = conv.ConvLayerSpec(8, 8, 3, 4, 4, rng.integers(-127, 128, (4, 4, 3, 3)))
+    assert conv.conv_proposed_many([], spec, P) == []
+    lay = conv.layout_direct(P, 16, 16, 3)
+    x = conv.PackedTensor(_cts(rng.integers(0, Q, (lay.ct_count(4), 2, N), dtype=np.int64)), lay, 4)
+    with pytest.raises(ParameterError):
+        conv.conv_proposed_many([x], spec, P)

@@ -715,6 +715,23 @@ def _proposed_plan(x: PackedTensor, layer: ConvLayerSpec, params: RingParams) ->
     return conv_plan(layer, layout, params)  # runs _check_budget before caching a plan
 
 
+def _stream_order(meta, params: RingParams) -> list[int]:
+    """Issue order of conv_proposed_stream's independent jobs (results keep the
+    call's order). The three streams form an upload -> K1 -> download pipeline
+    whose downloads dominate (outputs are c_o·frags ciphertexts, inputs c_i·frags
+    / c_n): the job with the smallest upload goes first, so the download stream
+    starts early, and the job with the largest download second, so every other
+    job's upload and convolution runs under it; the rest keep their order."""
+    if len(meta) < 3 or _os.environ.get("FLASHHE_STREAM_ORDER") == "given":
+        return list(range(len(meta)))
+    n_in = [len(x.cts) for x, _, _ in meta]
+    n_out = [plan.n_out for *_, plan in meta]
+    first = min(range(len(meta)), key=lambda j: (n_in[j], n_out[j], j))
+    rest = [j for j in range(len(meta)) if j != first]
+    second = max(rest, key=lambda j: (n_out[j], -j))
+    return [first, second] + [j for j in rest if j != second]
+
+
 def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     """Serving form of conv_proposed over a sequence of independent
     (PackedTensor, ConvLayerSpec) jobs — e.g. one layer of many requests, or
@@ -738,12 +755,13 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
     sizes = [plan.n_out * 2 * params.n for *_, plan in meta]
     host_all = torch.empty(sum(sizes), dtype=torch.int64, pin_memory=True)
     views = torch.split(host_all, sizes)
-    outs = []
+    outs = [None] * len(meta)
     fast = _native.fn("fhe_conv_stream_job")
     ev_up, ev_comp = torch.cuda.Event(), torch.cuda.Event()
     ev_up.record(comp)  # create the cudaEvent handles (torch makes them on first record)
     ev_comp.record(comp)
-    for (x, layer, plan), hv in zip(meta, views):  # one pass: job i's download is enqueued before job i+1's upload
+    for j in _stream_order(meta, params):  # one pass: job i's download is enqueued before job i+1's upload
+        (x, layer, plan), hv = meta[j], views[j]
         ready = None
         rows_in = x.cts.rows if isinstance(x.cts, bfv.CtStack) else None
         if plan.path == "tc" and rows_in is not None and rows_in._dev is None and rows_in._pinned is not None:
@@ -771,7 +789,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
             h.flags.writeable = False
             rows = device.DeviceRows(dev=out.reshape(-1, params.n), host=h, pinned=hv)
             cts = bfv.CtStack(rows, params.q, Encoding.DIRECT, Domain.COEFF)
-            outs.append(PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale))
+            outs[j] = PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)
             continue
         if isinstance(x.cts, bfv.CtStack):
             inp, ready = x.cts.rows.upload_on(up)
@@ -784,7 +802,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
         down.wait_event(ev)
         rows = device.DeviceRows.download_on(out, down, into=hv)
         cts = bfv.CtStack(rows, params.q, Encoding.DIRECT, Domain.COEFF)
-        outs.append(PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale))
+        outs[j] = PackedTensor(cts, replace(x.layout, c_n=1), layer.c_o, x.scale + layer.weight_scale)
     down.synchronize()
     return outs
 

@@ -286,3 +286,22 @@ def test_stack_schedule_is_johnson_optimal():
         assert sorted(order) == list(range(m))
         best = min(makespan(p, times) for p in itertools.permutations(range(m)))
         assert abs(makespan(order, times) - best) < 1e-9
+
+
+def test_stream_order_smallest_upload_then_largest_download():
+    """conv._stream_order: the job with the smallest upload first, the largest
+    download second, the rest in the call's order; every job exactly once."""
+    from types import SimpleNamespace as NS
+
+    from paper_2401_16732_b200 import conv, params
+
+    P = params.default_params()
+
+    def job(k_in, k_out):
+        return (NS(cts=[None] * k_in), None, NS(n_out=k_out))
+
+    meta = [job(240, 5120), job(128, 128), job(16, 32), job(64, 512), job(16, 64)]
+    order = conv._stream_order(meta, P)
+    assert sorted(order) == list(range(len(meta)))
+    assert order[:2] == [2, 0] and order[2:] == [1, 3, 4]
+    assert conv._stream_order(meta[:2], P) == [0, 1]

@@ -470,11 +470,22 @@ def _graph_for(plan: RepackPlan, params: RingParams, f: int) -> _LayerGraph:
     return hit[1]
 
 
+def _defer_budget(acc: "bfv.MaxAcc", into) -> None:
+    """Keep the round's largest decryption residual for a later check: an
+    8-byte device copy into slot `into = (tensor, index)` (no host read now)."""
+    buf, i = into
+    buf[i : i + 1].copy_(acc.t)
+
+
 def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
-                         params: RingParams, graph: bool | None = None):
+                         params: RingParams, graph: bool | None = None, budget_into=None):
     """Both parties in-process: one layer's full two-round exchange. With
     `graph` (default: FLASHHE_ACT_GRAPH != 0) the exchange replays a CUDA graph
-    captured per RepackPlan (identical ciphertexts, one launch)."""
+    captured per RepackPlan (identical ciphertexts, one launch).
+    `budget_into = (device int64 tensor, index)` (addition): the client's
+    noise-budget check is deferred — the round's largest residual is stored
+    there for one check after a whole chain (check_deferred_budgets) instead
+    of one host read per layer."""
     import os
 
     if graph is None:
@@ -493,7 +504,10 @@ def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zer
         f = session.codec.frac_bits if session.codec else 0
         out, maxw = _graph_for(plan, params, f).run(bfv.cts_rows(cts), session, sk, zero_rows)
         session.round = Round.DONE
-        _check_budget_rows(params, maxw)
+        if budget_into is not None:
+            _defer_budget(maxw, budget_into)
+        else:
+            _check_budget_rows(params, maxw)
         res = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
         return conv.PackedTensor(res, plan.dst, plan.channels, getattr(conv_out, "scale", 0))
     plan = session.plan
@@ -503,7 +517,10 @@ def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zer
     m2 = server_round2_layer((sq, w), session, params)
     back = client_round2_layer(m2, plan, sk, zeros, pending)
     out = server_finalize_layer(sq, back, session, params, getattr(conv_out, "scale", 0))
-    _check_budget_rows(params, pending)
+    if budget_into is not None:
+        _defer_budget(pending, budget_into)
+    else:
+        _check_budget_rows(params, pending)
     return out
 
 
@@ -515,6 +532,14 @@ def run_layer_activation(conv_out, session: LayerSession, sk: bfv.SecretKey, zer
 # ⟦a⟧ with r, the client decrypts a + r, repacks it and re-encrypts it
 # (direct), the server removes the repacked mask r'. One round trip, two
 # messages, the client sees only a + r.
+
+
+def check_deferred_budgets(params: RingParams, residuals) -> None:
+    """The client's noise-budget checks of a chain run with `budget_into`: one
+    host read of every stored residual; raises like the per-round check."""
+    vmax = int(residuals.cpu().numpy().max()) if residuals.numel() else 0  # one D2H copy, no reduction kernel
+    if bfv._budget(params, vmax) <= 0:
+        raise ProtocolError("noise budget exhausted: ciphertext no longer decrypts reliably")
 
 
 @dataclass
@@ -532,8 +557,9 @@ def offline_prepare_repack(plan: RepackPlan, params: RingParams, rng) -> RepackS
 
 
 def run_repack_round(x, session: RepackSession, sk: bfv.SecretKey, zeros: bfv.ZeroRowPool,
-                     params: RingParams):
-    """⟦a⟧ (any direct layout, stride pending) -> ⟦a'⟧ packed for the next conv."""
+                     params: RingParams, budget_into=None):
+    """⟦a⟧ (any direct layout, stride pending) -> ⟦a'⟧ packed for the next conv
+    (`budget_into`: as run_layer_activation's)."""
     from . import conv
 
     _expect(session, Round.INIT)
@@ -548,6 +574,9 @@ def run_repack_round(x, session: RepackSession, sk: bfv.SecretKey, zeros: bfv.Ze
     back = _encrypt_rows(zeros.take_rows(plan.k_dst), _gather(plan.idx, w), params)
     out = _encrypt_rows(back, session.neg_r_dst, params)  # server: ⟦a' + r'⟧ − r' (plain_add of −r')
     session.round = Round.DONE
-    _check_budget_rows(params, pending)
+    if budget_into is not None:
+        _defer_budget(pending, budget_into)
+    else:
+        _check_budget_rows(params, pending)
     cts_out = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
     return conv.PackedTensor(cts_out, plan.dst, plan.channels, getattr(x, "scale", 0))

@@ -244,5 +244,81 @@ def he_forward_many(layers, xs, weights: dict, sk: bfv.SecretKey, rng, params: R
     return outs
 
 
+def he_prepare(layers, params: RingParams, sk: bfv.SecretKey, rng, frac_bits: int = 0) -> list:
+    """The chain's offline phase up front: for every activation exchange and
+    pool repack of the main path, its repack plan, masks (act2pc sessions) and
+    encryptions of zero, in chain order. The layouts follow from the geometry
+    alone (conv output = input layout with one channel per ciphertext, stride
+    pending; exchange output = the plan's destination), so no ciphertext is
+    needed. Sessions are single-use: prepare once per inference."""
+    P = params
+    seq, pool, _ = main_path(layers)
+
+    def next_layout(i, h):
+        nxt = seq[i + 1]
+        return conv.layout_direct(P, h, h, nxt.f_w if nxt.kind == "conv" else 3)
+
+    steps = []
+    lay = conv.layout_direct(P, seq[0].H, seq[0].W, seq[0].f_w)
+    for i, l in enumerate(seq):
+        if l.kind == "conv":
+            y_lay = replace(lay, c_n=1, stride=l.stride) if l.stride > 1 else replace(lay, c_n=1)
+            plan = act2pc.repack_plan(y_lay, l.c_o, next_layout(i, l.H // l.stride), P)
+            sess = act2pc.offline_prepare_layer(plan, P, rng, frac_bits=frac_bits)
+            steps.append(("act", plan, sess, bfv.precompute_zero_rows(sk, rng, 3 * plan.k_dst)))
+            lay = plan.dst
+        elif l.kind == "pool" and l is not pool:
+            pooled = replace(lay, stride=l.f_w)
+            plan = act2pc.repack_plan(pooled, l.c_o, next_layout(i, lay.height // l.f_w), P)
+            steps.append(("repack", plan, act2pc.offline_prepare_repack(plan, P, rng),
+                          bfv.precompute_zero_rows(sk, rng, plan.k_dst)))
+            lay = plan.dst
+    return steps
+
+
+def he_forward_online(layers, cur, weights: dict, sk: bfv.SecretKey, params: RingParams, prepared: list,
+                      specs: dict | None = None) -> np.ndarray:
+    """The online phase of he_forward with the offline material of he_prepare:
+    convs, activation exchanges and repacks enqueued back to back on the
+    stream with no host synchronisation until the logits are read; the
+    client's noise-budget checks are deferred to one read at the end
+    (act2pc.check_deferred_budgets). `cur`: the uploaded input (a device
+    PackedTensor). Returns the decrypted logits mod p (equal to he_forward's)."""
+    import torch
+
+    P = params
+    seq, pool, _ = main_path(layers)
+    specs = specs if specs is not None else layer_specs(layers, weights)
+    residuals = torch.zeros(max(1, len(prepared)), dtype=torch.int64, device=device_of(cur))
+    k = 0
+    for l in seq:
+        if l.kind == "conv":
+            spec = specs[l.name]
+            buf = spec.__dict__.get("_out_buf")  # reused across inferences: the previous output is consumed
+            y = conv.conv_proposed(cur, spec, P, out=buf)
+            spec.__dict__["_out_buf"] = bfv.cts_rows(y.cts)
+            if l.stride > 1:  # subsampled by the client's repack below
+                y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
+            kind, plan, sess, zeros = prepared[k]
+            assert kind == "act" and plan.src == y.layout, "prepared material does not match the chain"
+            cur = act2pc.run_layer_activation(y, sess, sk, zeros, P, budget_into=(residuals, k))
+            k += 1
+        elif l.kind == "pool" and l is not pool:
+            pooled = conv.avg_pool(cur, l.f_w, P)
+            kind, plan, rs, zeros = prepared[k]
+            assert kind == "repack" and plan.src == pooled.layout, "prepared material does not match the chain"
+            cur = act2pc.run_repack_round(pooled, rs, sk, zeros, P, budget_into=(residuals, k))
+            k += 1
+    pooled = conv.avg_pool(cur, pool.f_w, P)
+    logits = conv.fully_connected(pooled, weights["fc"], P)
+    out = bfv.centered(conv.read_scalar_outputs(logits, sk), P.p) % P.p
+    act2pc.check_deferred_budgets(P, residuals[:k])
+    return out
+
+
+def device_of(x):
+    return bfv.cts_rows(x.cts).device
+
+
 def config_layers(name: str):
     return stacks.CONFIGS[name]()

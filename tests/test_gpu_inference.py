@@ -41,3 +41,44 @@ def test_chain_many_requests(name, reqs):
     got = inference.he_forward_many(layers, xs, weights, sk, rng, P)
     for x, g in zip(xs, got):
         assert np.array_equal(g, inference.plain_forward(layers, x, weights, P.p))
+
+
+@pytest.mark.parametrize("name", ["config3", "config5"])
+def test_chain_online_phase_matches(name):
+    """he_prepare (the offline phase up front) + he_forward_online (no host
+    synchronisation until the logits; budget checks deferred) equals the
+    integer model; a second inference prepares fresh material."""
+    from paper_2401_16732_b200 import bfv, conv, inference, params
+
+    P = params.default_params()
+    rng = np.random.default_rng(31 + len(name))
+    layers = inference.config_layers(name)
+    seq, pool, fc = inference.main_path(layers)
+    weights = inference.random_weights(layers, rng)
+    specs = inference.layer_specs(layers, weights)
+    sk = bfv.keygen(P, rng)
+    for _ in range(2):
+        x = rng.integers(0, 8, (seq[0].c_i, seq[0].H, seq[0].W), dtype=np.int64)
+        prepared = inference.he_prepare(layers, P, sk, rng)
+        cur = conv.pack_input(x, P, seq[0].f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
+        rows = bfv.cts_rows(cur.cts).contiguous()
+        cur = conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), cur.layout,
+                                cur.channels, cur.scale)
+        got = inference.he_forward_online(layers, cur, weights, sk, P, prepared, specs=specs)
+        assert np.array_equal(got, inference.plain_forward(layers, x, weights, P.p))
+
+
+def test_deferred_budget_check_raises():
+    """A stored residual above the budget makes the deferred check raise the
+    per-round check's ProtocolError."""
+    import torch
+
+    from paper_2401_16732_b200 import act2pc, params
+    from paper_2401_16732_b200.errors import ProtocolError
+
+    P = params.default_params()
+    ok = torch.tensor([1, 5, 3], dtype=torch.int64, device="cuda")
+    act2pc.check_deferred_budgets(P, ok)
+    bad = torch.tensor([1, P.q // (2 * P.p) * 4, 3], dtype=torch.int64, device="cuda")
+    with pytest.raises(ProtocolError):
+        act2pc.check_deferred_budgets(P, bad)

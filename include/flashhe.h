@@ -181,6 +181,14 @@ int fhe_decrypt_round(uint64_t q, uint64_t p, uint64_t delta, int R, int n,
  * (the reference checks each decryption, bfv.py:278-293). */
 int fhe_decrypt_round_max(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* u,
                           uint64_t* m_out, uint64_t* max_all, void* stream);
+/* bfv.decrypt over a batch in one launch (bfv.py:278-293, K6 fused): cts = DEVICE
+ * [k][2][n] ciphertexts mod q (eval = 0: COEFF domain, 1: EVAL domain), s_eval =
+ * DEVICE [n] secret key in EVAL order; writes m_out [k][n] = round(Δ^-1 [c1 s + c0]_q)
+ * mod p and folds every row's largest |residual| into *max_all (atomic max). The
+ * same values as fhe_ntt_forward + fhe_binary(mul, add) + fhe_ntt_inverse +
+ * fhe_decrypt_round_max, in one kernel (one CTA per ciphertext); n = 1024, 2048, 4096. */
+int fhe_decrypt_fused(const fhe_plan* plan, int k, int eval, const uint64_t* cts, const uint64_t* s_eval,
+                      uint64_t p, uint64_t delta, uint64_t* m_out, uint64_t* max_all, void* stream);
 
 /* ------------------------------------------ K1: Flash convolution core */
 /* Lazy DRot x CMult accumulation with one reduction per coefficient

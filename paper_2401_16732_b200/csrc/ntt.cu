@@ -644,6 +644,112 @@ __global__ void __launch_bounds__((1 << LOGN) >> LOGR) ntt_row_direct_kernel(con
   });
 }
 
+// K6 fused (the client's decryption of a batch, bfv.py:278-293): one CTA per
+// ciphertext computes [c1·s + c0]_q and rounds it to the message in one pass —
+// NTT(c1) (forward phases), · s in registers, the inverse phases (the forward
+// transform's last phase and the inverse's first share their register
+// positions, so no shared-memory trip between them), + c0, then round(u/Δ)
+// mod p with the residual folded into max_all. EVAL ciphertexts skip the
+// forward transform: (c1·s + c0) is formed in registers before the inverse.
+// Replaces the 7-launch chain (two column copies, NTT, ·s, iNTT, + c0, round)
+// with one launch; values are identical (every step is exact mod q).
+template <int LOGN, int LOGR, bool EVAL>
+__global__ void __launch_bounds__((1 << LOGN) >> LOGR) decrypt_fused_kernel(
+    const NttDesc d, const uint64_t* __restrict__ cts, const uint64_t* __restrict__ s_eval, uint64_t p,
+    uint64_t delta, uint64_t magic, uint64_t* __restrict__ mout, unsigned long long* __restrict__ max_all) {
+  extern __shared__ uint64_t sm[];
+  constexpr int n = 1 << LOGN, E = 1 << LOGR;
+  constexpr int NPH = RowPhase<LOGN, LOGR, false, 0>::count;
+  const int row = blockIdx.x, item = threadIdx.x;
+  const uint64_t* c0 = cts + (size_t)row * 2 * n;
+  const uint64_t* c1 = c0 + n;
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  uint64_t e[E];
+  if constexpr (!EVAL) {
+    static_for<0, NPH>([&](auto kc) {  // forward transform of c1
+      constexpr int K = decltype(kc)::value;
+      using Ph = RowPhase<LOGN, LOGR, false, K>;
+      constexpr int TL = Ph::TL;
+      const int B = ((item >> TL) << (TL + LOGR)) + (item & ((1 << TL) - 1));
+      if constexpr (K == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) e[i] = c1[B + (i << TL)];
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) e[i] = sm[spad(B) + (i << TL) + ((i << TL) >> 4)];
+      }
+      phase_math<LOGR, Ph::R, false, TL>(e, d, (uint32_t)(n + B), false);
+      if constexpr (K < NPH - 1) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) sm[spad(B) + (i << TL) + ((i << TL) >> 4)] = e[i];
+        __syncthreads();
+      }
+    });
+  }
+  // the forward's last phase positions = the inverse's first: · s (+ c0 for EVAL input)
+  {
+    using Ph = RowPhase<LOGN, LOGR, true, 0>;
+    constexpr int TL = Ph::TL;
+    const int B = ((item >> TL) << (TL + LOGR)) + (item & ((1 << TL) - 1));
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int pos = B + (i << TL);
+      uint64_t x;
+      if constexpr (EVAL) {
+        x = c1[pos];
+      } else {
+        x = e[i] >= q2 ? e[i] - q2 : e[i];
+        x = csub(x, q);
+      }
+      x = mulmod(x, s_eval[pos], d.m);
+      if constexpr (EVAL) x = csub(x + c0[pos], q);
+      e[i] = x;
+    }
+  }
+  uint64_t local = 0;
+  static_for<0, NPH>([&](auto kc) {  // inverse transform, then + c0 and the rounding
+    constexpr int K = decltype(kc)::value;
+    using Ph = RowPhase<LOGN, LOGR, true, K>;
+    constexpr int TL = Ph::TL;
+    const int B = ((item >> TL) << (TL + LOGR)) + (item & ((1 << TL) - 1));
+    if constexpr (K > 0) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) e[i] = sm[spad(B) + (i << TL) + ((i << TL) >> 4)];
+    }
+    phase_math<LOGR, Ph::R, true, TL>(e, d, (uint32_t)(n + B), Ph::S == 0);
+    if constexpr (K < NPH - 1) {
+      // (a thread stores exactly the positions it loaded for this phase: no barrier before)
+#pragma unroll
+      for (int i = 0; i < E; ++i) sm[spad(B) + (i << TL) + ((i << TL) >> 4)] = e[i];
+      __syncthreads();
+    } else {
+      const uint64_t half = delta / 2;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int pos = B + (i << TL);
+        uint64_t u = csub(e[i], q);
+        if constexpr (!EVAL) u = csub(u + c0[pos], q);
+        const uint64_t x = u + half;  // (u + Δ//2) // Δ  (bfv.py:288)
+        uint64_t mq = __umul64hi(x, magic);
+        uint64_t rem = x - mq * delta;
+        if (rem >= delta) {
+          ++mq;
+          rem -= delta;
+        }
+        const uint64_t aw = rem >= half ? rem - half : half - rem;  // |u - Δ m_raw|
+        local = aw > local ? aw : local;
+        while (mq >= p) mq -= p;
+        mout[(size_t)row * n + pos] = mq;
+      }
+    }
+  });
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t v = __shfl_xor_sync(0xffffffffu, local, o);
+    local = v > local ? v : local;
+  }
+  if ((item & 31) == 0) atomicMax(max_all, (unsigned long long)local);
+}
+
 static bool row_direct_enabled() {  // FHE_NTT_ROW_DIRECT=0 selects the staged row kernel (A/B checks)
   static int v = -1;
   if (v < 0) {
@@ -810,6 +916,39 @@ int fhe_ntt_inverse(const fhe_plan* const* plans, int L, int B, int P, const uin
   if (!src || !dst) return fail(FHE_ERR_VALUE, "null NTT buffer");
   LoadMap lm{src, P, 0, 0, 0, ~0ull};
   return launch<true>(ls, lm, dst, B * L * P, n, (cudaStream_t)stream);
+}
+
+int fhe_decrypt_fused(const fhe_plan* plan, int k, int eval, const uint64_t* cts, const uint64_t* s_eval,
+                      uint64_t p, uint64_t delta, uint64_t* m_out, uint64_t* max_all, void* stream) {
+  if (!plan || !cts || !s_eval || !m_out || !max_all) return fail(FHE_ERR_VALUE, "null decrypt operand");
+  if (k < 0 || delta < 2 || p < 2) return fail(FHE_ERR_VALUE, "bad decrypt arguments");
+  if (plan->desc.m.q >= (1ull << 62)) return fail(FHE_ERR_PARAMETER, "modulus too large");
+  if (!k) return FHE_OK;
+  const uint64_t magic = ~0ull / delta;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* mx = reinterpret_cast<unsigned long long*>(max_all);
+#define FHE_DECRYPT_N(LOGN)                                                                                    \
+  case (1 << LOGN): {                                                                                        \
+    constexpr int LOGR = 3;                                                                                  \
+    const size_t smem = (size_t)((1 << LOGN) + ((1 << LOGN) >> 4) + 1) * sizeof(uint64_t);                   \
+    if (eval)                                                                                                \
+      decrypt_fused_kernel<LOGN, LOGR, true><<<k, (1 << LOGN) >> LOGR, smem, st>>>(plan->desc, cts, s_eval, p, \
+                                                                                  delta, magic, m_out, mx);  \
+    else                                                                                                     \
+      decrypt_fused_kernel<LOGN, LOGR, false><<<k, (1 << LOGN) >> LOGR, smem, st>>>(plan->desc, cts, s_eval, \
+                                                                                   p, delta, magic, m_out, mx); \
+    break;                                                                                                   \
+  }
+  switch (plan->n) {
+    FHE_DECRYPT_N(10)
+    FHE_DECRYPT_N(11)
+    FHE_DECRYPT_N(12)
+    default:
+      return fail(FHE_ERR_PARAMETER, "fused decryption supports n = 1024, 2048, 4096 (got %d)", plan->n);
+  }
+#undef FHE_DECRYPT_N
+  FHE_CHECK_LAUNCH("decrypt_fused_kernel");
+  return FHE_OK;
 }
 
 int fhe_ntt_forward_digits(const fhe_plan* const* plans, int L, int B, const uint64_t* src,

@@ -243,3 +243,32 @@ def test_keyswitch_multi_equals_per_step(N, L, B, ndig, S):
     torch.cuda.synchronize()
     for s in range(S):
         assert torch.equal(got[s], want[s]), f"step {s} (gpow {gp[s]}) differs"
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+@pytest.mark.parametrize("domain", ["coeff", "eval"])
+def test_decrypt_fused_matches_chain(n, domain, monkeypatch):
+    """fhe_decrypt_fused (one launch: NTT, ·s, iNTT, + c0, round) equals the
+    launch chain it replaces — messages and the folded residual maximum — on
+    fresh encryptions and on arbitrary (over-noisy) rows."""
+    import torch
+
+    from paper_2401_16732_b200 import bfv, params
+    from paper_2401_16732_b200.ring import Domain
+
+    P = params.make_params(n)
+    rng = np.random.default_rng(n + len(domain))
+    sk = bfv.keygen(P, rng)
+    fresh = bfv.precompute_zero_rows(sk, rng, 5).rows.reshape(-1, 2, n)  # encryptions of zero (COEFF)
+    noise = torch.from_numpy(rng.integers(0, P.q, (7, 2, n), dtype=np.int64)).cuda()
+    rows = torch.cat([fresh, noise])
+    dom = Domain.EVAL if domain == "eval" else Domain.COEFF
+    cts = bfv.cts_from_rows(rows.contiguous(), P.q, bfv.Encoding.DIRECT, dom)
+    res = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("FLASHHE_DECRYPT_FUSED", fused)
+        acc = bfv.MaxAcc()
+        m = bfv.decrypt_rows_max(cts, sk, acc)
+        res[fused] = (m.cpu().numpy(), acc.value())
+    assert np.array_equal(res["1"][0], res["0"][0])
+    assert res["1"][1] == res["0"][1]

@@ -306,6 +306,9 @@ int fhe_keyswitch_multi(const uint64_t* moduli, int L, int B, int n, const uint6
 int fhe_gather_rows(const uint64_t* const* srcs, int k, int n, uint64_t* dst, void* stream);
 int fhe_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
                 void* stream);
+/* count (<= 8) DEVICE-to-DEVICE copies of bytes[i] (multiples of 8, 8-byte aligned) in
+ * one kernel launch (srcs / dsts / bytes: HOST arrays). */
+int fhe_copy_many(int count, const void* const* srcs, void* const* dsts, const size_t* bytes, void* stream);
 int fhe_zero(void* dst, size_t bytes, void* stream);
 
 /* Fused PMult-accumulate of the conventional convolution (conv.py:457-564:

@@ -15,6 +15,7 @@ Algebra (frac bits f; the paper's protocol is f = 0):
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -448,13 +449,21 @@ class _LayerGraph:
         torch.cuda.current_stream().wait_stream(side)
 
     def run(self, conv_rows: torch.Tensor, session: "LayerSession", sk: bfv.SecretKey, zero_rows: torch.Tensor):
-        self.inp.copy_(conv_rows)
-        self.zeros.copy_(zero_rows)
-        self.r.copy_(session.r)
-        self.two_r.copy_(session.two_r_eval)
-        self.v_eval.copy_(session.v_eval)
-        self.const.copy_(session.const)
-        self.s_eval.copy_(sk.s_eval_dev())
+        # the replay's operands into the static buffers: seven copies, one launch (fhe_copy_many)
+        pairs = ((conv_rows, self.inp), (zero_rows, self.zeros), (session.r, self.r),
+                 (session.two_r_eval, self.two_r), (session.v_eval, self.v_eval), (session.const, self.const),
+                 (sk.s_eval_dev(), self.s_eval))
+        srcs = (ctypes.c_void_p * 7)()
+        dsts = (ctypes.c_void_p * 7)()
+        nbytes = (ctypes.c_size_t * 7)()
+        keep = []
+        for i, (src, dst) in enumerate(pairs):
+            src = src.contiguous()
+            keep.append(src)
+            if src.numel() != dst.numel():
+                raise EncodingError("exchange operand does not match the layer graph")
+            srcs[i], dsts[i], nbytes[i] = src.data_ptr(), dst.data_ptr(), dst.numel() * 8
+        _native.call("fhe_copy_many", 7, srcs, dsts, nbytes, device.stream())
         self.graph.replay()
         return self.out.clone(), self.acc
 

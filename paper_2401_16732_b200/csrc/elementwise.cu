@@ -331,6 +331,26 @@ __global__ void decrypt_round_kernel(uint64_t p, uint64_t delta, uint64_t magic,
 }
 
 // ------------------------------------------------------- row plumbing
+constexpr int kCopyMany = 8;
+struct CopyTable {
+  const uint64_t* src[kCopyMany];
+  uint64_t* dst[kCopyMany];
+  unsigned long long start[kCopyMany + 1];  // word offsets of each copy in the concatenation
+  int count;
+};
+
+// grid-stride over the concatenated words of all copies; the copy of word w is
+// found by a short scan of the (<= 8) start offsets
+__global__ void copy_many_kernel(const CopyTable t) {
+  const unsigned long long total = t.start[t.count];
+  for (unsigned long long w = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; w < total;
+       w += (unsigned long long)gridDim.x * blockDim.x) {
+    int c = 0;
+    while (w >= t.start[c + 1]) ++c;
+    const unsigned long long i = w - t.start[c];
+    t.dst[c][i] = t.src[c][i];
+  }
+}
 // Gather k device rows of n words (arbitrary addresses) into one contiguous
 // stack: the list form of a ciphertext batch (bfv.cts_rows of separate
 // Ciphertext objects) becomes one [k][n] operand without a torch kernel.
@@ -1200,6 +1220,33 @@ int fhe_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t
   if (!dst || !src) return fail(FHE_ERR_VALUE, "null copy operand");
   FHE_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToDevice,
                              (cudaStream_t)stream));
+  return FHE_OK;
+}
+
+int fhe_copy_many(int count, const void* const* srcs, void* const* dsts, const size_t* bytes, void* stream) {
+  // several device-to-device copies (8-byte multiples, 8-byte aligned) in ONE launch: the
+  // act2pc layer graph's operand refill (seven buffers) costs one kernel instead of seven
+  // memcpy nodes
+  if (count < 0 || count > fhe::kCopyMany) return fail(FHE_ERR_VALUE, "copy count %d out of range", count);
+  if (!count) return FHE_OK;
+  if (!srcs || !dsts || !bytes) return fail(FHE_ERR_VALUE, "null copy table");
+  fhe::CopyTable t{};
+  t.count = count;
+  unsigned long long total = 0;
+  for (int i = 0; i < count; ++i) {
+    if (bytes[i] % 8 || ((uintptr_t)srcs[i] | (uintptr_t)dsts[i]) % 8) return fail(FHE_ERR_VALUE, "unaligned copy %d", i);
+    if (bytes[i] && (!srcs[i] || !dsts[i])) return fail(FHE_ERR_VALUE, "null copy operand %d", i);
+    t.src[i] = static_cast<const uint64_t*>(srcs[i]);
+    t.dst[i] = static_cast<uint64_t*>(dsts[i]);
+    t.start[i] = total;
+    total += bytes[i] / 8;
+  }
+  t.start[count] = total;
+  if (!total) return FHE_OK;
+  const int threads = 256;
+  const unsigned long long blocks = std::min<unsigned long long>((total + threads - 1) / threads, 148ull * 16);
+  fhe::copy_many_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(t);
+  FHE_CHECK_LAUNCH("copy_many_kernel");
   return FHE_OK;
 }
 

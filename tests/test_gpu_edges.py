@@ -80,3 +80,26 @@ def test_act2pc_layer_single_channel():
     out = act2pc.run_layer_activation(x, act2pc.offline_prepare_layer(plan, P, rng), sk,
                                       bfv.precompute_zero_rows(sk, rng, 3), P)
     assert np.array_equal(conv.unpack(out, sk), bfv.centered(a * a + a, P.p))
+
+
+def test_copy_many_kernel():
+    """fhe_copy_many: several device copies of different sizes in one launch."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2401_16732_b200 import _native, device
+
+    rng = np.random.default_rng(3)
+    sizes = [1, 7, 4096, 0, 33, 100000]
+    srcs = [torch.from_numpy(rng.integers(-2**62, 2**62, max(s, 1), dtype=np.int64)).cuda() for s in sizes]
+    dsts = [torch.zeros(max(s, 1), dtype=torch.int64, device="cuda") for s in sizes]
+    a = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in srcs])
+    b = (ctypes.c_void_p * 6)(*[t.data_ptr() for t in dsts])
+    c = (ctypes.c_size_t * 6)(*[8 * s for s in sizes])
+    _native.call("fhe_copy_many", 6, a, b, c, device.stream())
+    for s, x, y in zip(sizes, srcs, dsts):
+        assert torch.equal(x[:s], y[:s])
+        if s == 0:
+            assert int(y[0]) == 0

@@ -577,11 +577,12 @@ struct RowPhase {
 // 1) and the last phase's results stored straight from registers: two
 // shared-memory passes and two barriers fewer than staging the row through
 // shared memory at both ends. n = 2048: 3 phases, 2 shared-memory exchanges.
-#ifndef FHE_NTT_MINB
-#define FHE_NTT_MINB 4  // min resident CTAs per SM of the row kernels: 64 registers (fused decryption of 5120 rows 254 -> 228 us)
-#endif
+// Row kernels: enough resident CTAs per SM for 1024 threads, i.e. a 64-register cap
+// (n = 2048: 4 CTAs; fused decryption of 5120 rows 254 -> 228 us, row NTT unchanged)
+// (radix 16 keeps 16 values per thread: half the CTAs, a 128-register cap)
+#define FHE_ROW_MINB(T, LOGR) ((LOGR) >= 4 ? ((T) < 512 ? 512 / (T) : 1) : ((T) < 1024 ? 1024 / (T) : 1))
 template <bool INV, int LOGN, int LOGR>
-__global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_NTT_MINB) ntt_row_direct_kernel(const LimbSet ls, const LoadMap lm,
+__global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_ROW_MINB((1 << LOGN) >> LOGR, LOGR)) ntt_row_direct_kernel(const LimbSet ls, const LoadMap lm,
                                                                           uint64_t* __restrict__ dst) {
   extern __shared__ uint64_t sm[];
   constexpr int n = 1 << LOGN, E = 1 << LOGR;
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_NTT_MINB) ntt_row_dir
 // Replaces the 7-launch chain (two column copies, NTT, ·s, iNTT, + c0, round)
 // with one launch; values are identical (every step is exact mod q).
 template <int LOGN, int LOGR, bool EVAL>
-__global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_NTT_MINB) decrypt_fused_kernel(
+__global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_ROW_MINB((1 << LOGN) >> LOGR, LOGR)) decrypt_fused_kernel(
     const NttDesc d, const uint64_t* __restrict__ cts, const uint64_t* __restrict__ s_eval, uint64_t p,
     uint64_t delta, uint64_t magic, uint64_t* __restrict__ mout, unsigned long long* __restrict__ max_all) {
   extern __shared__ uint64_t sm[];

@@ -425,7 +425,11 @@ class _LayerGraph:
             _native.call("fhe_zero", pending.t.data_ptr(), 8, device.stream())
             m1 = _encrypt_rows(self.inp, self.r, params)
             w = _decrypt_rows_checked(m1, Domain.COEFF, key, pending)
-            ct_sq = _encrypt_rows(self.zeros[:kd], _gather(plan.idx, w), params, square=True, f=f)
+            # the repack gather fused into the encryption of the squares (fhe_act_encrypt_gather)
+            ct_sq = torch.empty((kd, 2, n), dtype=torch.int64, device=dev)
+            _native.call("fhe_act_encrypt_gather", params.q, params.p, params.delta, f, 1, kd, n,
+                         self.zeros.data_ptr(), w.contiguous().data_ptr(), plan.idx.data_ptr(), ct_sq.data_ptr(),
+                         device.stream())
             ct_w = _encrypt_rows(self.zeros[kd : 2 * kd], _batch_coeffs(_gather(plan.idx_eval, w), params), params)
             w_eval = ring.ntt_rows(ct_w.reshape(-1, n), n, [params.q])
             m2 = torch.empty_like(ct_w)
@@ -433,10 +437,12 @@ class _LayerGraph:
                          self.v_eval.data_ptr(), m2.data_ptr(), device.stream())
             mm = _decrypt_rows_checked(m2, Domain.EVAL, key, pending)
             evals = ring.ntt_rows(mm, n, [params.p])
-            back = _encrypt_rows(self.zeros[2 * kd :], evals, params, perm=plan.slot)
+            # the client's re-encryption of the round-2 values and the server's finalisation
+            # in one pass (fhe_act_encrypt_finalize: no intermediate ciphertexts)
             out = torch.empty_like(ct_sq)
-            _native.call("fhe_act_finalize", params.q, params.p, params.delta, kd, n, ct_sq.data_ptr(),
-                         back.data_ptr(), self.const.data_ptr(), out.data_ptr(), device.stream())
+            _native.call("fhe_act_encrypt_finalize", params.q, params.p, params.delta, kd, n, ct_sq.data_ptr(),
+                         self.zeros[2 * kd :].data_ptr(), evals.contiguous().data_ptr(), plan.slot.data_ptr(),
+                         self.const.data_ptr(), out.data_ptr(), device.stream())
             return out
 
         body()  # plans, tables and kernels initialised outside the capture

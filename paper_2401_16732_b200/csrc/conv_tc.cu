@@ -23,20 +23,26 @@
 //
 // One cooperative persistent launch (one CTA per SM) runs a whole STACK of
 // independent conv layers (one layer for conv_proposed; a network's layers or
-// many requests for the serving path). Per layer:
-//  phase 1  relayout: every warp grabs (32 positions x 16 channels) units from
-//           a per-layer work counter and writes the digit-plane operand X
-//           (two X buffers alternate between layers);
-//  barrier  one grid-wide arrival (the X of this layer is complete);
-//  phase 2  warp-specialised GEMM over the layer's tiles:
-//             warp 0     MMA issue (one thread: tcgen05.mma, tcgen05.commit)
-//             warp 1     stage loads (one thread: two cp.async.bulk per stage)
-//             warps 2-9  epilogue: tcgen05.ld, in-thread recombination, one
-//                        canonical reduction mod q (+ fused bias), row stores
-//           with an NST-deep stage ring and two TMEM accumulator buffers.
-// A warp moves on to the next layer's relayout as soon as its own role in
-// this layer is done, so relayout work fills the SMs that finish early (the
-// GEMM's wave-quantisation tail) and no per-layer launch gap remains.
+// many requests for the serving path):
+//  relayout  warps 10-13 (and, for layer 0, the epilogue warps) stream through
+//            the layers in order, each taking (32 positions x 16 channels)
+//            units round-robin and writing that layer's own digit-plane
+//            region of X; the CTA's last warp publishes one per-layer count
+//            (release fences: generic -> async proxy, then gpu scope);
+//  GEMM      per layer, once its X count reaches the grid size:
+//             warp 1     the loader: grabs the CTA's tiles from a per-layer
+//                        counter (dynamic scheduling; the launch's last grab
+//                        resets it), publishes the tile sequence in a
+//                        shared-memory ring, and fills the stage ring with
+//                        cp.async.bulk (window + weights, or the window only
+//                        when the layer's weights are resident);
+//             warp 0     MMA issue (elect.sync: tcgen05.mma kind::i8, commits);
+//             warps 2-9  epilogue: tcgen05.ld, in-thread recombination of the
+//                        eight byte planes, one canonical reduction mod q
+//                        (pseudo-Mersenne or Shoup; + fused bias), row stores;
+//            two TMEM accumulator buffers (a 64-position tile uses both).
+// Roles move on to the next layer as soon as their part of this one is done:
+// relayout runs ahead of the GEMM and no per-layer launch gap remains.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>

@@ -246,7 +246,7 @@ def stack_clock_mhz(layers):
 
     from paper_2401_16732_b200 import _native, conv
 
-    buf = torch.zeros(9 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(25 * 4096, dtype=torch.int64, device="cuda")  # (the trace area fhe_debug_trace needs)
     _native.call("fhe_debug_trace", buf.data_ptr())
     try:
         conv.issue_k1([(L["plan"], L["dev"], None, L["out"]) for L in layers])

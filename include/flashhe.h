@@ -57,7 +57,9 @@ uint64_t fhe_launch_count(void);
  * (external event node); used by the benchmark's kernel-level timing. */
 int fhe_record_event(void* event, void* stream);
 /* Timeline instrumentation of the K1-TC pipeline: CTA 0 records clock64() at
- * its pipeline events into dev_buf (8 kinds x 4096 uint64); NULL disables. */
+ * its pipeline events into dev_buf, which must hold 25 x 4096 uint64 (kinds 0-7:
+ * pipeline events, 7 also the tile sequence; 8: per-CTA start/end and relayout
+ * completion times; 9-24: per-epilogue-warp events); NULL disables. */
 int fhe_debug_trace(void* dev_buf);
 
 /* Roofline micro-benchmarks (register-resident, no memory traffic):

@@ -30,7 +30,7 @@ def main():
     inp = torch.from_numpy(rng.integers(0, P.q, (lay.ct_count(l.c_i), 2, P.n))).cuda()
     out = torch.empty((plan.n_out, 2, P.n), dtype=torch.int64, device="cuda")
     plan.run(inp, out)
-    buf = torch.zeros(8 * 4096, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(25 * 4096, dtype=torch.int64, device="cuda")  # (the trace area fhe_debug_trace needs)
     _native.call("fhe_debug_trace", buf.data_ptr())
     plan.run(inp, out)
     torch.cuda.synchronize()

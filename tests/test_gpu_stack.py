@@ -120,3 +120,25 @@ def test_two_stacks_beyond_24_layers():
         assert len(set(map(id, ev))) == 2
         torch.cuda.synchronize()
         _compare(layers, refs, f"split launch {rep}")
+
+
+def test_sync_buffer_shared_by_different_stacks():
+    """Dynamic tile counters: the last grab of a launch resets each layer's
+    counter, so ONE counter buffer can serve stacks with different per-layer
+    tile counts in turn (config 4's layers, then config 3's, then config 4's
+    again) and every output still equals the single-layer launches."""
+    from paper_2401_16732_b200 import conv, device
+
+    sync = device.zeros_i64(conv.SYNC_WORDS)
+    stacks = []
+    for w, seed in (("config4", 61), ("config3", 62)):
+        P, layers = bench.build_stack(w, seed=seed)
+        layers = layers[:12]
+        refs = [L["plan"].run(L["dev"], torch.empty_like(L["out"])) for L in layers]
+        stacks.append((layers, refs))
+    for layers, refs in (stacks[0], stacks[1], stacks[0], stacks[1]):
+        for L in layers:
+            L["out"].fill_(-1)
+        conv.run_tc_stack([(L["plan"].tc, L["dev"], L["out"]) for L in layers], sync=sync)
+        torch.cuda.synchronize()
+        _compare(layers, refs, "shared counter buffer")

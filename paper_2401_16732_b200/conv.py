@@ -675,7 +675,7 @@ def conv_proposed_many(xs, layer: ConvLayerSpec, params: RingParams, outs=None) 
     xs = list(xs)
     if not xs:
         return []
-    items, plans = [], []
+    items = []
     for i, x in enumerate(xs):
         plan = _proposed_plan(x, layer, params)
         out = outs[i] if outs is not None else None
@@ -686,7 +686,6 @@ def conv_proposed_many(xs, layer: ConvLayerSpec, params: RingParams, outs=None) 
         if out is None:
             out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=inp.device)
         items.append((plan, inp, None, out))
-        plans.append(plan)
     issue_k1(items)
     return [PackedTensor(bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF), _out_layout(x.layout),
                          layer.c_o, x.scale + layer.weight_scale) for x, (_, _, _, out) in zip(xs, items)]

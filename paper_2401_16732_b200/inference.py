@@ -18,7 +18,8 @@ from dataclasses import replace
 
 import numpy as np
 
-from . import act2pc, bfv, conv, stacks
+from . import act2pc, bfv, conv, device, stacks
+from .errors import EncodingError
 from .params import RingParams
 
 
@@ -289,7 +290,7 @@ def he_forward_online(layers, cur, weights: dict, sk: bfv.SecretKey, params: Rin
     P = params
     seq, pool, _ = main_path(layers)
     specs = specs if specs is not None else layer_specs(layers, weights)
-    residuals = torch.zeros(max(1, len(prepared)), dtype=torch.int64, device=device_of(cur))
+    residuals = device.zeros_i64(max(1, len(prepared)))  # (cudaMemsetAsync, no fill kernel)
     k = 0
     for l in seq:
         if l.kind == "conv":
@@ -300,13 +301,15 @@ def he_forward_online(layers, cur, weights: dict, sk: bfv.SecretKey, params: Rin
             if l.stride > 1:  # subsampled by the client's repack below
                 y = conv.PackedTensor(y.cts, replace(y.layout, stride=l.stride), y.channels, y.scale)
             kind, plan, sess, zeros = prepared[k]
-            assert kind == "act" and plan.src == y.layout, "prepared material does not match the chain"
+            if kind != "act" or plan.src != y.layout:
+                raise EncodingError("prepared material does not match the chain (he_prepare for these layers)")
             cur = act2pc.run_layer_activation(y, sess, sk, zeros, P, budget_into=(residuals, k))
             k += 1
         elif l.kind == "pool" and l is not pool:
             pooled = conv.avg_pool(cur, l.f_w, P)
             kind, plan, rs, zeros = prepared[k]
-            assert kind == "repack" and plan.src == pooled.layout, "prepared material does not match the chain"
+            if kind != "repack" or plan.src != pooled.layout:
+                raise EncodingError("prepared material does not match the chain (he_prepare for these layers)")
             cur = act2pc.run_repack_round(pooled, rs, sk, zeros, P, budget_into=(residuals, k))
             k += 1
     pooled = conv.avg_pool(cur, pool.f_w, P)
@@ -314,10 +317,6 @@ def he_forward_online(layers, cur, weights: dict, sk: bfv.SecretKey, params: Rin
     out = bfv.centered(conv.read_scalar_outputs(logits, sk), P.p) % P.p
     act2pc.check_deferred_budgets(P, residuals[:k])
     return out
-
-
-def device_of(x):
-    return bfv.cts_rows(x.cts).device
 
 
 def config_layers(name: str):

@@ -285,8 +285,6 @@ def he_forward_online(layers, cur, weights: dict, sk: bfv.SecretKey, params: Rin
     client's noise-budget checks are deferred to one read at the end
     (act2pc.check_deferred_budgets). `cur`: the uploaded input (a device
     PackedTensor). Returns the decrypted logits mod p (equal to he_forward's)."""
-    import torch
-
     P = params
     seq, pool, _ = main_path(layers)
     specs = specs if specs is not None else layer_specs(layers, weights)

@@ -383,17 +383,12 @@ int fhe_ct_pmult_add(uint64_t q, int R, int n, const uint64_t* ct, const uint64_
  * constant c = r^2 - r*2^f + v (fhe_act_server_const), [R][n] mod p. */
 int fhe_act_finalize(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* a,
                      const uint64_t* b, const uint64_t* c, uint64_t* out, void* stream);
-/* Fused forms of the layer exchange (same values, fewer launches):
+/* Fused form of the client's repack + encryption (same values, one launch):
  * fhe_act_encrypt_gather = fhe_act_gather(gidx) + fhe_act_encrypt_rows (the message of
- *   element i is m[gidx[i]], gidx DEVICE int32 [R][n]);
- * fhe_act_encrypt_finalize = fhe_act_encrypt_rows(zero, m, perm) into b + fhe_act_finalize(a, b, c). */
+ *   element i is m[gidx[i]], gidx DEVICE int32 [R][n]). */
 int fhe_act_encrypt_gather(uint64_t q, uint64_t p, uint64_t delta, int f, int square, int R, int n,
                            const uint64_t* zero, const uint64_t* m, const int32_t* gidx, uint64_t* out,
                            void* stream);
-int fhe_act_encrypt_finalize(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* a,
-                             const uint64_t* zero, const uint64_t* m, const int32_t* perm, const uint64_t* c,
-                             uint64_t* out, void* stream);
-
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -96,7 +96,6 @@ SIGNATURES = {
     "fhe_ct_pmult_add": (_int, [_u64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "fhe_act_finalize": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "fhe_act_encrypt_gather": (_int, [_u64, _u64, _u64, _int, _int, _int, _int, _vp, _vp, _vp, _vp, _vp]),
-    "fhe_act_encrypt_finalize": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

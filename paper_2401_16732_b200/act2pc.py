@@ -437,12 +437,11 @@ class _LayerGraph:
                          self.v_eval.data_ptr(), m2.data_ptr(), device.stream())
             mm = _decrypt_rows_checked(m2, Domain.EVAL, key, pending)
             evals = ring.ntt_rows(mm, n, [params.p])
-            # the client's re-encryption of the round-2 values and the server's finalisation
-            # in one pass (fhe_act_encrypt_finalize: no intermediate ciphertexts)
+            # the client's round-2 message is materialised (it crosses to the server)
+            back = _encrypt_rows(self.zeros[2 * kd :], evals, params, perm=plan.slot)
             out = torch.empty_like(ct_sq)
-            _native.call("fhe_act_encrypt_finalize", params.q, params.p, params.delta, kd, n, ct_sq.data_ptr(),
-                         self.zeros[2 * kd :].data_ptr(), evals.contiguous().data_ptr(), plan.slot.data_ptr(),
-                         self.const.data_ptr(), out.data_ptr(), device.stream())
+            _native.call("fhe_act_finalize", params.q, params.p, params.delta, kd, n, ct_sq.data_ptr(),
+                         back.data_ptr(), self.const.data_ptr(), out.data_ptr(), device.stream())
             return out
 
         body()  # plans, tables and kernels initialised outside the capture

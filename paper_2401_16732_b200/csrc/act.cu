@@ -101,27 +101,6 @@ __global__ void act_encrypt_gather_kernel(ModDesc mq, ModDesc mp, uint64_t delta
   out[base + n + s] = zero[base + n + s];
 }
 
-// act_encrypt_kernel (b = Enc(m[perm]) from a zero ciphertext) followed by
-// act_finalize_kernel (a − b + Δ c) in one pass: the client's re-encryption
-// of the second round and the server's finalisation without the b buffer
-__global__ void act_encrypt_finalize_kernel(ModDesc mq, ModDesc mp, uint64_t delta, int logn,
-                                            const uint64_t* __restrict__ a, const uint64_t* __restrict__ zero,
-                                            const uint64_t* __restrict__ m, const int32_t* __restrict__ perm,
-                                            const uint64_t* __restrict__ c, uint64_t* __restrict__ out,
-                                            int64_t total) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int64_t r = i >> logn;
-  const int n = 1 << logn, s = (int)(i & (n - 1));
-  const int64_t base = r << (logn + 1);
-  const uint64_t q = mq.q;
-  const uint64_t v = reduce_u64(m[(r << logn) + (perm ? perm[s] : s)], mp);
-  const uint64_t b0 = csub(zero[base + s] + delta * v, q);
-  const uint64_t d0 = csub(a[base + s] + q - b0, q);
-  out[base + s] = csub(d0 + delta * reduce_u64(c[i], mp), q);
-  out[base + n + s] = csub(a[base + n + s] + q - zero[base + n + s], q);
-}
-
 }  // namespace fhe
 
 using namespace fhe;
@@ -177,22 +156,6 @@ int fhe_act_encrypt_gather(uint64_t q, uint64_t p, uint64_t delta, int f, int sq
   act_encrypt_gather_kernel<<<act_grid(total), kActThreads, 0, (cudaStream_t)stream>>>(
       mq.m[0], mp.m[0], delta, h_powmod(2, (uint64_t)f, p), square, logn, zero, m, gidx, out, total);
   FHE_CHECK_LAUNCH("act_encrypt_gather_kernel");
-  return FHE_OK;
-}
-
-int fhe_act_encrypt_finalize(uint64_t q, uint64_t p, uint64_t delta, int R, int n, const uint64_t* a,
-                             const uint64_t* zero, const uint64_t* m, const int32_t* perm, const uint64_t* c,
-                             uint64_t* out, void* stream) {
-  ModSet mq, mp;
-  if (int rc = act_moduli(q, p, delta, &mq, &mp)) return rc;
-  const int logn = act_logn(n);
-  if (logn < 0 || R < 0) return fail(FHE_ERR_VALUE, "bad row geometry (R=%d n=%d)", R, n);
-  if (!R) return FHE_OK;
-  if (!a || !zero || !m || !c || !out) return fail(FHE_ERR_VALUE, "null finalize pointer");
-  const int64_t total = (int64_t)R << logn;
-  act_encrypt_finalize_kernel<<<act_grid(total), kActThreads, 0, (cudaStream_t)stream>>>(
-      mq.m[0], mp.m[0], delta, logn, a, zero, m, perm, c, out, total);
-  FHE_CHECK_LAUNCH("act_encrypt_finalize_kernel");
   return FHE_OK;
 }
 

@@ -817,6 +817,28 @@ def main():
             evs[i + 1].record()
         torch.cuda.synchronize()
         layer_ms += [evs[i].elapsed_time(evs[i + 1]) / 3 for i in range(len(layers))]
+    # the same single-layer launches replayed from a CUDA graph each (no host issue, no
+    # gap between launches): the device time of the drop-in path per layer
+    layer_graph_ms = []
+    for L in layers:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            L["plan"].run(L["dev"], L["out"])
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(5):
+                L["plan"].run(L["dev"], L["out"])
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        layer_graph_ms.append(e0.elapsed_time(e1) / 5)
+        del g
     # the timed step: one CUDA-graph replay of every layer's launches
     launches0 = _native.launch_count()
     if args.no_graph:
@@ -912,6 +934,11 @@ def main():
             "clocks": clocks,
             "peaks_measured": {k: v for k, v in peaks.items()},
             "per_layer_ms_eager": {L["layer"].name: round(float(m), 4) for L, m in zip(layers, layer_ms)},
+            "per_layer_ms_graph": {L["layer"].name: round(float(m), 4) for L, m in zip(layers, layer_graph_ms)},
+            "drop_in_sum_ms": {"eager": round(float(sum(layer_ms)), 3), "graph": round(float(sum(layer_graph_ms)), 3),
+                               "note": "the layers as single-layer drop-in launches (conv_proposed's path) back to "
+                                       "back (eager: events between launches; graph: each layer's launches "
+                                       "replayed from a CUDA graph, no host issue) against ms_per_step"},
             "timing": ("value: CUDA-graph replay of the whole stack per step" if not args.no_graph
                        else "value: eager launches") + "; layers are independent inputs: the 20 tensor-core layers "
                       "run as one stacked persistent launch (conv.issue_k1)",

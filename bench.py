@@ -518,10 +518,7 @@ def inference_chain(name):
         rng = np.random.default_rng(95 + it)
         x = rng.integers(0, 8, (convs[0].c_i, convs[0].H, convs[0].W), dtype=np.int64)
         prepared = inference.he_prepare(layers, P, sk, rng)
-        cur = conv.pack_input(x, P, convs[0].f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
-        rows = bfv.cts_rows(cur.cts).contiguous()
-        cur = conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), cur.layout,
-                                cur.channels, cur.scale)
+        cur = conv.pack_input_private(x, P, convs[0].f_w, sk, rng)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         got = inference.he_forward_online(layers, cur, weights, sk, P, prepared, specs=specs)

@@ -191,6 +191,18 @@ def pack_input(values, params: RingParams, f_w: int, encrypt_fn, batch: bool = F
     return PackedTensor(cts, layout, c, scale)
 
 
+def pack_input_private(values, params: RingParams, f_w: int, sk: bfv.SecretKey, rng, scale: int = 0) -> PackedTensor:
+    """pack_input with encrypt_fn = encrypt_private(·, sk, rng), the encryptions
+    batched (bfv.encrypt_private_rows): bit-identical ciphertexts and RNG
+    consumption, one device pass instead of one per ciphertext; the result is
+    one device-resident stack."""
+    values = np.asarray(values, dtype=np.int64)
+    c, h, w = values.shape
+    layout = layout_direct(params, h, w, f_w)
+    msgs = np.stack([np.asarray(v, dtype=np.int64) for v in pack_vectors(values, layout, params.p)])
+    return PackedTensor(bfv.encrypt_private_rows(msgs, sk, rng), layout, c, scale)
+
+
 def unpack(tensor: PackedTensor, sk: bfv.SecretKey, signed: bool = True) -> np.ndarray:
     """Decrypt (batched on the device) and gather readable slots to (c, H', W')."""
     params = sk.params

@@ -98,12 +98,9 @@ def he_forward(layers, x: np.ndarray, weights: dict, sk: bfv.SecretKey, rng, par
     per_conv = []
     first = seq[0]
     t0 = time.perf_counter()
-    cur = conv.pack_input(x, P, first.f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
-    # the client's ciphertexts as one device stack (seeded c1 halves are host
-    # arrays until uploaded): the upload is the input transfer, not the conv
-    rows = bfv.cts_rows(cur.cts).contiguous()
-    cur = conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), cur.layout,
-                            cur.channels, cur.scale)
+    # the client's encrypted input as one device stack (encryptions batched,
+    # bit-identical to encrypt_private per ciphertext)
+    cur = conv.pack_input_private(x, P, first.f_w, sk, rng)
     torch.cuda.synchronize()
     t["input_s"] = time.perf_counter() - t0
 
@@ -176,12 +173,7 @@ def he_forward_many(layers, xs, weights: dict, sk: bfv.SecretKey, rng, params: R
     per_conv = []
     first = seq[0]
     t0 = time.perf_counter()
-    curs = []
-    for x in xs:
-        c = conv.pack_input(x, P, first.f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
-        rows = bfv.cts_rows(c.cts).contiguous()
-        curs.append(conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), c.layout,
-                                      c.channels, c.scale))
+    curs = [conv.pack_input_private(x, P, first.f_w, sk, rng) for x in xs]
     torch.cuda.synchronize()
     t["input_s"] = time.perf_counter() - t0
 

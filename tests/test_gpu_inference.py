@@ -60,10 +60,7 @@ def test_chain_online_phase_matches(name):
     for _ in range(2):
         x = rng.integers(0, 8, (seq[0].c_i, seq[0].H, seq[0].W), dtype=np.int64)
         prepared = inference.he_prepare(layers, P, sk, rng)
-        cur = conv.pack_input(x, P, seq[0].f_w, lambda pt: bfv.encrypt_private(pt, sk, rng))
-        rows = bfv.cts_rows(cur.cts).contiguous()
-        cur = conv.PackedTensor(bfv.cts_from_rows(rows, P.q, bfv.Encoding.DIRECT, bfv.Domain.COEFF), cur.layout,
-                                cur.channels, cur.scale)
+        cur = conv.pack_input_private(x, P, seq[0].f_w, sk, rng)
         got = inference.he_forward_online(layers, cur, weights, sk, P, prepared, specs=specs)
         assert np.array_equal(got, inference.plain_forward(layers, x, weights, P.p))
 
@@ -82,3 +79,20 @@ def test_deferred_budget_check_raises():
     bad = torch.tensor([1, P.q // (2 * P.p) * 4, 3], dtype=torch.int64, device="cuda")
     with pytest.raises(ProtocolError):
         act2pc.check_deferred_budgets(P, bad)
+
+
+def test_pack_input_private_matches_per_ciphertext_encryption():
+    """conv.pack_input_private (batched encryptions) equals pack_input with
+    encrypt_private per ciphertext on the same rng: identical ciphertexts and
+    the same rng state afterwards."""
+    from paper_2401_16732_b200 import bfv, conv, params
+
+    P = params.default_params()
+    sk = bfv.keygen(P, np.random.default_rng(5))
+    x = np.random.default_rng(6).integers(0, 8, (3, 56, 56), dtype=np.int64)
+    r1, r2 = np.random.default_rng(9), np.random.default_rng(9)
+    a = conv.pack_input(x, P, 7, lambda pt: bfv.encrypt_private(pt, sk, r1))
+    b = conv.pack_input_private(x, P, 7, sk, r2)
+    assert a.layout == b.layout and a.channels == b.channels
+    assert np.array_equal(bfv.cts_rows(a.cts).cpu().numpy(), bfv.cts_rows(b.cts).cpu().numpy())
+    assert r1.integers(0, 1 << 62) == r2.integers(0, 1 << 62)

@@ -191,6 +191,12 @@ int fhe_decrypt_round_max(uint64_t q, uint64_t p, uint64_t delta, int R, int n, 
  * fhe_decrypt_round_max, in one kernel (one CTA per ciphertext); n = 1024, 2048, 4096. */
 int fhe_decrypt_fused(const fhe_plan* plan, int k, int eval, const uint64_t* cts, const uint64_t* s_eval,
                       uint64_t p, uint64_t delta, uint64_t* m_out, uint64_t* max_all, void* stream);
+/* bfv.to_eval + pmult + plain_add of a ciphertext batch in one launch (the layer
+ * exchange's server round 2): ct = DEVICE [k][2][n] in COEFF form, pt / add = DEVICE
+ * [k][n] in EVAL order; out [k][2][n] = NTT(ct) ⊙ pt (+ add on c0). Identical to
+ * fhe_ntt_forward + fhe_ct_pmult_add; n = 1024, 2048, 4096; add may be NULL. */
+int fhe_ntt_pmult_add(const fhe_plan* plan, int k, const uint64_t* ct, const uint64_t* pt, const uint64_t* add,
+                      uint64_t* out, void* stream);
 
 /* ------------------------------------------ K1: Flash convolution core */
 /* Lazy DRot x CMult accumulation with one reduction per coefficient

@@ -66,6 +66,7 @@ SIGNATURES = {
     "fhe_decrypt_round_max": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp]),
     "fhe_decrypt_fused": (_int, [_vp, _int, _int, _vp, _vp, _u64, _u64, _vp, _vp, _vp]),
     "fhe_copy_many": (_int, [_int, _vp, _vp, _vp, _vp]),
+    "fhe_ntt_pmult_add": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp]),
     "fhe_gather_rows": (_int, [_vp, _int, _int, _vp, _vp]),
     "fhe_copy_2d": (_int, [_vp, ctypes.c_size_t, _vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, _vp]),
     "fhe_zero": (_int, [_vp, ctypes.c_size_t, _vp]),

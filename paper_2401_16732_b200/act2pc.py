@@ -431,10 +431,10 @@ class _LayerGraph:
                          self.zeros.data_ptr(), w.contiguous().data_ptr(), plan.idx.data_ptr(), ct_sq.data_ptr(),
                          device.stream())
             ct_w = _encrypt_rows(self.zeros[kd : 2 * kd], _batch_coeffs(_gather(plan.idx_eval, w), params), params)
-            w_eval = ring.ntt_rows(ct_w.reshape(-1, n), n, [params.q])
+            # server: to_eval + pmult(2r') + plain_add(v) in one launch (fhe_ntt_pmult_add)
             m2 = torch.empty_like(ct_w)
-            _native.call("fhe_ct_pmult_add", params.q, kd, n, w_eval.data_ptr(), self.two_r.data_ptr(),
-                         self.v_eval.data_ptr(), m2.data_ptr(), device.stream())
+            _native.call("fhe_ntt_pmult_add", device.native_plan(n, params.q), kd, ct_w.data_ptr(),
+                         self.two_r.data_ptr(), self.v_eval.data_ptr(), m2.data_ptr(), device.stream())
             mm = _decrypt_rows_checked(m2, Domain.EVAL, key, pending)
             evals = ring.ntt_rows(mm, n, [params.p])
             # the client's round-2 message is materialised (it crosses to the server)

@@ -754,6 +754,54 @@ __global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_ROW_MINB((1 << LOGN) 
   if ((item & 31) == 0) atomicMax(max_all, (unsigned long long)local);
 }
 
+// The server's second round of the layer exchange (bfv.to_eval + pmult +
+// plain_add, bfv.py:359-372, 503-512) in one launch: the forward transform of
+// every row of ct [k][2][n] (one CTA per row), then out = NTT(row) ⊙ pt[ct]
+// (+ add[ct] on c0 rows) before the store — the transformed ciphertext is
+// never written. Values identical to fhe_ntt_forward + fhe_ct_pmult_add.
+template <int LOGN, int LOGR>
+__global__ void __launch_bounds__((1 << LOGN) >> LOGR, FHE_ROW_MINB((1 << LOGN) >> LOGR, LOGR))
+    ntt_pmult_add_kernel(const NttDesc d, const uint64_t* __restrict__ ct, const uint64_t* __restrict__ pt,
+                         const uint64_t* __restrict__ add, uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t sm[];
+  constexpr int n = 1 << LOGN, E = 1 << LOGR;
+  constexpr int NPH = RowPhase<LOGN, LOGR, false, 0>::count;
+  const int row = blockIdx.x, item = threadIdx.x;
+  const int c = row >> 1;
+  const bool c0 = (row & 1) == 0;
+  const uint64_t* srow = ct + (size_t)row * n;
+  const uint64_t q = d.m.q, q2 = 2 * q;
+  uint64_t e[E];
+  static_for<0, NPH>([&](auto kc) {
+    constexpr int K = decltype(kc)::value;
+    using Ph = RowPhase<LOGN, LOGR, false, K>;
+    constexpr int TL = Ph::TL;
+    const int B = ((item >> TL) << (TL + LOGR)) + (item & ((1 << TL) - 1));
+    if constexpr (K == 0) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) e[i] = srow[B + (i << TL)];
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) e[i] = sm[spad(B) + (i << TL) + ((i << TL) >> 4)];
+    }
+    phase_math<LOGR, Ph::R, false, TL>(e, d, (uint32_t)(n + B), false);
+    if constexpr (K == NPH - 1) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int pos = B + (i << TL);
+        uint64_t x = e[i] >= q2 ? e[i] - q2 : e[i];
+        x = mulmod(csub(x, q), pt[(size_t)c * n + pos], d.m);
+        if (c0 && add) x = csub(x + add[(size_t)c * n + pos], q);
+        out[(size_t)row * n + pos] = x;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) sm[spad(B) + (i << TL) + ((i << TL) >> 4)] = e[i];
+      __syncthreads();
+    }
+  });
+}
+
 static bool row_direct_enabled() {  // FHE_NTT_ROW_DIRECT=0 selects the staged row kernel (A/B checks)
   static int v = -1;
   if (v < 0) {
@@ -952,6 +1000,31 @@ int fhe_decrypt_fused(const fhe_plan* plan, int k, int eval, const uint64_t* cts
   }
 #undef FHE_DECRYPT_N
   FHE_CHECK_LAUNCH("decrypt_fused_kernel");
+  return FHE_OK;
+}
+
+int fhe_ntt_pmult_add(const fhe_plan* plan, int k, const uint64_t* ct, const uint64_t* pt, const uint64_t* add,
+                      uint64_t* out, void* stream) {
+  if (!plan || !ct || !pt || !out) return fail(FHE_ERR_VALUE, "null ntt-pmult operand");
+  if (k < 0) return fail(FHE_ERR_VALUE, "bad ciphertext count");
+  if (ct == out) return fail(FHE_ERR_VALUE, "ntt-pmult cannot run in place");
+  if (!k) return FHE_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+#define FHE_NTT_PMULT_N(LOGN)                                                                                \
+  case (1 << LOGN): {                                                                                      \
+    const size_t smem = (size_t)((1 << LOGN) + ((1 << LOGN) >> 4) + 1) * sizeof(uint64_t);                 \
+    ntt_pmult_add_kernel<LOGN, 3><<<2 * k, (1 << LOGN) >> 3, smem, st>>>(plan->desc, ct, pt, add, out);    \
+    break;                                                                                                 \
+  }
+  switch (plan->n) {
+    FHE_NTT_PMULT_N(10)
+    FHE_NTT_PMULT_N(11)
+    FHE_NTT_PMULT_N(12)
+    default:
+      return fail(FHE_ERR_PARAMETER, "ntt-pmult supports n = 1024, 2048, 4096 (got %d)", plan->n);
+  }
+#undef FHE_NTT_PMULT_N
+  FHE_CHECK_LAUNCH("ntt_pmult_add_kernel");
   return FHE_OK;
 }
 

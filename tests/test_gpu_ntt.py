@@ -251,3 +251,29 @@ def test_widepoly_vs_eager():
     with pytest.raises(ring.AccumulatorBudgetError):
         for _ in range(3):
             big.accumulate(ModPoly(np.zeros(n), Q), 1 << 31)
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+@pytest.mark.parametrize("with_add", [True, False])
+def test_ntt_pmult_add_fused(n, with_add):
+    """fhe_ntt_pmult_add (forward transform + pmult + plain_add in one launch)
+    equals fhe_ntt_forward followed by fhe_ct_pmult_add."""
+    import torch
+
+    from paper_2401_16732_b200 import _native, device, params, ring
+
+    P = params.make_params(n)
+    q = P.q
+    rng = np.random.default_rng(n + int(with_add))
+    k = 37
+    ct = torch.from_numpy(rng.integers(0, q, (k, 2, n), dtype=np.int64)).cuda()
+    pt = torch.from_numpy(rng.integers(0, q, (k, n), dtype=np.int64)).cuda()
+    add = torch.from_numpy(rng.integers(0, q, (k, n), dtype=np.int64)).cuda() if with_add else None
+    ev = ring.ntt_rows(ct.reshape(-1, n), n, [q]).reshape(k, 2, n)
+    want = torch.empty_like(ct)
+    _native.call("fhe_ct_pmult_add", q, k, n, ev.data_ptr(), pt.data_ptr(), device.ptr(add), want.data_ptr(),
+                 device.stream())
+    got = torch.empty_like(ct)
+    _native.call("fhe_ntt_pmult_add", device.native_plan(n, q), k, ct.data_ptr(), pt.data_ptr(), device.ptr(add),
+                 got.data_ptr(), device.stream())
+    assert torch.equal(got, want)

@@ -465,7 +465,8 @@ def inference_chain_many(name, reqs):
         got = inference.he_forward_many(layers, xs, weights, sk, rng, P, timings=t, specs=specs)
         ok = all(np.array_equal(g, inference.plain_forward(layers, x, weights, P.p)) for x, g in zip(xs, got))
         per_conv = t.pop("per_conv_s")
-        out = {"requests": reqs, "convs": len(convs), "bit_exact_vs_integer_model": ok,
+        out = {"requests": reqs, "convs": len(convs), "residual_blocks": len(inference.blocks(layers)),
+               "bit_exact_vs_integer_model": ok,
                "conv_ms_total": round(t["conv_s"] * 1e3, 2), "conv_ms_per_request": round(t["conv_s"] * 1e3 / reqs, 3),
                "conv_gpu_ms_per_request": round(t["conv_gpu_s"] * 1e3 / reqs, 3),
                "act_ms_per_request": round(t["act_s"] * 1e3 / reqs, 2),
@@ -505,7 +506,8 @@ def inference_chain(name):
                **{k: round(v * 1e3, 2) for k, v in t.items()}}
         out["per_conv_ms"] = [round(v * 1e3, 3) for v in per_conv]
         out = {k.replace("_s", "_ms") if k.endswith("_s") else k: v for k, v in out.items()}
-    out["online_ms"] = round(out["conv_ms"] + out["act_ms"] + out["repack_ms"] + out["tail_ms"], 2)
+    out["online_ms"] = round(out["conv_ms"] + out["act_ms"] + out["repack_ms"] + out["shortcut_ms"] + out["tail_ms"], 2)
+    out["residual_blocks"] = len(inference.blocks(layers))  # shortcuts added before each block's second activation
     # the online phase as a client would see it: offline material prepared up front
     # (inference.he_prepare), then every conv / exchange / repack enqueued back to back
     # with the budget checks deferred (inference.he_forward_online); wall clock from the

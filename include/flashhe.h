@@ -133,6 +133,13 @@ int fhe_poly_scalar_mul(const uint64_t* moduli, int L, int B, int P, int n,
 /* ring.monomial_mul (ring.py:279-299): out = a * x^(-shift) (any shift) */
 int fhe_poly_monomial(const uint64_t* moduli, int L, int B, int P, int n,
                       const uint64_t* a, int64_t shift, uint64_t* out, void* stream);
+/* ResNet shortcut add in the conv output layout (inference chain; the DRot of
+ * ring.monomial_mul, ring.py:279-299, then bfv.hadd, bfv.py:316-320):
+ * out[j] = y[j] + a[j / c_n] * x^(-tile*(j mod c_n)) for j < count, both
+ * polynomials; y, out: [count][2][n], a: [ceil(count/c_n)][2][n] (the packed
+ * block input, c_n channel tiles of `tile` slots per ciphertext). out may be y. */
+int fhe_residual_add(uint64_t q, int count, int c_n, int tile, int n, const uint64_t* y,
+                     const uint64_t* a, uint64_t* out, void* stream);
 /* ring.apply_galois (ring.py:316-334): out = a(x^gpow), gpow odd */
 int fhe_poly_automorphism(const uint64_t* moduli, int L, int B, int P, int n,
                           const uint64_t* a, uint64_t gpow, uint64_t* out, void* stream);

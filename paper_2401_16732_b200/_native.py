@@ -54,6 +54,7 @@ SIGNATURES = {
     "fhe_shoup_companions": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp]),
     "fhe_poly_scalar_mul": (_int, [_vp, _int, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "fhe_poly_monomial": (_int, [_vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp]),
+    "fhe_residual_add": (_int, [_u64, _int, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "fhe_poly_automorphism": (_int, [_vp, _int, _int, _int, _int, _vp, _u64, _vp, _vp]),
     "fhe_poly_add_delta": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp]),
     "fhe_encrypt_combine": (_int, [_u64, _u64, _u64, _int, _int, _vp, _vp, _vp, _vp, _vp]),

@@ -830,6 +830,31 @@ def _bias_plaintext(layout: TileLayout, frag: int, value: int, params: RingParam
 _fc_plans: dict[tuple, tuple] = {}
 
 
+def residual_add(y: PackedTensor, shortcut: PackedTensor, params: RingParams, inplace: bool = True) -> PackedTensor:
+    """ResNet shortcut addition on ciphertexts (addition; the reference has no
+    model module): y, a conv_proposed output (one channel per ciphertext),
+    plus `shortcut` in y's layout. `shortcut` is either another conv output
+    (a projection) or the packed block input itself, whose channel j is moved
+    from tile j mod c_n of ciphertext j / c_n to slot 0 by a DRot
+    (bfv.drot, key-switch-free) and added (bfv.hadd) — one fhe_residual_add
+    launch for the whole tensor. Written into y's rows when `inplace`."""
+    sl = shortcut.layout
+    if y.channels != shortcut.channels or y.layout.stride != 1 or sl.stride != 1:
+        raise EncodingError("residual operands differ in channels or carry a pending stride")
+    if replace(sl, c_n=1) != y.layout:
+        raise EncodingError("shortcut layout does not match the conv output layout")
+    c_n, tile = (1, 0) if sl.fragmented else (sl.c_n, sl.tile)
+    yr, ar = bfv.cts_rows(y.cts).contiguous(), bfv.cts_rows(shortcut.cts).contiguous()
+    count = yr.shape[0]
+    if count != y.layout.ct_count(y.channels) or ar.shape[0] != -(-count // c_n) or ar.shape[0] != len(shortcut.cts):
+        raise EncodingError("residual operands do not match their layouts")
+    out = yr if inplace else torch.empty_like(yr)
+    _native.call("fhe_residual_add", params.q, count, c_n, tile, params.n, yr.data_ptr(), ar.data_ptr(),
+                 out.data_ptr(), device.stream())
+    cts = bfv.cts_from_rows(out, params.q, Encoding.DIRECT, Domain.COEFF)
+    return PackedTensor(cts, y.layout, y.channels, y.scale)
+
+
 def avg_pool(x: PackedTensor, k: int, params: RingParams) -> PackedTensor:
     """k×k sliding sums via DRot taps of weight 1; /k² and the subsample are
     deferred (stride marker), as conv.py:604-623. One separable pass

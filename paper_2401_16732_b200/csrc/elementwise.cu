@@ -187,6 +187,29 @@ __global__ void monomial_kernel(const ModSet ms, RowGeom g, int64_t s, int flip,
   out[idx] = (neg && v) ? ms.m[l].q - v : v;
 }
 
+// ResNet shortcut in the conv output layout (one channel per ciphertext):
+// out[j] = y[j] + a[j / c_n] * x^(-tile*(j mod c_n)) for both polynomials of
+// ciphertext j. The DRot (ring.monomial_mul, ring.py:279-299) moves channel j's
+// tile of the packed block input to slot 0, where conv_proposed writes channel
+// j; c_n = 1 is a plain hadd (bfv.py:316-320). In place on y is allowed.
+__global__ void residual_add_kernel(uint64_t q, int logn, int c_n, int tile,
+                                    const uint64_t* y, const uint64_t* __restrict__ a,
+                                    uint64_t* out, int64_t total) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int n = 1 << logn;
+  const int64_t r = idx >> logn;  // output row: ciphertext j = r / 2, polynomial r % 2
+  const int i = (int)(idx & (n - 1));
+  const int64_t j = r >> 1;
+  int src = i + tile * (int)(j % c_n);
+  const bool neg = src >= n;
+  if (neg) src -= n;
+  uint64_t v = a[(((j / c_n) << 1) + (r & 1)) * n + src];
+  if (neg && v) v = q - v;
+  uint64_t s = y[idx] + v;
+  out[idx] = s >= q ? s - q : s;
+}
+
 // out(x) = a(x^gpow) (ring.apply_galois, ring.py:326-334), scatter form
 __global__ void automorphism_kernel(const ModSet ms, RowGeom g, uint64_t gpow,
                                     const uint64_t* __restrict__ a, uint64_t* __restrict__ out,
@@ -900,6 +923,20 @@ int fhe_poly_monomial(const uint64_t* moduli, int L, int B, int P, int n, const 
   RowGeom g{L, P, log2i(n)};
   monomial_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(ms, g, s, flip, a, out, total);
   FHE_CHECK_LAUNCH("monomial_kernel");
+  return FHE_OK;
+}
+
+int fhe_residual_add(uint64_t q, int count, int c_n, int tile, int n, const uint64_t* y, const uint64_t* a,
+                     uint64_t* out, void* stream) {
+  if (n <= 0 || (n & (n - 1)) || count < 0 || c_n < 1 || tile < 0 || (int64_t)tile * c_n > n)
+    return fail(FHE_ERR_VALUE, "residual_add: bad geometry");
+  if (!q || q >= (1ull << 62)) return fail(FHE_ERR_VALUE, "residual_add: modulus out of range");
+  if (a == out) return fail(FHE_ERR_VALUE, "residual_add: the shortcut cannot alias the output");
+  const int64_t total = (int64_t)count * 2 * n;
+  if (!total) return FHE_OK;
+  residual_add_kernel<<<grid_for(total), kThreads, 0, (cudaStream_t)stream>>>(q, log2i(n), c_n, tile, y, a, out,
+                                                                              total);
+  FHE_CHECK_LAUNCH("residual_add_kernel");
   return FHE_OK;
 }
 

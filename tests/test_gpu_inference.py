@@ -96,3 +96,20 @@ def test_pack_input_private_matches_per_ciphertext_encryption():
     assert a.layout == b.layout and a.channels == b.channels
     assert np.array_equal(bfv.cts_rows(a.cts).cpu().numpy(), bfv.cts_rows(b.cts).cpu().numpy())
     assert r1.integers(0, 1 << 62) == r2.integers(0, 1 << 62)
+
+
+def test_chain_main_path_only_matches():
+    """residual=False keeps the main-path-only chain (no shortcut additions)
+    and equals the integer model without them."""
+    from paper_2401_16732_b200 import bfv, inference, params
+
+    P = params.default_params()
+    rng = np.random.default_rng(4040)
+    layers = inference.config_layers("config3")
+    seq, pool, fc = inference.main_path(layers)
+    weights = inference.random_weights(layers, rng)
+    sk = bfv.keygen(P, rng)
+    x = rng.integers(0, 8, (seq[0].c_i, seq[0].H, seq[0].W), dtype=np.int64)
+    got = inference.he_forward(layers, x, weights, sk, rng, P, residual=False)
+    assert np.array_equal(got, inference.plain_forward(layers, x, weights, P.p, residual=False))
+    assert not np.array_equal(got, inference.plain_forward(layers, x, weights, P.p))

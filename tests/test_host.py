@@ -305,3 +305,43 @@ def test_stream_order_smallest_upload_then_largest_download():
     assert sorted(order) == list(range(len(meta)))
     assert order[:2] == [2, 0] and order[2:] == [1, 3, 4]
     assert conv._stream_order(meta[:2], P) == [0, 1]
+
+
+def test_residual_add_rejects_mismatched_layouts():
+    """conv.residual_add checks the operand layouts before touching the device."""
+    from dataclasses import replace
+
+    from paper_2401_16732_b200 import conv, params
+    from paper_2401_16732_b200.errors import EncodingError
+
+    P = params.default_params()
+    lay = conv.layout_direct(P, 8, 8, 3)
+    y = conv.PackedTensor([], conv._out_layout(lay), 16)
+    for bad in (conv.PackedTensor([], conv.layout_direct(P, 16, 16, 3), 16),  # other resolution
+                conv.PackedTensor([], lay, 8),  # other channel count
+                conv.PackedTensor([], replace(lay, stride=2), 16)):  # stride pending
+        with pytest.raises(EncodingError):
+            conv.residual_add(y, bad, P)
+
+
+def test_blocks_and_residual_integer_model():
+    """The basic-block map of the stacks and the residual integer model: an
+    identity block adds its input, a projection block its strided 1x1 map."""
+    from paper_2401_16732_b200 import inference, stacks
+
+    blk = inference.blocks(stacks.config4())
+    assert blk["s1b1c2"] == ("s1b1c1", None)
+    assert blk["s2b1c2"][1].name == "s2b1proj" and len(blk) == 8
+    p = 65537
+    L = stacks.Layer
+    layers = [L("stem", "conv", 4, 4, 3, 1, 2), L("s1b1c1", "conv", 4, 4, 3, 2, 2), L("s1b1c2", "conv", 4, 4, 3, 2, 2),
+              L("avgpool", "pool", 4, 4, 4, 2, 2), L("fc", "fc", 1, 1, 1, 2, 1)]
+    rng = np.random.default_rng(3)
+    w = inference.random_weights(layers, rng, bound=3)
+    x = rng.integers(0, 4, (1, 4, 4))
+    sq = lambda a: (a * a + a) % p  # noqa: E731
+    a0 = sq(inference._conv_same(x, w["stem"]) % p)
+    a1 = sq(inference._conv_same(a0, w["s1b1c1"]) % p)
+    a2 = sq((inference._conv_same(a1, w["s1b1c2"]) + a0) % p)
+    want = (w["fc"] @ a2.reshape(2, -1).sum(axis=1)) % p
+    assert np.array_equal(inference.plain_forward(layers, x, w, p), want)

@@ -552,15 +552,24 @@ def _stack_order() -> bool:
 # relayout by the 4 relayout warps of every CTA ~0.9 TB/s of digit-plane
 # operand; GEMM bounded by the int8 MMA rate (~4 POPS, 16 ops per 60-bit x
 # 8-bit MAC) or by the epilogue's TMEM reads (32 B per output coefficient,
-# ~9.5 TB/s over the chip), plus ~2 us of per-layer pipeline fill.
+# ~9.5 TB/s over the chip), plus ~2 us of per-layer pipeline fill. A layer's
+# relayout also has a ~4 us latency floor (first loads of a cold input, the
+# completion fences and count): without it Johnson's rule put the small
+# layers first and the GEMM waited on their relayouts (config 5 0.403 ->
+# 0.390 ms, config 4 0.330 -> 0.316 ms with it; tools/order_search.py found
+# no better order by measured local search). Dev knobs: FLASHHE_REL_FILL_US,
+# FLASHHE_REL_TBPS, FLASHHE_GEMM_FILL_US.
 _RELAYOUT_BPS, _MMA_OPS, _TMEM_BPS, _LAYER_FILL_S = 0.9e12, 4.0e15, 9.5e12, 2e-6
+_RELAYOUT_FILL_S = float(_os.environ.get("FLASHHE_REL_FILL_US", "4")) * 1e-6
+_RELAYOUT_BPS = float(_os.environ.get("FLASHHE_REL_TBPS", "0.9")) * 1e12
+_LAYER_FILL_S = float(_os.environ.get("FLASHHE_GEMM_FILL_US", "2")) * 1e-6
 
 
 def _stage_times(plan: "ConvPlan") -> tuple[float, float]:
     tc = plan.tc
     macs = plan.n_out * plan.K * 2 * plan.n
     gemm = max(16 * macs / _MMA_OPS, plan.n_out * 2 * plan.n * 32 / _TMEM_BPS) + _LAYER_FILL_S
-    return tc.x_bytes / _RELAYOUT_BPS, gemm
+    return tc.x_bytes / _RELAYOUT_BPS + _RELAYOUT_FILL_S, gemm
 
 
 def _stack_schedule(items):

@@ -49,6 +49,32 @@ def _peaks():
     return 6650.0, "fallback"
 
 
+def _bf16_peaks():
+    """Driver-measured dense bf16 TF/s (burst, sustained) or None: MEASURED_PEAKS.json holds no
+    int8 entry, so the roofline's own peak is the in-run kind::i8 probe; 2 x bf16 (the nominal
+    int8 : bf16 ratio of the tensor pipe) is reported beside it as a cross-check."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    if "bf16_tflops" not in d:
+        return None
+    return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"]))
+
+
+def _bf16_cross(achieved_tops):
+    b = _bf16_peaks()
+    if not b or not achieved_tops:
+        return {}
+    burst, sustained = b
+    return {"measured_peaks_cross_check": {
+        "bf16_tflops_burst": burst, "bf16_tflops_sustained": sustained,
+        "frac_vs_2x_bf16_burst": round(achieved_tops / (2 * burst), 4),
+        "frac_vs_2x_bf16_sustained": round(achieved_tops / (2 * sustained), 4),
+        "note": "MEASURED_PEAKS.json (driver-written cuBLAS bf16) x 2 = the tensor pipe's nominal int8 rate; "
+                "`frac` above uses the stricter in-run kind::i8 probe"}}
+
+
 # --------------------------------------------------------------- clocks
 
 
@@ -924,7 +950,7 @@ def main():
                          "int_pipe_peak_tmac60_per_s": round(peak_tmac, 3),
                          "stack_vs_int_pipe_peak": round(macs / step_s / 1e12 / peak_tmac, 3),
                          "hbm_achieved_gbs": round(alg_bytes / step_s / 1e9, 1), "hbm_peak_gbs": hbm,
-                         "hbm_peak_source": hbm_kind},
+                         "hbm_peak_source": hbm_kind, **_bf16_cross(achieved_tops)},
             "verified": verified,
             "verification": "after the timed loop: every layer's output of the last timed replay equals the "
                             "integer-pipe K1 kernel (conv_flash_kernel, an independent implementation) on the "

@@ -147,6 +147,22 @@ def call(name: str, *args) -> None:
         check(rc)
 
 
+if os.environ.get("FLASHHE_NVTX") == "1":
+    # profiling aid: every C-ABI call becomes an NVTX range named after its entry
+    # point (ncu --nvtx --nvtx-include "fhe_keyswitch_multi/" selects one family);
+    # off by default so the hot path pays nothing
+    _plain_call = call
+
+    def call(name: str, *args) -> None:  # noqa: F811
+        from torch.cuda import nvtx
+
+        nvtx.range_push(name)
+        try:
+            _plain_call(name, *args)
+        finally:
+            nvtx.range_pop()
+
+
 class ConvTcLayer(ctypes.Structure):
     """struct fhe_conv_tc_layer (include/flashhe.h)."""
 

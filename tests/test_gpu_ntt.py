@@ -102,6 +102,45 @@ def test_config2_batched_limbs(golden, N):
     assert np.array_equal(f[2, 3, 1], O.ntt_fwd(x[2, 3, 1], limbs[3]))
 
 
+@pytest.mark.parametrize("N", [4096, 8192, 16384])
+def test_config2_full_batch_properties(golden, N):
+    """Config 2 at the size bench.py times ([B=64][L=4][P=2][N], one launch;
+    the split two-kernel transform at N >= 8192): size-independent properties
+    over every row — inverse(forward(x)) == x, forward is Z_q-linear, forward of
+    a negacyclic shift x·X is the forward of x times the forward of X — plus
+    sampled rows against the oracle (ring.py:129-162)."""
+    from paper_2401_16732_b200 import ring
+
+    limbs = golden["ntt"]["sweep"][str(N)]["limbs"]
+    B, L, P = 64, len(limbs), 2
+    rng = np.random.default_rng(N + 1)
+    x = np.zeros((B, L, P, N), dtype=np.int64)
+    y = np.zeros_like(x)
+    for l, q in enumerate(limbs):
+        x[:, l] = rng.integers(0, q, (B, P, N), dtype=np.int64)
+        y[:, l] = rng.integers(0, q, (B, P, N), dtype=np.int64)
+    qv = _dev(np.array(limbs, dtype=np.int64)).view(1, L, 1, 1)
+    tx, ty = _dev(x), _dev(y)
+    fx = ring.ntt_rows(tx, N, limbs, P=P)
+    fy = ring.ntt_rows(ty, N, limbs, P=P)
+    assert int(fx.min()) >= 0 and bool((fx < qv).all())
+    assert torch.equal(ring.ntt_rows(fx, N, limbs, inverse=True, P=P), tx)
+    assert torch.equal(ring.ntt_rows((tx + ty) % qv, N, limbs, P=P), (fx + fy) % qv)
+    # x·X: coefficients move up one slot, the top one wraps around negated
+    sh = torch.roll(tx, 1, dims=-1)
+    sh[..., 0] = (qv - sh[..., 0:1]).squeeze(-1) % qv.squeeze(-1)
+    mono = np.zeros((1, L, 1, N), dtype=np.int64)
+    mono[..., 1] = 1
+    fm = ring.ntt_rows(_dev(mono), N, limbs, P=1)  # [1][L][1][N]
+    fsh = ring.ntt_rows(sh, N, limbs, P=P).cpu().numpy()
+    fxh, fmh = fx.cpu().numpy(), fm.cpu().numpy()
+    for l, q in enumerate(limbs):
+        want = (fxh[::16, l].astype(object) * fmh[0, l, 0].astype(object)) % q  # every 16th ciphertext (big ints)
+        assert np.array_equal(fsh[::16, l].astype(object), want), f"limb {l}: shift theorem"
+    for b, l, p in ((0, 0, 0), (63, L - 1, 1), (17, 1, 0)):
+        assert np.array_equal(fxh[b, l, p], O.ntt_fwd(x[b, l, p], limbs[l]))
+
+
 @pytest.mark.parametrize("N", [4096, 16384])
 def test_config2_pmult_add(golden, N):
     from paper_2401_16732_b200 import _native, ring

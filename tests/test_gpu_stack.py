@@ -142,3 +142,28 @@ def test_sync_buffer_shared_by_different_stacks():
         conv.run_tc_stack([(L["plan"].tc, L["dev"], L["out"]) for L in layers], sync=sync)
         torch.cuda.synchronize()
         _compare(layers, refs, "shared counter buffer")
+
+
+@pytest.mark.parametrize("workload", ["config5", "config4"])
+def test_stacked_launch_is_linear_at_full_size(workload):
+    """A size-independent property at BASELINE's full sizes: the conv core is
+    Z_q-linear in the input ciphertexts (conv.py:326-352 is a signed-weight sum
+    of DRot-shifted rows), so without bias
+        K1(a) + K1(b) == K1(a + b)  (mod q)
+    for whole stacks, on every coefficient of every output ciphertext — no
+    oracle involved, every layer geometry of the workload at once."""
+    from paper_2401_16732_b200 import conv
+
+    P, layers = bench.build_stack(workload, seed=77)
+    rng = np.random.default_rng(78)
+    outs = []
+    others = [torch.from_numpy(rng.integers(0, P.q, L["host"].shape, dtype=np.int64)).cuda() for L in layers]
+    sums = [(L["dev"] + b) % P.q for L, b in zip(layers, others)]  # < 2^61: no int64 overflow
+    for inputs in ([L["dev"] for L in layers], others, sums):
+        res = [torch.full_like(L["out"], -1) for L in layers]
+        conv.issue_k1([(L["plan"], x, None, r) for L, x, r in zip(layers, inputs, res)])
+        torch.cuda.synchronize()
+        outs.append(res)
+    for L, ya, yb, ys in zip(layers, *outs):
+        assert int(ys.min()) >= 0 and int(ys.max()) < P.q, f"{L['layer'].name}: output not canonical mod q"
+        assert torch.equal((ya + yb) % P.q, ys), f"{L['layer'].name}: stacked launch is not linear mod q"

@@ -59,7 +59,11 @@ int fhe_record_event(void* event, void* stream);
 /* Timeline instrumentation of the K1-TC pipeline: CTA 0 records clock64() at
  * its pipeline events into dev_buf, which must hold 25 x 4096 uint64 (kinds 0-7:
  * pipeline events, 7 also the tile sequence; 8: per-CTA start/end and relayout
- * completion times; 9-24: per-epilogue-warp events); NULL disables. */
+ * completion times; 9-24: per-epilogue-warp events); NULL disables. The default build
+ * records only the per-CTA start/end stamps (kind 8: globaltimer at [2b], [2b+1],
+ * clock64 at [512+2b], [512+2b+1] for CTA b); the per-event points inside the role
+ * loops need a -DFHE_TC_TRACE=1 build (tools/build_probe.py trace -DFHE_TC_TRACE=1,
+ * loaded with FLASHHE_LIB): they cost instruction-cache space in the hot loops. */
 int fhe_debug_trace(void* dev_buf);
 
 /* Roofline micro-benchmarks (register-resident, no memory traffic):

@@ -4,6 +4,10 @@ Development probe:  python tools/trace_stack.py [--workload config4]
 Prints per layer (cycles from kernel start, CTA 0): relayout warp done with
 the layer, loader sees the layer's X ready, first MMA tile start, last MMA
 commit, last epilogue done.
+
+Needs a trace build of the library (the default build keeps only the per-CTA
+start/end stamps):  python tools/build_probe.py trace -DFHE_TC_TRACE=1, then run
+with FLASHHE_LIB=tools/_lib_trace.so.
 """
 
 import argparse

@@ -1,6 +1,10 @@
 """Timeline of the K1-TC pipeline on one config-4 layer (CTA 0), via fhe_debug_trace.
 
 Development probe:  python tools/trace_tc.py [--layer s4b1c2]
+
+Needs a trace build of the library (the default build keeps only the per-CTA
+start/end stamps):  python tools/build_probe.py trace -DFHE_TC_TRACE=1, then run
+with FLASHHE_LIB=tools/_lib_trace.so.
 """
 
 import argparse

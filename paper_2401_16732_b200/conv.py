@@ -365,6 +365,27 @@ class ConvTcPlan:
         return r, 1
 
     @staticmethod
+    def ilv_for(c_o: int, JB: int, steps, h: int, rep: int) -> list[int] | None:
+        """The merged window offsets of an interleaved layer, or None when the
+        layer keeps stacked groups. With c_o <= 64 half of every 128-row MMA is
+        idle (rep 1) or zero (rep 2). Interleaving the two groups — row 2 o + r
+        = channel o at positions 2 u + r, the window read at stride 2 — makes
+        the taps with equal offset step + r ONE full MMA: the 7 column taps of
+        the 7x7 stem take 8 MMAs per 64 positions instead of 14, a 3x3 layer 12
+        instead of 18, and every TMEM lane quadrant has epilogue work.
+        FLASHHE_TC_ILV = auto (default) | 0."""
+        import os
+
+        if os.environ.get("FLASHHE_TC_ILV", "auto") == "0" or c_o > 64 or rep > 2:
+            return None
+        st = [int(s) for s in steps]
+        merged = sorted(set(st) | {s + 1 for s in st})
+        if len(set(st)) != len(st) or len(merged) >= 2 * len(st) or len(merged) > 64:
+            return None  # repeated steps, nothing to merge (e.g. 1x1), or above the kernel's tap limit
+        stage = -(-(64 + 2 * h) * 256 // 1024) * 1024 + len(merged) * 32 * ConvTcPlan.OC_TILE
+        return merged if 2 * stage <= 218 * 1024 else None
+
+    @staticmethod
     def eligible(weights3d: np.ndarray, q: int, n: int, h: int, taps: int) -> bool:
         c_o, c_i, _ = weights3d.shape
         if n < 64 or n % 64 or taps > 64 or 2 * h >= n:
@@ -399,17 +420,31 @@ class ConvTcPlan:
             chan, self.fstride = np.stack([j * layout.frags, np.zeros_like(j)], 1), 1
         else:
             chan, self.fstride = np.stack([j // layout.c_n, layout.tile * (j % layout.c_n)], 1), 0
-        T = self.taps * self.rep
-        wp = np.zeros((OB * N, JB * 32, T), dtype=np.int8)
-        rows = N // self.rep
-        for r in range(self.rep):  # position group r: rows [r·rows, r·rows + c_o), tap blocks [r·taps, (r+1)·taps)
-            wp[r * rows : r * rows + self.c_o, : self.c_i, r * self.taps : (r + 1) * self.taps] = weights3d
+        merged = self.ilv_for(self.c_o, JB, steps, self.h, self.rep) if self.pos_tile == 32 else None
+        if merged is not None:
+            # Interleaved position groups (csrc/conv_tc.cu LayerDesc.ilv): row 2 o + r computes channel o
+            # at positions 2 u + r, so tap t of group r reads window offset step_t + r — taps of the two
+            # groups with the same offset share one full-height MMA. The C layer sees the merged taps.
+            self.rep, self.tsplit = 2, 2
+            T = len(merged)
+            wp = np.zeros((OB * N, JB * 32, T), dtype=np.int8)
+            for r in range(2):
+                for t, st in enumerate(steps):
+                    wp[r : 2 * self.c_o : 2, : self.c_i, merged.index(int(st) + r)] = weights3d[:, :, t]
+            steps = np.asarray(merged, dtype=np.int64)
+        else:
+            T = self.taps * self.rep
+            wp = np.zeros((OB * N, JB * 32, T), dtype=np.int8)
+            rows = N // self.rep
+            for r in range(self.rep):  # position group r: rows [r·rows, r·rows + c_o), tap blocks [r·taps, (r+1)·taps)
+                wp[r * rows : r * rows + self.c_o, : self.c_i, r * self.taps : (r + 1) * self.taps] = weights3d
+        self.k_taps = len(steps)  # taps as the C layer counts them (merged when interleaved)
         # [ob][jb][tap][g][kh][r][jj] with o = ob*128 + g*8 + r, j = jb*32 + kh*16 + jj
         wp = wp.reshape(OB, N // 8, 8, JB, 2, 16, T).transpose(0, 3, 6, 1, 4, 2, 5)
         dev = device.require_cuda()
         self.w = torch.from_numpy(np.ascontiguousarray(wp)).to(dev)
         self.chan = torch.from_numpy(np.ascontiguousarray(chan, dtype=np.int32)).to(dev)
-        self.steps = (ctypes.c_int32 * self.taps)(*[int(s) for s in steps])
+        self.steps = (ctypes.c_int32 * self.k_taps)(*[int(s) for s in steps])
         self.sync = device.zeros_i64(SYNC_WORDS)  # counters of this plan's own launches
         self._single: dict = {}  # cached one-layer launch arguments per (input, output) buffers
         self.bias, self.mask = bias, mask
@@ -423,7 +458,7 @@ class ConvTcPlan:
         """This layer's entry of a fhe_conv_tc_stack launch."""
         return _native.ConvTcLayer(
             inp.data_ptr(), inp.numel() // (2 * self.n), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
-            self.c_o, self.taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
+            self.c_o, self.k_taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
             device.ptr(self.mask), out.data_ptr(), self.rep, self.tsplit)
 
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:

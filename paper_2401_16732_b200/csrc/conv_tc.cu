@@ -111,6 +111,12 @@ constexpr int kPfAhead = FHE_PF_AHEAD;
 #ifndef FHE_EPI_PIPE
 #define FHE_EPI_PIPE 0  // 1: software-pipelined TMEM loads in the pair epilogue (measured 2.5 % slower on config 5)
 #endif
+#ifndef FHE_ILV_EPI
+#define FHE_ILV_EPI 1  // 0: A/B probe of the interleaved-group epilogue code's cost (interleaved layers then wrong)
+#endif
+#ifndef FHE_ILV_FAST
+#define FHE_ILV_FAST 1  // unrolled MMA issue paths for 8 and 12 merged taps
+#endif
 #ifndef FHE_EPI_SLEEP
 #define FHE_EPI_SLEEP 0
 #endif
@@ -137,6 +143,13 @@ struct LayerDesc {
                            // a stage is just the window (slots follow the weights); loaded once per CTA
   int rep;   // 32-position groups stacked in the 128 accumulator rows (c_o <= 128 / rep): 1, 2 or 4
   int pair;  // 1: plane sums are below 2^31 / 257 (short contraction): the epilogue pairs planes in 32 bits
+  int ilv;   // 1 (rep == 2): the two position groups interleave — accumulator row 2 o + r computes channel o at
+             // positions s0 + 2 u + r, so the taps of both groups that read the same window offset share ONE
+             // full-height MMA (7 column taps -> 8 MMAs per 64 positions instead of 14 half-empty ones; 3x3 ->
+             // 12 instead of 18). X is stored de-interleaved per plane ([even positions | odd positions], Y/2
+             // each) and a window is two bulk copies, so column u of a tap is a plain contiguous read:
+             // tap_off = (e & 1)(32 + h) + (e >> 1) for window offset e — the MMA issue loop sees an
+             // ordinary layer
   int16_t tap_off[kMaxTaps];  // step_t + h
 };
 
@@ -513,7 +526,10 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
   }
   // two rounds of 16 lanes through a 2 KB staging area: 16 positions x 128 B
   const int rows = min(32, d.Y - U.y0);
-  uint4* dst = reinterpret_cast<uint4*>(d.X + (((size_t)U.pf * d.JB + U.jb) * d.Y + U.y0) * 256 + U.kh * 128);
+  // interleaved layers: position y of a plane lives at (y & 1) * Y/2 + (y >> 1) (y0 is even)
+  const int ilv = d.ilv, yh = d.Y >> 1;
+  uint4* dst = reinterpret_cast<uint4*>(d.X + (((size_t)U.pf * d.JB + U.jb) * d.Y + (ilv ? U.y0 >> 1 : U.y0)) * 256 +
+                                        U.kh * 128);
   const uint4* st4 = reinterpret_cast<const uint4*>(stg);
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
@@ -528,8 +544,9 @@ __device__ __forceinline__ void relayout_store(const LayerDesc& d, uint64_t q, i
     for (int i = 0; i < 4; ++i) {
       const int idx = i * 32 + lane, pl = idx >> 3, ch = idx & 7, pos = half * 16 + pl;
       if (pos < rows) {
-        FHE_CHECK((const uint8_t*)(dst + pos * 16 + ch + 1) <= d.X + d.x_bytes);
-        dst[pos * 16 + ch] = st4[pl * 8 + (ch ^ (pl & 7))];
+        const int pd = ilv ? (pos & 1) * yh + (pos >> 1) : pos;
+        FHE_CHECK((const uint8_t*)(dst + pd * 16 + ch + 1) <= d.X + d.x_bytes);
+        dst[pd * 16 + ch] = st4[pl * 8 + (ch ^ (pl & 7))];
       }
     }
     __syncwarp();
@@ -878,6 +895,12 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                 issue_taps<14>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
               } else if (taps == 7) {
                 issue_taps<7>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+#if FHE_ILV_FAST
+              } else if (taps == 8) {  // 7 column taps, two interleaved position groups (the 7x7 stem)
+                issue_taps<8>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+              } else if (taps == 12) {  // 3x3, two interleaved position groups
+                issue_taps<12>(acc, alo, blo, dhi, off16, idesc, jb == 0, wait_next);
+#endif
               } else {
                 for (int tp = 0; tp < taps; ++tp) {
                   if (tp == taps - 1) wait_next();
@@ -962,6 +985,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
           tq_put(tq, sq++, l, t);
           const Tile T = tile_of(t, d, n);
           const uint8_t* xbase = d.X + ((size_t)(T.p * d.F + T.f) * d.JB) * plane_stride + (size_t)T.s0 * 256;
+          const uint8_t* xilv = xbase - (size_t)(T.s0 >> 1) * 256;  // (interleaved: the even half starts at s0 / 2)
           const uint8_t* wbase = d.W + (size_t)T.ob * d.JB * wstage;
           for (int jb = 0; jb < d.JB; ++jb) {  // stage = one 32-channel block
             const int s = s_ld;
@@ -985,7 +1009,13 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                         win_load <= (uint32_t)d.slot_bytes && d.OB == 1 &&
                         xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
                         (size_t)d.res_bytes <= d.w_bytes);
-              bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+              if (d.ilv) {  // even positions, then odd positions (each 32 + h) of the plane
+                bulk_load(sx, xilv + (size_t)jb * plane_stride, win_load >> 1, full_bar(s));
+                bulk_load(sx + (win_load >> 1), xilv + (size_t)jb * plane_stride + (plane_stride >> 1), win_load >> 1,
+                          full_bar(s));
+              } else {
+                bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+              }
               if (res_pending) bulk_load(smem_u32(smem), d.W, (uint32_t)d.res_bytes, full_bar(s));
               res_pending = false;
             } else {
@@ -996,7 +1026,13 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                         d.stage_bytes <= d.slot_bytes &&
                         win_load <= (uint32_t)d.win_bytes && xbase + (size_t)jb * plane_stride + win_load <= d.X + d.x_bytes &&
                         wbase + (size_t)(jb + 1) * wstage <= d.W + d.w_bytes);
-              bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+              if (d.ilv) {
+                bulk_load(sx, xilv + (size_t)jb * plane_stride, win_load >> 1, full_bar(s));
+                bulk_load(sx + (win_load >> 1), xilv + (size_t)jb * plane_stride + (plane_stride >> 1), win_load >> 1,
+                          full_bar(s));
+              } else {
+                bulk_load(sx, xbase + (size_t)jb * plane_stride, win_load, full_bar(s));
+              }
               bulk_load(sx + d.win_bytes, wbase + (size_t)jb * wstage, wstage, full_bar(s));
             }
 #endif
@@ -1045,8 +1081,11 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
         const int c_o = d.c_o, F = d.F, npos = d.npos, nacc = d.nacc, pair = d.pair;
         // rows of the accumulator: rep groups of rows_per output channels, group
         // r holding positions [32 r, 32 r + 32) of the tile
+        // (interleaved groups, d.ilv: row 2 o + r = channel o at positions s0 + 2 u + r)
+        const int ilv = FHE_ILV_EPI ? d.ilv : 0;
         const int rows_per = kOcTile / d.rep;
-        const int grp = (quad * 32 + lane) / rows_per, orow = (quad * 32 + lane) % rows_per;
+        const int grp = ilv ? 0 : (quad * 32 + lane) / rows_per;
+        const int orow = ilv ? (quad * 32 + lane) >> 1 : (quad * 32 + lane) % rows_per;
         uint64_t* const dout = d.out;
         const uint8_t* const bmask = d.bmask;
         const uint64_t* const bias = d.bias;
@@ -1054,7 +1093,7 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
         const int t = (int)(lt & 0xFFFFFFu);
         const Tile T = tile_of(t, d, n);
         const int o = T.ob * kOcTile + orow;
-        const bool active = T.ob * kOcTile + (quad * 32) % rows_per < c_o;  // warp-uniform (rows_per >= 32)
+        const bool active = T.ob * kOcTile + (ilv ? quad * 16 : (quad * 32) % rows_per) < c_o;  // warp-uniform
         const uint64_t bd = (active && T.p == 0 && bias && o < c_o) ? bias[o] : 0;
         for (int a = 0; a < nacc; ++a) {
           int buf;
@@ -1114,8 +1153,22 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
                   r[j] = val >= q ? val - q : val;
                 }
               }
+              int kk = 4 * k;  // the lane's 4 consecutive positions within the tile row
+              if (ilv) {
+                // the lane pair (2 o, 2 o + 1) holds positions 8 k + {0, 2, 4, 6} and 8 k + {1, 3, 5, 7}:
+                // exchange two values each so the even lane stores 8 k .. 8 k + 3, the odd one 8 k + 4 .. + 7
+                const bool odd = lane & 1;
+                const uint64_t g0 = __shfl_xor_sync(0xffffffffu, odd ? r[0] : r[2], 1);
+                const uint64_t g1 = __shfl_xor_sync(0xffffffffu, odd ? r[1] : r[3], 1);
+                if (odd) {
+                  r[0] = g0; r[1] = r[2]; r[2] = g1;
+                } else {
+                  r[2] = r[1]; r[1] = g0; r[3] = g1;
+                }
+                kk = 8 * k + (odd ? 4 : 0);
+              }
               if (bd) {
-                const uint32_t mk = *reinterpret_cast<const uint32_t*>(bmask + (size_t)T.f * n + s0 + 4 * k);
+                const uint32_t mk = *reinterpret_cast<const uint32_t*>(bmask + (size_t)T.f * n + s0 + kk);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                   if ((mk >> (8 * j)) & 0xff) r[j] = csub(r[j] + bd, q);
@@ -1123,10 +1176,10 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
 #ifdef TC_PROBE_NOSTORE  // timing probe only: results reduced but not stored
               if (o < c_o && (r[0] ^ r[1] ^ r[2] ^ r[3]) == 0x5eed5eedull) orow[0] = 1;
 #else
-              FHE_CHECK(o >= c_o || ((uint8_t*)(orow + 4 * k + 4) <= (uint8_t*)dout + d.out_bytes &&
-                                     s0 + 4 * k + 4 <= n));
+              FHE_CHECK(o >= c_o || ((uint8_t*)(orow + kk + 4) <= (uint8_t*)dout + d.out_bytes &&
+                                     s0 + kk + 4 <= n));
               if (o < c_o)  // one 32-byte store per lane: a full sector (STG.256)
-                asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(orow + 4 * k), "l"(r[0]), "l"(r[1]),
+                asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(orow + kk), "l"(r[0]), "l"(r[1]),
                              "l"(r[2]), "l"(r[3])
                              : "memory");
 #endif
@@ -1419,7 +1472,11 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     if (rep != 1 && rep != 2 && rep != 4) return fail(FHE_ERR_VALUE, "tc layer %d: rep must be 1, 2 or 4", l);
     if (rep > 1 && (s.pos_tile != 32 || s.c_o > tc::kOcTile / rep))
       return fail(FHE_ERR_VALUE, "tc layer %d: rep %d needs pos_tile 32 and c_o <= %d", l, rep, tc::kOcTile / rep);
-    if (s.taps * rep > tc::kMaxTaps) return fail(FHE_ERR_VALUE, "tc layer %d: taps x rep above %d", l, tc::kMaxTaps);
+    // rep 2 with tsplit 2: the two position groups interleave (LayerDesc.ilv); taps / tap_steps / w are
+    // then the MERGED taps (distinct window offsets step + r), each one full-height MMA
+    const bool ilv = rep == 2 && s.tsplit == 2;
+    if (!ilv && s.taps * rep > tc::kMaxTaps)
+      return fail(FHE_ERR_VALUE, "tc layer %d: taps x rep above %d", l, tc::kMaxTaps);
     if (127ll * 255 * ((s.c_i + 31) / 32 * 32) * s.taps >= (1ll << 31))
       return fail(FHE_ERR_VALUE, "tc layer %d: plane sums would exceed s32", l);
     d.in = s.in;
@@ -1440,9 +1497,10 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.fstride = s.fstride;
     d.c_o = s.c_o;
     d.OB = (s.c_o + tc::kOcTile - 1) / tc::kOcTile;
-    d.taps = s.taps * rep;  // MMAs per 32-channel block: every tap for every stacked position group
-    if (s.tsplit > 1) return fail(FHE_ERR_VALUE, "tc layer %d: tsplit is reserved (0 or 1)", l);
+    d.taps = ilv ? s.taps : s.taps * rep;  // MMAs per 32-channel block: every tap for every stacked position group
+    if (s.tsplit > 1 && !ilv) return fail(FHE_ERR_VALUE, "tc layer %d: tsplit is 0, 1, or 2 with rep 2", l);
     d.rep = rep;
+    d.ilv = ilv ? 1 : 0;
     // |P_d| <= 127·255·c_i·taps (each accumulator row sums one position group's taps)
     d.pair = 127ll * 255 * 257 * s.c_i * s.taps < (1ll << 31) ? 1 : 0;
     d.h = s.h;
@@ -1454,7 +1512,12 @@ int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl
     d.out_bytes = (size_t)s.c_o * s.frags * 2 * n * 8;
     for (int t = 0; t < s.taps; ++t) {
       const int off = s.tap_steps[t] + s.h;
-      if (off < 0 || off > 2 * s.h) return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
+      if (off < 0 || off > 2 * s.h + (ilv ? 1 : 0))
+        return fail(FHE_ERR_VALUE, "tc layer %d: tap step outside the halo", l);
+      if (ilv) {  // merged taps: column u reads window position 2 u + off = entry u + (off >> 1) of its parity half
+        d.tap_off[t] = (int16_t)((off & 1) * (d.npos + s.h) + (off >> 1));
+        continue;
+      }
       for (int r = 0; r < rep; ++r) d.tap_off[r * s.taps + t] = (int16_t)(off + r * d.npos);  // group r: +32 r
     }
     d.win_bytes = ((d.tpos + 2 * d.h) * 256 + 1023) / 1024 * 1024;

@@ -424,6 +424,58 @@ _EPI_MODULI = {
 }
 
 
+ILV_CASES = [
+    # H, W, f_w, c_i, c_o, bias — layers that take the interleaved position groups (c_o <= 64)
+    (56, 56, 3, 64, 64, True),    # a config-5 s1 layer: fragmented, 2 channel blocks, 12 merged taps, bias
+    (224, 224, 7, 3, 64, True),   # the config-5 stem: row-folded, 8 merged taps, pair epilogue, bias
+    (16, 16, 3, 40, 37, True),    # c_n = 6, c_o not a multiple of 16 (partly active warp), bias
+    (8, 8, 3, 70, 24, False),     # c_n = 20, 3 channel blocks (the last partial), c_o <= 32: two quadrants active
+    (32, 32, 3, 64, 64, False),   # c_n = 1, rep-1 layer before (long contraction)
+]
+
+
+@pytest.mark.parametrize("case", ILV_CASES)
+def test_conv_tc_interleaved_groups(case, monkeypatch):
+    """Layers with c_o <= 64 run two interleaved position groups (LayerDesc.ilv:
+    merged taps, window read at stride 2, lane-pair exchange in the epilogue):
+    equal to the integer-pipe kernel on every coefficient, to the stacked-group
+    launch (FLASHHE_TC_ILV=0) and to the oracle on sampled channels."""
+    from oracle.flash_oracle import add_bias
+    from paper_2401_16732_b200 import conv
+
+    H, W, f_w, c_i, c_o, bias = case
+    P = _P()
+    rng = np.random.default_rng(H * 77 + c_i)
+    lay = conv.layout_direct(P, H, W, f_w)
+    arr = rng.integers(0, Q, (lay.ct_count(c_i), 2, N), dtype=np.int64)
+    arr[:, :, ::19] = Q - 1
+    w = rng.integers(-127, 128, (c_o, c_i, f_w, f_w), dtype=np.int64)
+    b = rng.integers(-5000, 5000, c_o, dtype=np.int64) if bias else None
+
+    def run(path, ilv):
+        monkeypatch.setenv("FLASHHE_CONV_PATH", path)
+        monkeypatch.setenv("FLASHHE_TC_ILV", ilv)
+        spec = conv.ConvLayerSpec(H, W, f_w, c_i, c_o, w, bias=b)  # a fresh plan cache per mode
+        plan = conv.conv_plan(spec, lay, P)
+        assert plan.tc is not None
+        if path == "tc":
+            assert (plan.tc.tsplit == 2) == (ilv == "auto"), "interleaving should follow FLASHHE_TC_ILV"
+        return _out(conv.conv_proposed(conv.PackedTensor(_cts(arr), lay, c_i), spec, P).cts)
+
+    y_ilv = run("tc", "auto")
+    assert np.array_equal(y_ilv, run("int", "auto"))
+    assert np.array_equal(y_ilv, run("tc", "0"))
+    layd = {"n": N, "w_p": lay.w_p, "pad": lay.pad, "tile": lay.tile, "c_n": lay.c_n, "frags": lay.frags}
+    chans = sorted({0, c_o // 2, c_o - 1})
+    ref = O.conv_proposed(arr, w.reshape(c_o, c_i, -1), layd, Q, channels=chans)
+    if b is not None:
+        out_lay = {"n": N, "height": H, "width": W, "pad": lay.pad, "w_p": lay.w_p, "frags": lay.frags,
+                   "frag_len": lay.frag_len, "halo": lay.halo}
+        ref = add_bias(ref, b[chans], O.bias_masks(out_lay), P.delta, P.p, Q)
+    sel = np.concatenate([np.arange(c * lay.frags, (c + 1) * lay.frags) for c in chans])
+    assert np.array_equal(y_ilv[sel], ref)
+
+
 @pytest.mark.parametrize("qname", sorted(_EPI_MODULI))
 @pytest.mark.parametrize("geom", [(8, 3, 64, 130), (16, 1, 64, 96), (32, 7, 3, 16)])
 def test_tc_epilogue_moduli(qname, geom, monkeypatch):

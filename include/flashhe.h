@@ -254,9 +254,14 @@ typedef struct fhe_conv_tc_layer {
                              positions; w then holds taps*rep tap blocks, block r*taps + t
                              carrying tap t's weights in rows [r*128/rep, r*128/rep + c_o)
                              (zero elsewhere) — group r reads the window 32 r positions on */
-  int tsplit;             /* reserved, 0 or 1 (a 32-channel block's MMAs run in one pipeline
-                             stage; layers with one output-channel block keep their weights
-                             resident in shared memory instead) */
+  int tsplit;             /* 0 or 1: nothing. 2 (with rep == 2, c_o <= 64): the two position
+                             groups INTERLEAVE — accumulator row 2 o + r computes channel o at
+                             positions s0 + 2 u + r. taps / tap_steps are then the MERGED taps:
+                             the distinct values of step_t + r (each in [-h, h + 1]), and w holds
+                             one tap block per merged tap with W[o][j][t] in row 2 o + r of the
+                             block of step_t + r (zero elsewhere): taps of the two groups that
+                             read the same window offset share one full-height MMA. X is stored
+                             de-interleaved per plane (even positions, then odd) by the relayout */
 } fhe_conv_tc_layer;
 /* layers: HOST array of nl (<= 24) layers sharing (q, n), 2^56 <= q < 2^62.
  * X: DEVICE scratch. x_stride > 0: 3 operand buffers x_stride bytes apart

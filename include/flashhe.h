@@ -274,9 +274,10 @@ typedef struct fhe_conv_tc_layer {
  *   counter and, per layer, work / relayout-done / GEMM-done / tile counters
  *   (CTAs grab tiles dynamically, the last grab of a launch resets the
  *   layer's tile counter; FHE_TC_DYNAMIC=0 deals them statically). The other
- *   counters only grow (graph-replay safe); reuse one sync buffer only for
- *   stacks with the same number of layers and never for launches that may
- *   run concurrently. */
+ *   counters only grow (graph-replay safe; the GEMM-done counters advance only
+ *   with x_stride > 0 and nl > 3, the one mode that waits on them); reuse one
+ *   sync buffer only for stacks with the same number of layers and the same
+ *   x_stride mode, and never for launches that may run concurrently. */
 int fhe_conv_tc_stack(uint64_t q, int n, const fhe_conv_tc_layer* layers, int nl,
                       uint8_t* X, size_t x_stride, uint64_t* sync, void* stream);
 /* conv.avg_pool (conv.py:604-623): every row (polynomial) of in [rows][n]

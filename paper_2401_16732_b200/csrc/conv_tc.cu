@@ -103,6 +103,9 @@ constexpr int kAccCols = 256;        // TMEM columns per accumulator buffer (npo
 #ifndef FHE_RELAYOUT_STATIC
 #define FHE_RELAYOUT_STATIC 1
 #endif
+#ifndef FHE_GEM_ALWAYS
+#define FHE_GEM_ALWAYS 0  // 1: the per-layer GEMM-done barrier + count in every mode (A/B probe)
+#endif
 #ifndef FHE_REL_TWO
 #define FHE_REL_TWO 0  // static relayout: 1 = two units in flight per warp. 0 (one unit: half the relayout
                        // code in the roles' shared 32 KB instruction cache) measured 2.6 % faster on config 5
@@ -1274,11 +1277,15 @@ __global__ void FHE_STACK_BOUNDS conv_tc_stack_kernel(const __grid_constant__ St
         }
         }
       }
-      // this CTA consumed all of layer l's X (every tile's MMAs completed)
-      asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue));
-      if (tid == 64) {
-        __threadfence();
-        atomicAdd(A.sync + kGem + l, 1ull);
+      // this CTA consumed all of layer l's X (every tile's MMAs completed). Only the rotating-X mode
+      // with more than three layers ever waits for this count; otherwise the epilogue warps move on
+      // to the next layer without meeting at a barrier.
+      if (FHE_GEM_ALWAYS || (A.xrot && nl > 3)) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpilogue));
+        if (tid == 64) {
+          __threadfence();
+          atomicAdd(A.sync + kGem + l, 1ull);
+        }
       }
     }
   }

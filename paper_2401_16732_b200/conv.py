@@ -454,11 +454,15 @@ class ConvTcPlan:
         """Size of the digit-plane operand X: [2][frags][JB][n + 2h][256 B]."""
         return 2 * self.frags * (-(-self.c_i // 32)) * (self.n + 2 * self.h) * 256
 
-    def layer(self, inp: torch.Tensor, out: torch.Tensor) -> "_native.ConvTcLayer":
-        """This layer's entry of a fhe_conv_tc_stack launch."""
+    def layer(self, inp: torch.Tensor, out: torch.Tensor, alone: bool = False) -> "_native.ConvTcLayer":
+        """This layer's entry of a fhe_conv_tc_stack launch. `alone`: the layer is
+        the launch's only one — 64-position tiles (chosen for a stack, where other
+        layers fill the tail) then give way to 32-position ones: twice the tiles
+        over the 148 CTAs (a config-5 s3 layer alone: 128 -> 256 tiles, 41 -> 28 us)."""
+        pos_tile = 32 if alone and self.pos_tile == 64 and _os.environ.get("FLASHHE_TC_POS", "auto") == "auto" else self.pos_tile
         return _native.ConvTcLayer(
             inp.data_ptr(), inp.numel() // (2 * self.n), self.c_i, self.frags, self.fstride, self.chan.data_ptr(), self.h, self.w.data_ptr(),
-            self.c_o, self.k_taps, self.pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
+            self.c_o, self.k_taps, pos_tile, ctypes.cast(self.steps, ctypes.c_void_p), device.ptr(self.bias),
             device.ptr(self.mask), out.data_ptr(), self.rep, self.tsplit)
 
     def run(self, inp: torch.Tensor, out: torch.Tensor, mark=None) -> torch.Tensor:
@@ -474,7 +478,7 @@ class ConvTcPlan:
             if len(self._single) > 16:
                 self._single.clear()
             need = _x_total([self])
-            hit = self._single[key] = ((_native.ConvTcLayer * 1)(self.layer(inp, out)), need)
+            hit = self._single[key] = ((_native.ConvTcLayer * 1)(self.layer(inp, out, alone=True)), need)
         arr, need = hit
         X = device.scratch("conv_tc_x", need)
         rc = _stack_launch(self.q, self.n, arr, 1, X, 0, self.sync.data_ptr(), device.stream())
@@ -517,7 +521,7 @@ def run_tc_stack(jobs, sync: torch.Tensor | None = None) -> None:
     if sync is None:
         sync = _stack_sync_for([tc for tc, *_ in jobs])
     X = device.scratch("conv_tc_x", _x_total([tc for tc, *_ in jobs]))  # every layer its own operand region
-    arr = (_native.ConvTcLayer * len(jobs))(*[tc.layer(inp, out) for tc, inp, out in jobs])
+    arr = (_native.ConvTcLayer * len(jobs))(*[tc.layer(inp, out, alone=len(jobs) == 1) for tc, inp, out in jobs])
     rc = _native.fn("fhe_conv_tc_stack")(tc0.q, tc0.n, arr, len(jobs), X, 0, sync.data_ptr(), device.stream())
     if rc:
         _native.check(rc)
@@ -831,7 +835,7 @@ def conv_proposed_stream(jobs, params: RingParams) -> list[PackedTensor]:
                                   device=comp.device)
             inp.record_stream(comp)
             out = torch.empty((plan.n_out, 2, params.n), dtype=torch.int64, device=comp.device)
-            lay = (_native.ConvTcLayer * 1)(plan.tc.layer(inp, out))
+            lay = (_native.ConvTcLayer * 1)(plan.tc.layer(inp, out, alone=True))
             sync = _stack_sync_for([plan.tc])
             X = device.scratch("conv_tc_x", need)  # already sized: never reallocated here
             rc = fast(params.q, params.n, lay, pin.data_ptr(), pin.numel() * 8, hv.data_ptr(), hv.numel() * 8, X,
